@@ -1,0 +1,8 @@
+"""CPU fp64 oracle for the Falkon hot path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+legs may import this package.  See falkon_oracle.py for the citations and pins.
+"""
+from .falkon_oracle import *  # noqa: F401,F403
+from .falkon_oracle import (GAUSSIAN, LAPLACIAN, DEFAULT_JITTER, NotPositiveDefinite,  # noqa: F401
+                            NonFinite)
