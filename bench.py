@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Benchmark of the Falkon hot path on B200 (contract: see DESIGN.md "Measurement").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config msd] [--impl ours|reference]
+
+One STEP = one fused product  u = sum_ranks Knm_r^T (Knm_r v)  (SURVEY.md §8(a) rows a1-a6:
+prep, cross term, exp, both contractions, deterministic reduction, allreduce) over the
+config's synthetic data, inputs resident in HBM.  metric = n*m kernel evaluations per second
+(whole job, all ranks).  After the timed product steps one full falkon_fit (rows a1-a9, the
+paper's Table 1 split) is timed and reported under "fit".
+
+Multi-GPU: launched by torch.distributed.run; rows of X are sharded (synth.shard_range), C
+and v are replicated, one NCCL allreduce(m) per product; timing is max over ranks.
+`--impl reference` times the CPU oracle (oracle/, fp64 NumPy) on a bounded row sample of
+the same workload on rank 0 (the only other place allowed to execute oracle/).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="msd", choices=list(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-fit", action="store_true", help="skip the full falkon_fit timing")
+    ap.add_argument("--fit-iters", type=int, default=None)
+    ap.add_argument("--path", default="auto", choices=["auto", "simt", "tensor"])
+    ap.add_argument("--n", type=int, default=None, help="override global n (debug)")
+    ap.add_argument("--m", type=int, default=None, help="override m (debug)")
+    ap.add_argument("--oracle-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_rate(cfg, n_global, m, seconds: float, rank_workers: int):
+    """Time the fp64 CPU oracle's Knm^T(Knm v) on a bounded row sample of the workload.
+    Returns (n*m/s, dict)."""
+    import oracle
+    C = synth.gen_C(cfg.seed, n_global, m, cfg.d) if m == cfg.m and n_global == cfg.n else \
+        synth.gen_rows(cfg.seed, synth.STREAM_X, synth.center_indices(cfg.seed, n_global, m), cfg.d)
+    v = synth.gen_vec(cfg.seed, m).astype(np.float64)
+    # calibrate on a small sample, then size the sample to ~`seconds`
+    q = max(1, (1 << 23) // m)
+    n_cal = max(rank_workers * q, 256)
+    Xc = synth.gen_X(cfg.seed, 0, n_cal, cfg.d)
+    t0 = time.perf_counter()
+    oracle.knm_t_knm_vec(Xc, C, v, oracle.GAUSSIAN, cfg.sigma, workers=rank_workers)
+    dt = time.perf_counter() - t0
+    rate = n_cal * m / dt
+    n_s = int(min(n_global, max(n_cal, rate * seconds / m)))
+    Xs = synth.gen_X(cfg.seed, 0, n_s, cfg.d)
+    t0 = time.perf_counter()
+    oracle.knm_t_knm_vec(Xs, C, v, oracle.GAUSSIAN, cfg.sigma, workers=rank_workers)
+    dt = time.perf_counter() - t0
+    return n_s * m / dt, {"rows": n_s, "m": m, "seconds": dt}
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    n_global = args.n or cfg.n
+    m = args.m or cfg.m
+    cores = host_cores()
+    steps_v = []
+    info = None
+    per_step = max(2.0, min(args.oracle_seconds, 60.0 / max(1, args.steps + args.warmup)))
+    for i in range(args.warmup + args.steps):
+        v, info = oracle_rate(cfg, n_global, m, per_step, cores)
+        if i >= args.warmup:
+            steps_v.append((v, info))
+    vals = [s[0] for s in steps_v]
+    value = statistics.median(vals)
+    ms = float(np.median([s[1]["seconds"] for s in steps_v])) * 1e3
+    out = {
+        "impl": "reference", "metric": "fused Knm^T(Knm v) kernel-evals/s", "value": value,
+        "unit": "n*m/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (synth/, seeded; shapes of BASELINE.json configs)",
+        "config": {"workload": cfg.name, "n": n_global, "d": cfg.d, "m": m, "sigma": cfg.sigma,
+                   "kernel": "gaussian"},
+        "cpu_baseline": {"value": value, "unit": "n*m/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{info['rows']} of {n_global} rows x all {m} centers per step "
+                                   f"(fp64 NumPy oracle, {cores} worker processes)"},
+        "e2e": {"value": value, "unit": "n*m/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = synth.CONFIGS[args.config]
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2006_10350_b200 import binding
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [binding.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = binding.Context(device=local, rank=rank, world=world, unique_id=obj[0])
+    else:
+        ctx = binding.Context(device=local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream)
+    ctx.set_option(binding.OPT_PATH, {"auto": 0, "simt": 1, "tensor": 2}[args.path])
+
+    n_global = args.n or cfg.n
+    m = args.m or cfg.m
+    lo, hi = synth.shard_range(n_global, world, rank)
+    n_local = hi - lo
+    # ---- inputs (seeded, synthetic; generated on the host, uploaded once) ----
+    Xh = torch.from_numpy(synth.gen_X(cfg.seed, lo, n_local, cfg.d)).pin_memory()
+    Ch = torch.from_numpy(synth.gen_rows(cfg.seed, synth.STREAM_X,
+                                         synth.center_indices(cfg.seed, n_global, m), cfg.d)
+                          ).pin_memory()
+    vh = torch.from_numpy(synth.gen_vec(cfg.seed, m).astype(np.float64)).pin_memory()
+    X, C, v = Xh.cuda(), Ch.cuda(), vh.cuda()
+    u = torch.zeros(m, dtype=torch.float64, device="cuda")
+    kernel, sigma = binding.GAUSSIAN, cfg.sigma
+
+    def step():
+        ctx.knm_matvec(X, C, v, kernel, sigma, u)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ctx.set_option(binding.OPT_KERNEL_TIMING, 1)
+    ctx.timings(reset=True)
+    l0 = ctx.launch_count()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms_total = e0.elapsed_time(e1)
+    kt = ctx.timings(reset=True)
+    launches = ctx.launch_count() - l0 - kt["allreduce"][1]
+    ctx.set_option(binding.OPT_KERNEL_TIMING, 0)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = n_global * m / (ms_step * 1e-3)
+
+    # ---- roofline of the dominant kernel (device-timed inside the timed region) ----
+    peaks, peak_src = measured_peaks()
+    dom = max(("pass_a", "pass_b"), key=lambda k: kt[k][0])
+    dom_ms = kt[dom][0] / max(1, kt[dom][1])
+    evals = n_local * m  # algorithmic units per launch of either pass (one kernel eval each)
+    f_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    d = cfg.d
+    path = "tensor" if (args.path != "simt" and d > 32) else "simt"
+    if path == "simt":
+        # FP32 pipe: d FMA (cross term) + 1 FADD (bias) + 1 FFMA (contraction) per entry
+        # (Laplacian: 2d); MUFU: 1 ex2 per entry.  Binding pipe = the slower.
+        fp32_peak = sms * 128 * f_hz / (d + 2)
+        mufu_peak = sms * 16 * f_hz
+        peak_evals, pipe = min((fp32_peak, "fp32"), (mufu_peak, "mufu"))
+    else:
+        mufu_peak = sms * 16 * f_hz
+        tc_peak = float(peaks["bf16_tflops"]) * 1e12 / (2.0 * d)  # algorithmic 2d flops/entry
+        peak_evals, pipe = min((tc_peak, "tensor"), (mufu_peak, "mufu"))
+    achieved = evals / (dom_ms * 1e-3)
+    roof = {"bound": "alu" if pipe != "tensor" else "tensor", "pipe": pipe,
+            "kernel": dom, "achieved": achieved / 1e9, "peak": peak_evals / 1e9,
+            "unit": "G kernel-evals/s (one exp-evaluated Knm entry = 2d+5 flops + 1 exp)",
+            "frac": achieved / peak_evals, "traffic": None,
+            "peak_source": f"{peak_src} sm_max_mhz x unit counts (148 SM x 128 FP32 / 16 MUFU "
+                           f"per clk) / bf16 tensor peak",
+            "kernel_ms": dom_ms,
+            "share_of_step": kt[dom][0] / ms_total if ms_total else None}
+
+    # ---- e2e: same metric through the C-ABI with HOST (pinned) buffers ----
+    uh = torch.zeros(m, dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        ctx.knm_matvec(Xh, Ch, vh, kernel, sigma, uh)
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(e2e_steps):
+        ctx.knm_matvec(Xh, Ch, vh, kernel, sigma, uh)
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": n_global * m / e2e_s, "unit": "n*m/s",
+           "h2d_bytes_per_step": int(Xh.numel() * 4 + Ch.numel() * 4 + vh.numel() * 8),
+           "d2h_bytes_per_step": int(uh.numel() * 8)}
+
+    # ---- one full Falkon fit (rows a1-a9) ----
+    fit = None
+    if not args.no_fit:
+        yh = torch.from_numpy(synth.gen_y(cfg.seed, Xh.numpy(), lo, cfg.task))
+        y = yh.cuda()
+        alpha = torch.zeros(m, dtype=torch.float64, device="cuda")
+        iters = args.fit_iters if args.fit_iters is not None else cfg.iters
+        try:
+            barrier()
+            t0 = time.perf_counter()
+            _, info = ctx.fit(X, y, C, kernel, sigma, cfg.lam, iters, alpha)
+            barrier()
+            wall = time.perf_counter() - t0
+            fit = {"seconds": wall, "iters": iters, "t_precond_s": info["t_precond_s"],
+                   "t_rhs_s": info["t_rhs_s"], "t_cg_s": info["t_cg_s"],
+                   "iters_run": info["iters_run"],
+                   "paper_context": "Table 2/4: MSD fit 62 s (2x Titan Xp) / 81 s (1x)"}
+        except Exception as ex:  # report, do not hide
+            fit = {"error": str(ex)}
+
+    cpu = None
+    if rank == 0 and world == 1:
+        rate, inf = oracle_rate(cfg, n_global, m, args.oracle_seconds, host_cores())
+        cpu = {"value": rate, "unit": "n*m/s", "cores": host_cores(), "kind": "oracle",
+               "sample": f"{inf['rows']} of {n_global} rows x all {m} centers, one product, "
+                         f"{inf['seconds']:.1f} s (fp64 NumPy oracle, {host_cores()} worker procs)"}
+
+    if rank == 0:
+        out = {
+            "metric": "fused Knm^T(Knm v) kernel-evals/s", "value": value, "unit": "n*m/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (synth/, seeded; "
+            "X ~ N(0,1) fp32, C = uniform rows of X; shapes of BASELINE.json)",
+            "config": {"workload": cfg.name, "n": n_global, "d": cfg.d, "m": m,
+                       "sigma": cfg.sigma, "kernel": "gaussian", "path": path,
+                       "parallelism": f"rows sharded dp{world}, allreduce(m) per product",
+                       "l2": "inputs larger than L2 (X packed %.0f MB)" % (n_local * cfg.d * 4 / 1e6)},
+            "clocks": clk, "gpu_launches": int(launches), "roofline": roof, "e2e": e2e,
+            "cpu_baseline": cpu, "fit": fit,
+            "kernel_ms": {k: v[0] for k, v in kt.items()},
+        }
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,183 @@
+/*
+ * falkon.h — C ABI of the B200-native Falkon hot path (libfalkon.so).
+ *
+ * What the library computes (PAPER.md = arXiv 2006.10350 text, cited by line):
+ *   - the Nystrom kernel product  u = Knm^T (Knm v)  in row blocks, Knm never stored
+ *     ("Blockwise Knm-vector product"), summed over all ranks;
+ *   - the one-sided products  w = Knm v  and  u = Knm^T w  (Alg. 1 line 9, PAPER.md:114;
+ *     prediction Eq. (4));
+ *   - the Falkon preconditioner  T = chol(Kmm),  A = chol(T T^T / m + lambda I)  in ONE
+ *     m x m fp64 buffer (Alg. 1 lines 13-17; Eq. (7) PAPER.md:254-256;
+ *     in-place layout PAPER.md:257-265 and Fig. 3);
+ *   - Falkon's preconditioned CG (Alg. 1) with LinOp read as
+ *     Eq. (9):  A^-T ( T^-T Knm^T Knm T^-1 A^-1 beta + lambda n A^-1 beta ).
+ *
+ * Kernels (`kernel` argument):
+ *   FALKON_GAUSSIAN   k(x,c) = exp(-||x-c||^2 / (2 sigma^2))
+ *   FALKON_LAPLACIAN  k(x,c) = exp(-||x-c|| / sigma)            (reading c7)
+ *
+ * Conventions (all entry points):
+ *   - Matrices are ROW-MAJOR, contiguous: X is n_local x d, C is m x d (fp32).
+ *   - Pointers may be CUDA device pointers on the context's device OR host pointers
+ *     (pinned or pageable); host inputs are staged into the context workspace, host
+ *     outputs are copied back.  If ANY output pointer is host memory the call
+ *     synchronises the context stream before returning; otherwise the call is
+ *     stream-ordered (asynchronous) on the context stream (see falkon_ctx_set_stream).
+ *     falkon_fit and the preconditioner build always return with results ready.
+ *   - Sizes are int64_t.  Arrays are caller-owned and never retained after return.
+ *   - Multi-GPU: one context per process/GPU.  X, y, f are ROW SHARDS (n_local rows on
+ *     this rank); C, v, u, alpha are REPLICATED.  Every call that produces an m-vector
+ *     sums it over all ranks with one NCCL allreduce; lambda * n uses
+ *     the GLOBAL n = sum of n_local (reading c15).
+ *   - Errors: functions return FALKON_OK (0) or an error code; falkon_strerror() names
+ *     it and falkon_last_error() returns a message with details.  On error, outputs are
+ *     unspecified.  EINVAL is returned for NULL pointers, n_local < 0, d < 1, m < 1,
+ *     sigma <= 0 or non-finite, lambda < 0, iters < 0, unknown kernel.
+ *   - Not re-entrant on one context; different contexts are independent.
+ */
+#ifndef FALKON_H_
+#define FALKON_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct falkon_ctx falkon_ctx;
+
+enum { FALKON_GAUSSIAN = 0, FALKON_LAPLACIAN = 1 };
+
+enum {
+  FALKON_OK = 0,
+  FALKON_EINVAL = 1,     /* invalid argument */
+  FALKON_ENOTPD = 2,     /* Cholesky met a non-positive pivot (see falkon_fit_info) */
+  FALKON_ENONFINITE = 3, /* CG: p^T A p <= 0 or non-finite (reading c9) */
+  FALKON_ENOMEM = 4,     /* device allocation failed */
+  FALKON_ECUDA = 5,      /* CUDA runtime error */
+  FALKON_ENCCL = 6,      /* NCCL error or NCCL library not loadable */
+  FALKON_EUNSUPPORTED = 7 /* no sm_100 device / feature unavailable */
+};
+
+/* Product-path selection (falkon_ctx_set_option FALKON_OPT_PATH). */
+enum { FALKON_PATH_AUTO = 0, FALKON_PATH_SIMT = 1, FALKON_PATH_TENSOR = 2 };
+
+/* Options (falkon_ctx_set_option). */
+enum {
+  FALKON_OPT_PATH = 1,          /* FALKON_PATH_*; AUTO = tensor cores for Gaussian with d > threshold */
+  FALKON_OPT_TC_MIN_D = 2,      /* AUTO threshold on d for the tensor path (default 32) */
+  FALKON_OPT_TC_TERMS = 3,      /* fp16 split terms of the tensor cross term: 1, 2 or 3 (default 3) */
+  FALKON_OPT_KERNEL_TIMING = 4  /* 1: record CUDA events around every launch (falkon_ctx_timings) */
+};
+
+/* Per-launch-class accumulated device times in ms (falkon_ctx_timings). */
+enum {
+  FALKON_T_PREP = 0,      /* a1: centering / scaling / packing / norms */
+  FALKON_T_PASS_A = 1,    /* a2-a4: w = Knm v  (fused cross term + exp + contraction) */
+  FALKON_T_PASS_B = 2,    /* a2,a3,a5: u = Knm^T w */
+  FALKON_T_REDUCE = 3,    /* deterministic fp64 reduction of per-CTA partials */
+  FALKON_T_ALLREDUCE = 4, /* a6: NCCL allreduce(m) */
+  FALKON_T_PRECOND = 5,   /* a9: Kmm, POTRF, LAUUM, POTRF */
+  FALKON_T_TRSV = 6,      /* a7: triangular solves */
+  FALKON_T_VEC = 7,       /* a7: CG vector ops */
+  FALKON_T_COUNT = 8
+};
+
+typedef struct {
+  double jitter_used;      /* delta actually added to diag(Kmm) (reading c6) */
+  int32_t failed_factor;   /* ENOTPD: 0 = T (Kmm), 1 = A (T T^T/m + lambda I); else -1 */
+  int64_t failed_column;   /* ENOTPD: first non-positive pivot column; else -1 */
+  int32_t iters_run;       /* < iters only on exact breakdown r^T r == 0 */
+  int32_t failed_iter;     /* ENONFINITE: CG iteration (1-based); else -1 */
+  double t_precond_s;      /* phase times (Table 1 split), device clock */
+  double t_rhs_s;
+  double t_cg_s;
+  double t_total_s;
+} falkon_fit_info;
+
+/* ---- context ------------------------------------------------------------------------- */
+
+/* NCCL unique id for a multi-rank context.  Call on rank 0, broadcast the 128 bytes to all
+   ranks (e.g. with torch.distributed), then call falkon_ctx_create on every rank. */
+int falkon_get_unique_id(unsigned char id[128]);
+
+/* Create a context on CUDA device `device` for rank `rank` of `world` ranks.  `id` must be
+   NULL iff world == 1.  Requires an sm_100 device (returns FALKON_EUNSUPPORTED otherwise).
+   The context owns a CUDA stream, a device workspace and (world > 1) an NCCL communicator. */
+int falkon_ctx_create(falkon_ctx **out, int device, int rank, int world, const unsigned char *id);
+int falkon_ctx_destroy(falkon_ctx *ctx);
+
+/* Make the context launch on `stream` (a cudaStream_t cast to void*; NULL = the context's
+   own stream).  The caller keeps ownership of the stream. */
+int falkon_ctx_set_stream(falkon_ctx *ctx, void *stream);
+int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value);
+/* Accumulated per-class device times (ms) since the last reset; out has FALKON_T_COUNT
+   entries; launches[] (optional) receives the number of kernel launches per class. */
+int falkon_ctx_timings(falkon_ctx *ctx, double *out_ms, int64_t *launches, int reset);
+/* Total number of kernel launches issued by the library on this context. */
+int64_t falkon_ctx_launch_count(const falkon_ctx *ctx);
+
+/* ---- the hot path ---------------------------------------------------------------------- */
+
+/* u = sum over ranks of Knm_r^T (Knm_r v).
+   X: n_local x d fp32 (row shard).  C: m x d fp32 (replicated).  v: m fp64 (replicated;
+   rounded to fp32 for the contractions).  u: m fp64 (allreduced; identical on all ranks).
+   n_local == 0 is allowed (contributes zero). */
+int falkon_knm_matvec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d,
+                      const float *C, int64_t m, int kernel, double sigma,
+                      const double *v, double *u);
+
+/* w = Knm v on this rank's rows (no collective).  w: n_local fp64. */
+int falkon_kernel_vec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d,
+                      const float *C, int64_t m, int kernel, double sigma,
+                      const double *v, double *w);
+
+/* u = sum over ranks of Knm_r^T w_r  (Alg. 1 line 9 right-hand side).  w: n_local fp64. */
+int falkon_kernel_tvec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d,
+                       const float *C, int64_t m, int kernel, double sigma,
+                       const double *w, double *u);
+
+/* ---- preconditioner (supporting machinery of the CG loop) ------------------------------ */
+
+/* Build the preconditioner into the caller-owned m x m fp64 row-major buffer `P` and the
+   two m-vectors diagT, diagA (Fig. 3):
+     strictly-upper(P) = strictly-upper(T),  diagT = diag(T),   T^T T = Kmm + delta I
+     strictly-lower(P) = strictly-lower(A^T), diagA = diag(A),  A^T A = T T^T/m + lambda I
+   (T, A upper triangular; the diagonal of P is scratch).  delta = jitter (< 0: default
+   1e-8).  Replicated: every rank builds the same bits (no collective).  Returns ENOTPD with
+   info->failed_factor/failed_column set when a pivot is <= 0 or non-finite. */
+int falkon_precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel,
+                         double sigma, double lambda, double jitter,
+                         double *P, double *diagT, double *diagA, falkon_fit_info *info);
+
+/* In-place triangular solve x <- op(F)^-1 x with F = T (which = 0) or A (which = 1) read
+   from a buffer built by falkon_precond_build; op = transpose if trans != 0. x: m fp64. */
+int falkon_precond_solve(falkon_ctx *ctx, const double *P, const double *diagT,
+                         const double *diagA, int64_t m, int which, int trans, double *x);
+
+/* ---- Falkon ---------------------------------------------------------------------------- */
+
+/* alpha = Falkon(X, y, C, kernel, sigma, lambda, iters)  (Alg. 1).
+   y: n_local fp32 targets (row shard).  alpha: m fp64 (replicated).  jitter < 0 -> 1e-8.
+   iters == 0 -> alpha = 0.  info (host, optional) receives phase times and diagnostics.
+   The m x m fp64 buffer (8 m^2 bytes) is allocated for the call and freed at return. */
+int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local, int64_t d,
+               const float *C, int64_t m, int kernel, double sigma, double lambda,
+               int32_t iters, double jitter, double *alpha, falkon_fit_info *info);
+
+/* f = k(X, C) alpha  (Eq. (4)) on this rank's rows; no collective.
+   alpha: m fp64.  f: n_local fp64. */
+int falkon_predict(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d,
+                   const float *C, int64_t m, int kernel, double sigma,
+                   const double *alpha, double *f);
+
+const char *falkon_strerror(int code);
+/* Details of the last error on this thread (static storage, valid until the next call). */
+const char *falkon_last_error(void);
+/* Library build info string (arch, version). */
+const char *falkon_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FALKON_H_ */

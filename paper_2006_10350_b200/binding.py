@@ -1,0 +1,251 @@
+"""Thin ctypes binding of libfalkon.so (include/falkon.h) — argument marshalling only.
+
+Every step of the Falkon hot path runs inside libfalkon's CUDA kernels; this module only
+turns torch tensors / numpy arrays into pointers and sizes, and error codes into
+exceptions.  There is no fallback: if libfalkon.so is missing or cannot be loaded, the
+import-time `load()` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfalkon.so")
+
+GAUSSIAN = 0
+LAPLACIAN = 1
+KERNELS = {"gaussian": GAUSSIAN, "laplacian": LAPLACIAN}
+
+PATH_AUTO, PATH_SIMT, PATH_TENSOR = 0, 1, 2
+OPT_PATH, OPT_TC_MIN_D, OPT_TC_TERMS, OPT_KERNEL_TIMING = 1, 2, 3, 4
+TIMING_NAMES = ["prep", "pass_a", "pass_b", "reduce", "allreduce", "precond", "trsv", "vec"]
+
+ERRORS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ENONFINITE", 4: "ENOMEM", 5: "ECUDA",
+          6: "ENCCL", 7: "EUNSUPPORTED"}
+
+# Every symbol include/falkon.h declares (checked by tests/test_abi.py).
+EXPORTS = ["falkon_get_unique_id", "falkon_ctx_create", "falkon_ctx_destroy",
+           "falkon_ctx_set_stream", "falkon_ctx_set_option", "falkon_ctx_timings",
+           "falkon_ctx_launch_count", "falkon_knm_matvec", "falkon_kernel_vec",
+           "falkon_kernel_tvec", "falkon_precond_build", "falkon_precond_solve", "falkon_fit",
+           "falkon_predict", "falkon_strerror", "falkon_last_error", "falkon_version"]
+
+
+class FalkonError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class FitInfo(ctypes.Structure):
+    _fields_ = [("jitter_used", ctypes.c_double), ("failed_factor", ctypes.c_int32),
+                ("failed_column", ctypes.c_int64), ("iters_run", ctypes.c_int32),
+                ("failed_iter", ctypes.c_int32), ("t_precond_s", ctypes.c_double),
+                ("t_rhs_s", ctypes.c_double), ("t_cg_s", ctypes.c_double),
+                ("t_total_s", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_LIB = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libfalkon.so (built by paper_2006_10350_b200.build) and declare signatures."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not found: run `python -m paper_2006_10350_b200.build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    P, I64, I32, D, C = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
+                         ctypes.c_int)
+    sig = {
+        "falkon_get_unique_id": (C, [P]),
+        "falkon_ctx_create": (C, [ctypes.POINTER(P), C, C, C, P]),
+        "falkon_ctx_destroy": (C, [P]),
+        "falkon_ctx_set_stream": (C, [P, P]),
+        "falkon_ctx_set_option": (C, [P, C, I64]),
+        "falkon_ctx_timings": (C, [P, P, P, C]),
+        "falkon_ctx_launch_count": (I64, [P]),
+        "falkon_knm_matvec": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
+        "falkon_kernel_vec": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
+        "falkon_kernel_tvec": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
+        "falkon_precond_build": (C, [P, P, I64, I64, C, D, D, D, P, P, P, P]),
+        "falkon_precond_solve": (C, [P, P, P, P, I64, C, C, P]),
+        "falkon_fit": (C, [P, P, P, I64, I64, P, I64, C, D, D, I32, D, P, P]),
+        "falkon_predict": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
+        "falkon_strerror": (ctypes.c_char_p, [C]),
+        "falkon_last_error": (ctypes.c_char_p, []),
+        "falkon_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = L
+    return L
+
+
+def _check(code: int):
+    if code != 0:
+        msg = _LIB.falkon_last_error()
+        raise FalkonError(code, msg.decode() if msg else "")
+
+
+def _ptr(a, dtype: str, name: str):
+    """(pointer, numel) of a contiguous torch tensor or numpy array of the given dtype."""
+    if a is None:
+        return None, 0
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.dtype(dtype) or not a.flags["C_CONTIGUOUS"]:
+            raise TypeError(f"{name}: expected C-contiguous numpy {dtype}, got {a.dtype}")
+        return a.ctypes.data, a.size
+    import torch
+    if isinstance(a, torch.Tensor):
+        tdt = {"float32": torch.float32, "float64": torch.float64}[dtype]
+        if a.dtype != tdt or not a.is_contiguous():
+            raise TypeError(f"{name}: expected contiguous torch {dtype}, got {a.dtype}")
+        return a.data_ptr(), a.numel()
+    raise TypeError(f"{name}: expected torch.Tensor or numpy.ndarray, got {type(a)}")
+
+
+def _kernel_id(kernel) -> int:
+    return KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
+
+
+def get_unique_id() -> bytes:
+    load()
+    buf = (ctypes.c_ubyte * 128)()
+    _check(_LIB.falkon_get_unique_id(buf))
+    return bytes(buf)
+
+
+class Context:
+    """One libfalkon context (one GPU, one rank)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1,
+                 unique_id: Optional[bytes] = None):
+        load()
+        h = ctypes.c_void_p()
+        uid = None
+        if unique_id is not None:
+            uid = (ctypes.c_ubyte * 128).from_buffer_copy(unique_id)
+        _check(_LIB.falkon_ctx_create(ctypes.byref(h), device, rank, world, uid))
+        self.h = h
+        self.device, self.rank, self.world = device, rank, world
+
+    def close(self):
+        if self.h:
+            _LIB.falkon_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- configuration
+    def set_stream(self, stream=None):
+        """stream: torch.cuda.Stream, raw cudaStream_t int, or None (own stream)."""
+        if stream is not None and not isinstance(stream, int):
+            stream = stream.cuda_stream
+        _check(_LIB.falkon_ctx_set_stream(self.h, stream))
+
+    def set_option(self, option: int, value: int):
+        _check(_LIB.falkon_ctx_set_option(self.h, option, int(value)))
+
+    def timings(self, reset: bool = False) -> dict:
+        ms = (ctypes.c_double * len(TIMING_NAMES))()
+        ln = (ctypes.c_int64 * len(TIMING_NAMES))()
+        _check(_LIB.falkon_ctx_timings(self.h, ms, ln, int(reset)))
+        return {n: (ms[i], ln[i]) for i, n in enumerate(TIMING_NAMES)}
+
+    def launch_count(self) -> int:
+        return int(_LIB.falkon_ctx_launch_count(self.h))
+
+    # -- hot path
+    @staticmethod
+    def _xc(X, C):
+        px, nx = _ptr(X, "float32", "X")
+        pc, nc = _ptr(C, "float32", "C")
+        n, d = X.shape
+        m = C.shape[0]
+        if C.shape[1] != d:
+            raise ValueError("X and C must have the same number of columns")
+        return px, n, d, pc, m
+
+    def knm_matvec(self, X, C, v, kernel, sigma, out):
+        """out[m] (fp64) = sum over ranks Knm^T (Knm v)."""
+        px, n, d, pc, m = self._xc(X, C)
+        pv, _ = _ptr(v, "float64", "v")
+        pu, _ = _ptr(out, "float64", "out")
+        _check(_LIB.falkon_knm_matvec(self.h, px, n, d, pc, m, _kernel_id(kernel), float(sigma),
+                                      pv, pu))
+        return out
+
+    def kernel_vec(self, X, C, v, kernel, sigma, out):
+        px, n, d, pc, m = self._xc(X, C)
+        pv, _ = _ptr(v, "float64", "v")
+        pw, _ = _ptr(out, "float64", "out")
+        _check(_LIB.falkon_kernel_vec(self.h, px, n, d, pc, m, _kernel_id(kernel), float(sigma),
+                                      pv, pw))
+        return out
+
+    def kernel_tvec(self, X, C, w, kernel, sigma, out):
+        px, n, d, pc, m = self._xc(X, C)
+        pw, _ = _ptr(w, "float64", "w")
+        pu, _ = _ptr(out, "float64", "out")
+        _check(_LIB.falkon_kernel_tvec(self.h, px, n, d, pc, m, _kernel_id(kernel), float(sigma),
+                                       pw, pu))
+        return out
+
+    def precond_build(self, C, kernel, sigma, lam, jitter, P, diagT, diagA) -> dict:
+        pc, _ = _ptr(C, "float32", "C")
+        m, d = C.shape
+        info = FitInfo()
+        code = _LIB.falkon_precond_build(self.h, pc, m, d, _kernel_id(kernel), float(sigma),
+                                         float(lam), float(jitter), _ptr(P, "float64", "P")[0],
+                                         _ptr(diagT, "float64", "diagT")[0],
+                                         _ptr(diagA, "float64", "diagA")[0], ctypes.byref(info))
+        if code != 0:
+            e = FalkonError(code, (_LIB.falkon_last_error() or b"").decode())
+            e.info = info.as_dict()
+            raise e
+        return info.as_dict()
+
+    def precond_solve(self, P, diagT, diagA, which: int, trans: bool, x):
+        m = x.shape[0]
+        _check(_LIB.falkon_precond_solve(self.h, _ptr(P, "float64", "P")[0],
+                                         _ptr(diagT, "float64", "diagT")[0],
+                                         _ptr(diagA, "float64", "diagA")[0], m, int(which),
+                                         int(bool(trans)), _ptr(x, "float64", "x")[0]))
+        return x
+
+    def fit(self, X, y, C, kernel, sigma, lam, iters, alpha, jitter: float = -1.0):
+        px, n, d, pc, m = self._xc(X, C)
+        py, _ = _ptr(y, "float32", "y")
+        pa, _ = _ptr(alpha, "float64", "alpha")
+        info = FitInfo()
+        code = _LIB.falkon_fit(self.h, px, py, n, d, pc, m, _kernel_id(kernel), float(sigma),
+                               float(lam), int(iters), float(jitter), pa, ctypes.byref(info))
+        if code != 0:
+            e = FalkonError(code, (_LIB.falkon_last_error() or b"").decode())
+            e.info = info.as_dict()
+            raise e
+        return alpha, info.as_dict()
+
+    def predict(self, X, C, alpha, kernel, sigma, out):
+        px, n, d, pc, m = self._xc(X, C)
+        pa, _ = _ptr(alpha, "float64", "alpha")
+        pf, _ = _ptr(out, "float64", "out")
+        _check(_LIB.falkon_predict(self.h, px, n, d, pc, m, _kernel_id(kernel), float(sigma),
+                                   pa, pf))
+        return out

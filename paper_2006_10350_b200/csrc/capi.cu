@@ -1,0 +1,611 @@
+// capi.cu — the extern "C" boundary of libfalkon (include/falkon.h) and the device-side
+// Falkon driver: RHS, conjugate gradient with LinOp (Alg. 1; Eq. (9)
+// PAPER.md:269), final alpha, prediction (Eq. (4)).
+//
+// Every step of the path runs in this library's kernels on the context stream.  The CG
+// loop never synchronises with the host: scalars (rho, gamma) live in device memory, the
+// breakdown tests of reading c9 are evaluated on the device, and the host reads the
+// diagnostics once at the end of the fit.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+
+#include "common.cuh"
+
+using namespace falkon;
+
+namespace falkon {
+const char *last_error_cstr();
+
+// ------------------------------------------------------------------ argument checks
+static int check_common(falkon_ctx *ctx, int64_t n, int64_t d, int64_t m, int kernel,
+                        double sigma) {
+  if (!ctx) return fail(FALKON_EINVAL, "ctx is NULL");
+  if (n < 0) return fail(FALKON_EINVAL, "n_local < 0");
+  if (d < 1) return fail(FALKON_EINVAL, "d < 1");
+  if (m < 1) return fail(FALKON_EINVAL, "m < 1");
+  if (kernel != FALKON_GAUSSIAN && kernel != FALKON_LAPLACIAN)
+    return fail(FALKON_EINVAL, "unknown kernel " + std::to_string(kernel));
+  if (!(sigma > 0.0) || !std::isfinite(sigma)) return fail(FALKON_EINVAL, "sigma must be > 0 and finite");
+  FK_CUDA(cudaSetDevice(ctx->device));
+  return FALKON_OK;
+}
+
+// Device view of a caller array: device pointers pass through; host arrays are staged.
+static int stage_in(falkon_ctx *ctx, int slot, const void *p, size_t bytes, const void **out) {
+  if (bytes == 0 || is_device_ptr(p)) {
+    *out = p;
+    return FALKON_OK;
+  }
+  void *w;
+  FK_TRY(ws_get(ctx, slot, bytes, &w));
+  FK_CUDA(cudaMemcpyAsync(w, p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  *out = w;
+  return FALKON_OK;
+}
+
+// ------------------------------------------------------------------ fp64 vector kernels
+constexpr int VT = 256;
+constexpr int DOT_BLOCKS = 256;
+
+// deterministic two-stage dot product: partials[b] then out = sum_b partials[b] (fixed order)
+__global__ void dot_partial_kernel(const double *__restrict__ a, const double *__restrict__ b,
+                                   int64_t n, double *__restrict__ part) {
+  __shared__ double s[VT];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * VT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VT)
+    acc = fma(a[i], b[i], acc);
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = VT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+}
+__global__ void dot_final_kernel(const double *__restrict__ part, int nb, double *__restrict__ out) {
+  __shared__ double s[DOT_BLOCKS];
+  s[threadIdx.x] = threadIdx.x < nb ? part[threadIdx.x] : 0.0;
+  __syncthreads();
+  for (int o = DOT_BLOCKS / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+// CG scalar slots
+enum { S_RHO = 0, S_RHO_NEW, S_GAMMA, S_STOP, S_ITERS, S_FAIL, S_NSLOTS };
+
+__global__ void cg_init_kernel(double *sc) {
+  // called after rho = r.r has been written to sc[S_RHO]
+  sc[S_STOP] = (sc[S_RHO] == 0.0) ? 1.0 : 0.0;  // reading c9: r^T r == 0 -> no iteration
+  sc[S_ITERS] = 0.0;
+  sc[S_FAIL] = -1.0;
+}
+
+// x += a p ; r -= a q  with a = rho / gamma; breakdown -> stop + record iteration
+__global__ void cg_xr_kernel(double *__restrict__ x, double *__restrict__ r,
+                             const double *__restrict__ p, const double *__restrict__ q, int64_t m,
+                             double *sc, int it) {
+  const double stop = sc[S_STOP];
+  if (stop != 0.0) return;
+  const double gamma = sc[S_GAMMA], rho = sc[S_RHO];
+  if (!(gamma > 0.0) || !isfinite(gamma)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc[S_FAIL] = it;
+    return;
+  }
+  const double a = rho / gamma;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(a, p[i], x[i]);
+    r[i] = fma(-a, q[i], r[i]);
+  }
+}
+// After rho_new = r.r: p = r + (rho_new/rho) p ; rho = rho_new ; handle stop/fail flags.
+// Runs as a single-CTA kernel followed by the vector update, so the flags are consistent.
+__global__ void cg_flags_kernel(double *sc, int it) {
+  if (sc[S_STOP] != 0.0) return;
+  if (sc[S_FAIL] >= 0.0) {
+    sc[S_STOP] = 2.0;
+    return;
+  }
+  const double rn = sc[S_RHO_NEW];
+  if (!isfinite(rn)) {
+    sc[S_FAIL] = it;
+    sc[S_STOP] = 2.0;
+    return;
+  }
+  sc[S_ITERS] = it;
+  sc[S_GAMMA] = rn / sc[S_RHO];  // beta, stored in the gamma slot for cg_p_kernel
+  sc[S_RHO] = rn;
+  if (rn == 0.0) sc[S_STOP] = 3.0;  // exact convergence: x is final (reading c9)
+}
+__global__ void cg_p_kernel(double *__restrict__ p, const double *__restrict__ r, int64_t m,
+                            const double *sc) {
+  if (sc[S_STOP] == 2.0) return;
+  if (sc[S_STOP] == 1.0) return;
+  const double beta = sc[S_GAMMA];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], r[i]);
+}
+// y += s x
+__global__ void axpy_kernel(double *__restrict__ y, const double *__restrict__ x, double s,
+                            int64_t m) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(s, x[i], y[i]);
+}
+
+static unsigned vgrid(int64_t m) { return (unsigned)std::min<int64_t>(cdiv<int64_t>(m, VT), 2048); }
+
+static int dot(falkon_ctx *ctx, const double *a, const double *b, int64_t m, double *part,
+               double *out) {
+  const int nb = (int)std::min<int64_t>(DOT_BLOCKS, std::max<int64_t>(1, cdiv<int64_t>(m, VT)));
+  LaunchScope ls(ctx, FALKON_T_VEC);
+  dot_partial_kernel<<<nb, VT, 0, ctx->stream>>>(a, b, m, part);
+  dot_final_kernel<<<1, DOT_BLOCKS, 0, ctx->stream>>>(part, nb, out);
+  ctx->launches++;
+  FK_LAUNCH_CHECK();
+  return FALKON_OK;
+}
+
+// ------------------------------------------------------------------ product pieces
+struct Fit {
+  Prepared pp;
+  float *v32 = nullptr;   // m_pad
+  float *w32 = nullptr;   // n_pad
+};
+
+static int product(falkon_ctx *ctx, Fit &F, const double *v, double *u) {
+  const int64_t m = F.pp.m;
+  FK_TRY(f64_to_f32(ctx, v, F.v32, m, round_up<int64_t>(m, 128)));
+  FK_TRY(pass_A(ctx, F.pp, F.v32, nullptr, F.w32));
+  FK_TRY(pass_B(ctx, F.pp, F.w32, u));
+  return nccl_allreduce_f64(ctx, u, m);
+}
+
+static int alloc_fit_vectors(falkon_ctx *ctx, Fit &F) {
+  void *a, *b;
+  FK_TRY(ws_get(ctx, WS_V32, sizeof(float) * round_up<int64_t>(F.pp.m, 128), &a));
+  FK_TRY(ws_get(ctx, WS_W32, sizeof(float) * round_up<int64_t>(std::max<int64_t>(F.pp.n, 1), 128), &b));
+  F.v32 = (float *)a;
+  F.w32 = (float *)b;
+  return FALKON_OK;
+}
+
+}  // namespace falkon
+
+#define BRK_CUDA(call)                                                              \
+  {                                                                                 \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      rc = fail(FALKON_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+      break;                                                                        \
+    }                                                                               \
+  }
+
+// ==================================================================== extern "C"
+extern "C" {
+
+const char *falkon_strerror(int code) {
+  switch (code) {
+    case FALKON_OK: return "ok";
+    case FALKON_EINVAL: return "invalid argument";
+    case FALKON_ENOTPD: return "matrix not positive definite (Cholesky pivot <= 0)";
+    case FALKON_ENONFINITE: return "non-finite value or non-positive curvature in CG";
+    case FALKON_ENOMEM: return "device out of memory";
+    case FALKON_ECUDA: return "CUDA error";
+    case FALKON_ENCCL: return "NCCL error";
+    case FALKON_EUNSUPPORTED: return "unsupported device or feature";
+    default: return "unknown error";
+  }
+}
+
+const char *falkon_last_error(void) { return falkon::last_error_cstr(); }
+
+const char *falkon_version(void) {
+  return "libfalkon 0.1 (sm_100a; fused SIMT FP32/MUFU + tcgen05 kernel-matvec, fp64 preconditioner)";
+}
+
+int falkon_get_unique_id(unsigned char id[128]) {
+  if (!id) return fail(FALKON_EINVAL, "id is NULL");
+  return nccl_get_unique_id(id);
+}
+
+int falkon_ctx_create(falkon_ctx **out, int device, int rank, int world, const unsigned char *id) {
+  if (!out) return fail(FALKON_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return fail(FALKON_EINVAL, "bad rank/world");
+  if ((world == 1) != (id == nullptr)) return fail(FALKON_EINVAL, "id must be NULL iff world == 1");
+  int ndev = 0;
+  FK_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(FALKON_EINVAL, "bad device ordinal");
+  cudaDeviceProp prop;
+  FK_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(FALKON_EUNSUPPORTED, std::string("libfalkon is built for sm_100a only; device is ") +
+                                         prop.name + " sm_" + std::to_string(prop.major) +
+                                         std::to_string(prop.minor));
+  FK_CUDA(cudaSetDevice(device));
+  falkon_ctx *c = new falkon_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  c->sm_count = prop.multiProcessorCount;
+  c->cc_major = prop.major;
+  c->cc_minor = prop.minor;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(FALKON_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+  }
+  c->stream = c->own_stream;
+  if (world > 1) {
+    int r = nccl_comm_init(c, id);
+    if (r != FALKON_OK) {
+      cudaStreamDestroy(c->own_stream);
+      delete c;
+      return r;
+    }
+  }
+  *out = c;
+  return FALKON_OK;
+}
+
+int falkon_ctx_destroy(falkon_ctx *ctx) {
+  if (!ctx) return FALKON_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  nccl_comm_destroy(ctx);
+  for (int i = 0; i < WS_COUNT; ++i)
+    if (ctx->ws[i]) cudaFree(ctx->ws[i]);
+  for (auto &e : ctx->pending) {
+    cudaEventDestroy(e.start);
+    cudaEventDestroy(e.stop);
+  }
+  for (auto &e : ctx->free_events) {
+    cudaEventDestroy(e.start);
+    cudaEventDestroy(e.stop);
+  }
+  cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return FALKON_OK;
+}
+
+int falkon_ctx_set_stream(falkon_ctx *ctx, void *stream) {
+  if (!ctx) return fail(FALKON_EINVAL, "ctx is NULL");
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  return FALKON_OK;
+}
+
+int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
+  if (!ctx) return fail(FALKON_EINVAL, "ctx is NULL");
+  switch (option) {
+    case FALKON_OPT_PATH:
+      if (value < 0 || value > 2) return fail(FALKON_EINVAL, "bad path");
+      ctx->opt.path = (int)value;
+      return FALKON_OK;
+    case FALKON_OPT_TC_MIN_D:
+      if (value < 1) return fail(FALKON_EINVAL, "bad tc_min_d");
+      ctx->opt.tc_min_d = (int)value;
+      return FALKON_OK;
+    case FALKON_OPT_TC_TERMS:
+      if (value < 1 || value > 3) return fail(FALKON_EINVAL, "tc_terms must be 1, 2 or 3");
+      ctx->opt.tc_terms = (int)value;
+      return FALKON_OK;
+    case FALKON_OPT_KERNEL_TIMING:
+      ctx->opt.kernel_timing = value ? 1 : 0;
+      return FALKON_OK;
+    default:
+      return fail(FALKON_EINVAL, "unknown option");
+  }
+}
+
+int falkon_ctx_timings(falkon_ctx *ctx, double *out_ms, int64_t *launches, int reset) {
+  if (!ctx) return fail(FALKON_EINVAL, "ctx is NULL");
+  FK_TRY(resolve_timings(ctx));
+  for (int i = 0; i < FALKON_T_COUNT; ++i) {
+    if (out_ms) out_ms[i] = ctx->t_ms[i];
+    if (launches) launches[i] = ctx->t_launches[i];
+    if (reset) {
+      ctx->t_ms[i] = 0.0;
+      ctx->t_launches[i] = 0;
+    }
+  }
+  return FALKON_OK;
+}
+
+int64_t falkon_ctx_launch_count(const falkon_ctx *ctx) { return ctx ? ctx->launches : -1; }
+
+// ------------------------------------------------------------------ products
+static int matvec_common(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const float *C,
+                         int64_t m, int kernel, double sigma, Fit &F) {
+  const void *Xd, *Cd;
+  FK_TRY(stage_in(ctx, WS_STAGE_X, X, sizeof(float) * n * d, &Xd));
+  FK_TRY(stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd));
+  FK_TRY(prepare_operands(ctx, (const float *)Xd, n, d, (const float *)Cd, m, kernel, sigma, &F.pp));
+  return alloc_fit_vectors(ctx, F);
+}
+
+int falkon_knm_matvec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d, const float *C,
+                      int64_t m, int kernel, double sigma, const double *v, double *u) {
+  FK_TRY(check_common(ctx, n_local, d, m, kernel, sigma));
+  if ((!X && n_local > 0) || !C || !v || !u) return fail(FALKON_EINVAL, "NULL array");
+  Fit F;
+  FK_TRY(matvec_common(ctx, X, n_local, d, C, m, kernel, sigma, F));
+  const void *vd;
+  FK_TRY(stage_in(ctx, WS_STAGE_V, v, sizeof(double) * m, &vd));
+  const bool host_out = !is_device_ptr(u);
+  double *ud = u;
+  if (host_out) {
+    void *w;
+    FK_TRY(ws_get(ctx, WS_STAGE_OUT, sizeof(double) * m, &w));
+    ud = (double *)w;
+  }
+  FK_TRY(product(ctx, F, (const double *)vd, ud));
+  if (host_out) {
+    FK_CUDA(cudaMemcpyAsync(u, ud, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return FALKON_OK;
+}
+
+int falkon_kernel_vec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d, const float *C,
+                      int64_t m, int kernel, double sigma, const double *v, double *w) {
+  FK_TRY(check_common(ctx, n_local, d, m, kernel, sigma));
+  if ((!X && n_local > 0) || !C || !v || (!w && n_local > 0)) return fail(FALKON_EINVAL, "NULL array");
+  if (n_local == 0) return FALKON_OK;
+  Fit F;
+  FK_TRY(matvec_common(ctx, X, n_local, d, C, m, kernel, sigma, F));
+  const void *vd;
+  FK_TRY(stage_in(ctx, WS_STAGE_V, v, sizeof(double) * m, &vd));
+  const bool host_out = !is_device_ptr(w);
+  double *wd = w;
+  if (host_out) {
+    void *p;
+    FK_TRY(ws_get(ctx, WS_STAGE_OUT, sizeof(double) * n_local, &p));
+    wd = (double *)p;
+  }
+  FK_TRY(f64_to_f32(ctx, (const double *)vd, F.v32, m, round_up<int64_t>(m, 128)));
+  FK_TRY(pass_A(ctx, F.pp, F.v32, wd, nullptr));
+  if (host_out) {
+    FK_CUDA(cudaMemcpyAsync(w, wd, sizeof(double) * n_local, cudaMemcpyDeviceToHost, ctx->stream));
+    FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return FALKON_OK;
+}
+
+int falkon_kernel_tvec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d, const float *C,
+                       int64_t m, int kernel, double sigma, const double *w, double *u) {
+  FK_TRY(check_common(ctx, n_local, d, m, kernel, sigma));
+  if ((!X && n_local > 0) || !C || (!w && n_local > 0) || !u) return fail(FALKON_EINVAL, "NULL array");
+  Fit F;
+  FK_TRY(matvec_common(ctx, X, n_local, d, C, m, kernel, sigma, F));
+  const bool host_out = !is_device_ptr(u);
+  double *ud = u;
+  if (host_out) {
+    void *p;
+    FK_TRY(ws_get(ctx, WS_STAGE_OUT, sizeof(double) * m, &p));
+    ud = (double *)p;
+  }
+  if (n_local > 0) {
+    const void *wd;
+    FK_TRY(stage_in(ctx, WS_STAGE_V, w, sizeof(double) * n_local, &wd));
+    FK_TRY(f64_to_f32(ctx, (const double *)wd, F.w32, n_local, round_up<int64_t>(n_local, 128)));
+  }
+  FK_TRY(pass_B(ctx, F.pp, F.w32, ud));
+  FK_TRY(nccl_allreduce_f64(ctx, ud, m));
+  if (host_out) {
+    FK_CUDA(cudaMemcpyAsync(u, ud, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return FALKON_OK;
+}
+
+int falkon_predict(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d, const float *C,
+                   int64_t m, int kernel, double sigma, const double *alpha, double *f) {
+  return falkon_kernel_vec(ctx, X, n_local, d, C, m, kernel, sigma, alpha, f);
+}
+
+// ------------------------------------------------------------------ preconditioner API
+int falkon_precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel,
+                         double sigma, double lambda, double jitter, double *P, double *diagT,
+                         double *diagA, falkon_fit_info *info) {
+  FK_TRY(check_common(ctx, 0, d, m, kernel, sigma));
+  if (!C || !P || !diagT || !diagA) return fail(FALKON_EINVAL, "NULL array");
+  if (!(lambda >= 0.0) || !std::isfinite(lambda)) return fail(FALKON_EINVAL, "lambda must be >= 0");
+  if (!is_device_ptr(P) || !is_device_ptr(diagT) || !is_device_ptr(diagA))
+    return fail(FALKON_EINVAL, "P, diagT, diagA must be device memory");
+  if (jitter < 0) jitter = 1e-8;
+  const void *Cd;
+  FK_TRY(stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd));
+  return precond_build(ctx, (const float *)Cd, m, d, kernel, sigma, lambda, jitter, P, diagT, diagA,
+                       info);
+}
+
+int falkon_precond_solve(falkon_ctx *ctx, const double *P, const double *diagT, const double *diagA,
+                         int64_t m, int which, int trans, double *x) {
+  if (!ctx || !P || !diagT || !diagA || !x || m < 1 || (which != 0 && which != 1))
+    return fail(FALKON_EINVAL, "bad arguments");
+  FK_CUDA(cudaSetDevice(ctx->device));
+  return trsv(ctx, P, which == 0 ? diagT : diagA, m, which, trans, x);
+}
+
+// ------------------------------------------------------------------ Falkon fit
+int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local, int64_t d,
+               const float *C, int64_t m, int kernel, double sigma, double lambda, int32_t iters,
+               double jitter, double *alpha, falkon_fit_info *info) {
+  FK_TRY(check_common(ctx, n_local, d, m, kernel, sigma));
+  if ((!X && n_local > 0) || (!y && n_local > 0) || !C || !alpha) return fail(FALKON_EINVAL, "NULL array");
+  if (!(lambda >= 0.0) || !std::isfinite(lambda)) return fail(FALKON_EINVAL, "lambda must be >= 0");
+  if (iters < 0) return fail(FALKON_EINVAL, "iters < 0");
+  if (jitter < 0) jitter = 1e-8;
+  falkon_fit_info loc;
+  memset(&loc, 0, sizeof(loc));
+  loc.failed_factor = -1;
+  loc.failed_column = -1;
+  loc.failed_iter = -1;
+  loc.jitter_used = jitter;
+  auto t_start = std::chrono::steady_clock::now();
+
+  const bool host_out = !is_device_ptr(alpha);
+  // global n (reading c15)
+  int64_t n_global = n_local;
+  if (ctx->world > 1) {
+    void *p;
+    FK_TRY(ws_get(ctx, WS_SCALARS, 64, &p));
+    FK_CUDA(cudaMemcpyAsync(p, &n_global, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    FK_TRY(nccl_allreduce_i64(ctx, (int64_t *)p, 1));
+    FK_CUDA(cudaMemcpyAsync(&n_global, p, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+
+  // CG vectors: x r p q t1 t2 u (+ alpha staging) and scalars
+  void *cgv, *scal;
+  FK_TRY(ws_get(ctx, WS_CG, sizeof(double) * m * 8, &cgv));
+  FK_TRY(ws_get(ctx, WS_CG2, sizeof(double) * (S_NSLOTS + DOT_BLOCKS + 8), &scal));
+  double *x = (double *)cgv, *r = x + m, *p = r + m, *q = p + m, *t1 = q + m, *t2 = t1 + m,
+         *u = t2 + m, *ares = u + m;
+  double *sc = (double *)scal, *dpart = sc + S_NSLOTS + 4;
+
+  if (iters == 0) {
+    FK_CUDA(cudaMemsetAsync(ares, 0, sizeof(double) * m, ctx->stream));
+  }
+
+  cudaEvent_t ev[4];
+  for (auto &e : ev) FK_CUDA(cudaEventCreate(&e));
+  FK_CUDA(cudaEventRecord(ev[0], ctx->stream));
+
+  // (1) preconditioner: one m x m fp64 buffer for this fit
+  double *P = nullptr, *dT = nullptr;
+  int rc = FALKON_OK;
+  if (iters > 0) {
+    cudaError_t e = cudaMalloc(&P, sizeof(double) * (size_t)m * (size_t)m);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      for (auto &ee : ev) cudaEventDestroy(ee);
+      return fail(FALKON_ENOMEM, "preconditioner buffer of " + std::to_string(8.0 * m * m / 1e9) +
+                                     " GB: " + cudaGetErrorString(e));
+    }
+    e = cudaMalloc(&dT, sizeof(double) * 2 * (size_t)m);
+    if (e != cudaSuccess) {
+      cudaFree(P);
+      for (auto &ee : ev) cudaEventDestroy(ee);
+      return fail(FALKON_ENOMEM, "diag vectors");
+    }
+  }
+  double *dA = dT ? dT + m : nullptr;
+  auto cleanup = [&]() {
+    if (P) cudaFree(P);
+    if (dT) cudaFree(dT);
+    for (auto &ee : ev) cudaEventDestroy(ee);
+  };
+  Fit F;
+  do {
+    if (iters == 0) break;
+    const void *Xd, *yd, *Cd;
+    if ((rc = stage_in(ctx, WS_STAGE_X, X, sizeof(float) * n_local * d, &Xd))) break;
+    if ((rc = stage_in(ctx, WS_STAGE_Y, y, sizeof(float) * n_local, &yd))) break;
+    if ((rc = stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd))) break;
+    if ((rc = precond_build(ctx, (const float *)Cd, m, d, kernel, sigma, lambda, jitter, P, dT, dA,
+                            &loc)))
+      break;
+    cudaEventRecord(ev[1], ctx->stream);
+    // (2) RHS  R = A^-T T^-T Knm^T y   (Alg. 1 line 9)
+    if ((rc = prepare_operands(ctx, (const float *)Xd, n_local, d, (const float *)Cd, m, kernel,
+                               sigma, &F.pp)))
+      break;
+    if ((rc = alloc_fit_vectors(ctx, F))) break;
+    if (n_local > 0) {
+      if ((rc = f32_to_f32_pad(ctx, (const float *)yd, F.w32, n_local,
+                               round_up<int64_t>(n_local, 128))))
+        break;
+    }
+    if ((rc = pass_B(ctx, F.pp, F.w32, r))) break;
+    if ((rc = nccl_allreduce_f64(ctx, r, m))) break;
+    if ((rc = trsv(ctx, P, dT, m, 0, 1, r))) break;  // T^-T
+    if ((rc = trsv(ctx, P, dA, m, 1, 1, r))) break;  // A^-T
+    cudaEventRecord(ev[2], ctx->stream);
+    // (3) CG  (Alg. 1 line 10; reading c9)
+    BRK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * m, ctx->stream));
+    BRK_CUDA(cudaMemcpyAsync(p, r, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+    if ((rc = dot(ctx, r, r, m, dpart, sc + S_RHO))) break;
+    {
+      LaunchScope ls(ctx, FALKON_T_VEC);
+      cg_init_kernel<<<1, 1, 0, ctx->stream>>>(sc);
+    }
+    const double lam_n = lambda * (double)n_global;
+    for (int it = 1; it <= iters && rc == FALKON_OK; ++it) {
+      // LinOp(p) = A^-T ( T^-T Knm^T Knm T^-1 A^-1 p + lambda n A^-1 p )   (Eq. (9))
+      BRK_CUDA(cudaMemcpyAsync(t1, p, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+      if ((rc = trsv(ctx, P, dA, m, 1, 0, t1))) break;  // t1 = A^-1 p
+      BRK_CUDA(cudaMemcpyAsync(t2, t1, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+      if ((rc = trsv(ctx, P, dT, m, 0, 0, t2))) break;  // t2 = T^-1 t1
+      if ((rc = product(ctx, F, t2, u))) break;          // u = Knm^T Knm t2 (allreduced)
+      if ((rc = trsv(ctx, P, dT, m, 0, 1, u))) break;   // u = T^-T u
+      {
+        LaunchScope ls(ctx, FALKON_T_VEC);
+        axpy_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(u, t1, lam_n, m);
+      }
+      if ((rc = trsv(ctx, P, dA, m, 1, 1, u))) break;   // q = A^-T u
+      double *qv = u;
+      if ((rc = dot(ctx, p, qv, m, dpart, sc + S_GAMMA))) break;
+      {
+        LaunchScope ls(ctx, FALKON_T_VEC);
+        cg_xr_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(x, r, p, qv, m, sc, it);
+      }
+      if ((rc = dot(ctx, r, r, m, dpart, sc + S_RHO_NEW))) break;
+      {
+        LaunchScope ls(ctx, FALKON_T_VEC);
+        cg_flags_kernel<<<1, 1, 0, ctx->stream>>>(sc, it);
+        cg_p_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(p, r, m, sc);
+        ctx->launches++;
+      }
+      FK_LAUNCH_CHECK();
+    }
+    if (rc) break;
+    cudaEventRecord(ev[3], ctx->stream);
+    // (4) alpha = T^-1 A^-1 x   (Alg. 1 line 11)
+    BRK_CUDA(cudaMemcpyAsync(ares, x, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+    if ((rc = trsv(ctx, P, dA, m, 1, 0, ares))) break;
+    if ((rc = trsv(ctx, P, dT, m, 0, 0, ares))) break;
+  } while (0);
+  if (rc != FALKON_OK) {
+    if (info) *info = loc;
+    cudaStreamSynchronize(ctx->stream);
+    cleanup();
+    return rc;
+  }
+  if (host_out)
+    FK_CUDA(cudaMemcpyAsync(alpha, ares, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
+  else
+    FK_CUDA(cudaMemcpyAsync(alpha, ares, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+  double hs[S_NSLOTS] = {};
+  if (iters > 0)
+    FK_CUDA(cudaMemcpyAsync(hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+  FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  auto t_end = std::chrono::steady_clock::now();
+  loc.t_total_s = std::chrono::duration<double>(t_end - t_start).count();
+  if (iters > 0) {
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    loc.t_precond_s = a * 1e-3;
+    loc.t_rhs_s = b * 1e-3;
+    loc.t_cg_s = c * 1e-3;
+    loc.iters_run = (int32_t)hs[S_ITERS];
+    loc.failed_iter = (int32_t)hs[S_FAIL];
+  }
+  cleanup();
+  if (info) *info = loc;
+  if (loc.failed_iter >= 0)
+    return fail(FALKON_ENONFINITE, "CG breakdown at iteration " + std::to_string(loc.failed_iter));
+  return FALKON_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,224 @@
+// common.cuh — internal definitions of libfalkon (context, workspace, errors, PTX helpers).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "falkon.h"
+
+namespace falkon {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+
+#define FK_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return ::falkon::fail(e_ == cudaErrorMemoryAllocation ? FALKON_ENOMEM : FALKON_ECUDA, \
+                            std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+#define FK_TRY(call)                 \
+  do {                               \
+    int r_ = (call);                 \
+    if (r_ != FALKON_OK) return r_;  \
+  } while (0)
+
+#define FK_LAUNCH_CHECK() FK_CUDA(cudaGetLastError())
+
+// ------------------------------------------------------------------ context
+enum WsSlot {
+  WS_CMEAN = 0,   // fp64 d: centering shift mu (mean of C)
+  WS_CMEAN_PART,  // fp64 partial column sums
+  WS_CP,          // packed centers (fp32 SIMT layout or fp16 split layout)
+  WS_CB,          // fp32 m: center biases b_j
+  WS_XP,          // packed rows
+  WS_XA,          // fp32 n: row biases a_i
+  WS_V32,         // fp32 m: v rounded
+  WS_W32,         // fp32 n: w rounded (pass B input)
+  WS_W64,         // fp64 n: w
+  WS_PART,        // fp64 partials
+  WS_U64,         // fp64 m scratch
+  WS_STAGE_X,     // staging of host inputs
+  WS_STAGE_C,
+  WS_STAGE_V,
+  WS_STAGE_OUT,
+  WS_STAGE_Y,
+  WS_CG,          // fp64 CG vectors
+  WS_FLAGS,       // int flags / counters
+  WS_SCALARS,     // fp64 scalars (dots)
+  WS_TMAP,        // TMA descriptors (device copies)
+  WS_PW,          // fp64 NB x NB inverse of the current diagonal block
+  WS_CG2,         // fp64 CG scalars
+  WS_COUNT
+};
+
+struct TimedEvent {
+  cudaEvent_t start, stop;
+  int cls;
+};
+
+struct Options {
+  int path = FALKON_PATH_AUTO;
+  int tc_min_d = 32;
+  int tc_terms = 3;
+  int kernel_timing = 0;
+};
+
+}  // namespace falkon
+
+struct falkon_ctx {
+  int device = 0, rank = 0, world = 1;
+  int sm_count = 148;
+  int cc_major = 10, cc_minor = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  void *nccl_comm = nullptr;
+  void *ws[falkon::WS_COUNT] = {};
+  size_t ws_bytes[falkon::WS_COUNT] = {};
+  falkon::Options opt;
+  // timing
+  std::vector<falkon::TimedEvent> pending;
+  std::vector<falkon::TimedEvent> free_events;
+  double t_ms[FALKON_T_COUNT] = {};
+  int64_t t_launches[FALKON_T_COUNT] = {};
+  int64_t launches = 0;
+};
+
+namespace falkon {
+
+// Grow-only workspace slot (contents undefined after growth).  Sizes are rounded up to
+// 256 B and a 256 B tail is always available so vector/bulk loads may overrun slightly.
+int ws_get(falkon_ctx *ctx, int slot, size_t bytes, void **out);
+
+// Launch accounting + optional CUDA-event timing around a launch.
+struct LaunchScope {
+  falkon_ctx *ctx;
+  int cls;
+  TimedEvent ev{};
+  bool timed = false;
+  LaunchScope(falkon_ctx *c, int cls_);
+  ~LaunchScope();
+};
+
+int resolve_timings(falkon_ctx *ctx);
+
+// pointer kind
+bool is_device_ptr(const void *p);
+
+// NCCL (dlopen'ed)
+int nccl_get_unique_id(unsigned char id[128]);
+int nccl_comm_init(falkon_ctx *ctx, const unsigned char *id);
+int nccl_comm_destroy(falkon_ctx *ctx);
+int nccl_allreduce_f64(falkon_ctx *ctx, double *buf, int64_t count);
+int nccl_allreduce_i64(falkon_ctx *ctx, int64_t *buf, int64_t count);
+
+// ------------------------------------------------------------------ product path (kvp.cu)
+struct Prepared {
+  // packed operands of one product call (owned by ctx workspace)
+  int64_t n = 0, m = 0, d = 0;
+  int kernel = 0;
+  int path = FALKON_PATH_SIMT;
+  int dq = 0;          // packed row stride (elements)
+  const void *Xp = nullptr;
+  const float *xa = nullptr;
+  const void *Cp = nullptr;
+  const float *cb = nullptr;
+};
+
+int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const float *C,
+                     int64_t m, int kernel, double sigma, Prepared *pp);
+// w = Knm z  (pass A).  z: fp32 m (device).  w64 (n, optional) and/or w32 (n, optional).
+int pass_A(falkon_ctx *ctx, const Prepared &pp, const float *z, double *w64, float *w32);
+// u = Knm^T w (pass B) on this rank (no collective).  w: fp32 n (padded).  u: fp64 m.
+int pass_B(falkon_ctx *ctx, const Prepared &pp, const float *w, double *u);
+int f64_to_f32(falkon_ctx *ctx, const double *src, float *dst, int64_t n, int64_t n_pad);
+int f32_to_f32_pad(falkon_ctx *ctx, const float *src, float *dst, int64_t n, int64_t n_pad);
+
+// tensor path (kvp_tc.cu)
+bool tc_supported(const falkon_ctx *ctx, int kernel, int64_t d);
+int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const float *C, int64_t m,
+               double sigma, const double *mu, Prepared *pp);
+int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, double *out64,
+            float *out32);
+
+// ------------------------------------------------------------------ preconditioner (precond.cu)
+int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel, double sigma,
+                  double lambda, double jitter, double *P, double *diagT, double *diagA,
+                  falkon_fit_info *info);
+// x <- op(F)^-1 x, F = T (which 0) or A (which 1)
+int trsv(falkon_ctx *ctx, const double *P, const double *diag, int64_t m, int which, int trans,
+         double *x);
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  while (!mbar_try_wait(bar, phase)) {
+  }
+}
+// 1-D bulk copy global -> shared (TMA engine, SASS UBLKCP), completes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t lmax(int64_t a, int64_t b) { return a > b ? a : b; }
+
+template <typename T>
+__host__ __device__ constexpr T cdiv(T a, T b) {
+  return (a + b - 1) / b;
+}
+template <typename T>
+__host__ __device__ constexpr T round_up(T a, T b) {
+  return cdiv(a, b) * b;
+}
+
+}  // namespace falkon

@@ -1,0 +1,550 @@
+// kvp.cu — fused kernel-vector products on the FP32 FMA + MUFU pipes (small d) and the
+// operand preparation shared by both product paths.
+//
+// The product u = Knm^T (Knm v) is evaluated block-wise without storing Knm
+// (PAPER.md:271-275).  Both passes are instances of ONE fused primitive
+//
+//     out[p] = sum_{q in Q} k(P_p, Q_q) z_q          ("kvp": kernel-vector product)
+//
+//   pass A (a2-a4):  P = rows of X, Q = centers C, z = v   -> w = Knm v
+//   pass B (a2,a3,a5): P = centers C, Q = rows of X, z = w  -> u = Knm^T w
+//
+// A CTA owns 128*R points of P and keeps their coordinates in registers; Q is streamed
+// through shared memory in tiles of TQ points by the TMA engine (1-D cp.async.bulk into a
+// 2-stage mbarrier ring).  Per (p, q) the cross term, the exp2 (MUFU) and the contraction
+// are fused in registers; the contraction over q is an in-thread reduction (no atomics).
+// fp32 partial sums are flushed into fp64 once per tile (<= TQ terms).
+// When P alone cannot fill the GPU the Q range is split across CTAs (blockIdx.y) and the
+// fp64 partials are reduced in a fixed order (deterministic, bitwise-reproducible).
+//
+// Gaussian, norm expansion with centred, pre-scaled inputs:
+//     x~ = (x - mu) * sqrt(log2 e)/sigma,  a_i = -||x~_i||^2/2,  b_j = -||c~_j||^2/2
+//     k(x_i, c_j) = exp2( min(a_i + b_j + x~_i . c~_j, 0) )        (clamp: reading c8)
+// Laplacian (reading c7), direct differences (never the expansion):
+//     x^ = (x - mu) * log2 e / sigma,   k = exp2( -sqrt(sum_k (x^_k - c^_k)^2) )
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace falkon {
+
+constexpr int KVP_THREADS = 128;
+constexpr int KVP_TQ = 128;             // streamed Q points per tile (small-d kernel)
+constexpr int KVP_TQ_G = 32;            // streamed Q points per tile (generic kernel)
+constexpr double LOG2E = 1.4426950408889634;
+
+// ------------------------------------------------------------------ centring shift mu = mean(C)
+// Gaussian and Laplacian kernels are translation invariant; centring shrinks the norms
+// and thus the cancellation of the norm expansion.
+__global__ void colsum_partial_kernel(const float *__restrict__ C, int64_t m, int64_t d,
+                                      int64_t rows_per_block, double *__restrict__ part) {
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r1 = min(m, r0 + rows_per_block);
+  for (int64_t k = threadIdx.x; k < d; k += blockDim.x) {
+    double s = 0.0;
+    for (int64_t r = r0; r < r1; ++r) s += (double)C[r * d + k];
+    part[(int64_t)blockIdx.x * d + k] = s;
+  }
+}
+
+__global__ void colsum_final_kernel(const double *__restrict__ part, int nblk, int64_t d,
+                                    int64_t m, double *__restrict__ mu) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= d) return;
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * d + k];
+  mu[k] = s / (double)m;
+}
+
+int center_mean(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, double **mu_out) {
+  const int64_t rpb = 64;
+  const int nblk = (int)cdiv<int64_t>(m, rpb);
+  void *part, *mu;
+  FK_TRY(ws_get(ctx, WS_CMEAN_PART, sizeof(double) * nblk * d, &part));
+  FK_TRY(ws_get(ctx, WS_CMEAN, sizeof(double) * d, &mu));
+  {
+    LaunchScope ls(ctx, FALKON_T_PREP);
+    colsum_partial_kernel<<<nblk, 128, 0, ctx->stream>>>(C, m, d, rpb, (double *)part);
+  }
+  FK_LAUNCH_CHECK();
+  {
+    LaunchScope ls(ctx, FALKON_T_PREP);
+    colsum_final_kernel<<<(unsigned)cdiv<int64_t>(d, 128), 128, 0, ctx->stream>>>(
+        (const double *)part, nblk, d, m, (double *)mu);
+  }
+  FK_LAUNCH_CHECK();
+  *mu_out = (double *)mu;
+  return FALKON_OK;
+}
+
+// ------------------------------------------------------------------ packing (SIMT layout)
+// One warp per row: out[r, k] = (in[r, k] - mu[k]) * g  (k < d), 0 for d <= k < dq;
+// bias[r] = -0.5 * ||out[r, :]||^2 computed in fp64 from the ROUNDED fp32 coordinates, so
+// that a_i + b_j + x~.c~ = -||x~ - c~||^2 / 2 holds for the coordinates actually used.
+__global__ void pack_rows_kernel(const float *__restrict__ in, int64_t rows, int64_t d,
+                                 const double *__restrict__ mu, double g, int dq,
+                                 float *__restrict__ out, float *__restrict__ bias) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    double s = 0.0;
+    for (int k = lane; k < dq; k += 32) {
+      float v = 0.f;
+      if (k < d) v = (float)(((double)in[r * d + k] - mu[k]) * g);
+      out[r * dq + k] = v;
+      s += (double)v * (double)v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0 && bias) bias[r] = (float)(-0.5 * s);
+  }
+}
+
+// ------------------------------------------------------------------ fused kvp, d <= 32
+template <int KER, int D, int R>
+__global__ void __launch_bounds__(KVP_THREADS)
+    kvp_small_kernel(const float *__restrict__ P, const float *__restrict__ pa, int64_t np,
+                     const float *__restrict__ Q, const float *__restrict__ qb,
+                     const float *__restrict__ z, int64_t nq, int64_t q_per_split,
+                     double *__restrict__ out64, float *__restrict__ out32) {
+  constexpr int DQ = (D + 3) & ~3;
+  constexpr int QF = KVP_TQ * DQ;  // floats of one Q tile
+  extern __shared__ __align__(128) float smem_f[];
+  // stage s: q tile at smem_f + s*QF, biases at SB + s*TQ, weights at SZ + s*TQ
+  float *const SB = smem_f + 2 * QF;
+  float *const SZ = SB + 2 * KVP_TQ;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_f + 2 * QF + 4 * KVP_TQ);
+
+  const int tid = threadIdx.x;
+  const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
+  const int64_t qhi = min(nq, qlo + q_per_split);
+  const int ntiles = qhi > qlo ? (int)cdiv<int64_t>(qhi - qlo, KVP_TQ) : 0;
+
+  auto issue = [&](int t) {
+    const int64_t q0 = qlo + (int64_t)t * KVP_TQ;
+    const int cnt = (int)lmin(KVP_TQ, qhi - q0);
+    const int cnt4 = (cnt + 3) & ~3;  // arrays are padded: reading up to cnt4 is in bounds
+    const int s = t & 1;
+    const uint32_t bq = (uint32_t)cnt * DQ * 4, bs = (uint32_t)cnt4 * 4;
+    mbar_expect_tx(&bar[s], bq + (KER == FALKON_GAUSSIAN ? bs : 0) + bs);
+    bulk_g2s(smem_f + s * QF, Q + q0 * DQ, bq, &bar[s]);
+    if (KER == FALKON_GAUSSIAN) bulk_g2s(SB + s * KVP_TQ, qb + q0, bs, &bar[s]);
+    bulk_g2s(SZ + s * KVP_TQ, z + q0, bs, &bar[s]);
+  };
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (ntiles > 0) issue(0);
+    if (ntiles > 1) issue(1);
+  }
+
+  // owned points -> registers
+  float pc[R][D];
+  float pav[R];
+  const int64_t pbase = (int64_t)blockIdx.x * (KVP_THREADS * R) + tid;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t p = min(pbase + (int64_t)r * KVP_THREADS, np - 1);
+#pragma unroll
+    for (int k = 0; k < D; ++k) pc[r][k] = P[p * DQ + k];
+    pav[r] = (KER == FALKON_GAUSSIAN) ? pa[p] : 0.f;
+  }
+  double acc64[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc64[r] = 0.0;
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t & 1;
+    mbar_wait(&bar[s], (t >> 1) & 1);
+    const int cnt = (int)lmin(KVP_TQ, qhi - (qlo + (int64_t)t * KVP_TQ));
+    const float *q = smem_f + s * QF;
+    const float *sbs = SB + s * KVP_TQ;
+    const float *szs = SZ + s * KVP_TQ;
+    float acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.f;
+#pragma unroll 2
+    for (int j = 0; j < cnt; ++j) {
+      float qc[DQ];
+#pragma unroll
+      for (int k4 = 0; k4 < DQ / 4; ++k4) {
+        const float4 v4 = reinterpret_cast<const float4 *>(q + j * DQ)[k4];
+        qc[4 * k4 + 0] = v4.x;
+        qc[4 * k4 + 1] = v4.y;
+        qc[4 * k4 + 2] = v4.z;
+        qc[4 * k4 + 3] = v4.w;
+      }
+      const float zj = szs[j];
+      if (KER == FALKON_GAUSSIAN) {
+        const float bj = sbs[j];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float e = pav[r] + bj;
+#pragma unroll
+          for (int k = 0; k < D; ++k) e = fmaf(pc[r][k], qc[k], e);
+          acc[r] = fmaf(ex2_approx(fminf(e, 0.f)), zj, acc[r]);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float dd = 0.f;
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const float df = pc[r][k] - qc[k];
+            dd = fmaf(df, df, dd);
+          }
+          acc[r] = fmaf(ex2_approx(-sqrt_approx(dd)), zj, acc[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc64[r] += (double)acc[r];
+    __syncthreads();
+    if (tid == 0 && t + 2 < ntiles) issue(t + 2);
+  }
+
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t p = pbase + (int64_t)r * KVP_THREADS;
+    if (p < np) {
+      if (out64) out64[(int64_t)blockIdx.y * np + p] = acc64[r];
+      if (out32) out32[p] = (float)acc64[r];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ fused kvp, any d (SIMT)
+// Each thread owns one P point; a tile of 32 Q points is in shared memory; the 32 exponents
+// of the tile are accumulated in registers over 32-wide chunks of the dimension.
+template <int KER>
+__global__ void __launch_bounds__(KVP_THREADS)
+    kvp_generic_kernel(const float *__restrict__ P, const float *__restrict__ pa, int64_t np,
+                       const float *__restrict__ Q, const float *__restrict__ qb,
+                       const float *__restrict__ z, int64_t nq, int64_t q_per_split, int dq,
+                       double *__restrict__ out64, float *__restrict__ out32) {
+  constexpr int TQ = KVP_TQ_G;
+  extern __shared__ __align__(128) float smem_f[];
+  const int QF = TQ * dq;
+  float *const SB = smem_f + 2 * QF;
+  float *const SZ = SB + 2 * TQ;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_f + 2 * QF + 4 * TQ);
+
+  const int tid = threadIdx.x;
+  const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
+  const int64_t qhi = min(nq, qlo + q_per_split);
+  const int ntiles = qhi > qlo ? (int)cdiv<int64_t>(qhi - qlo, TQ) : 0;
+  auto issue = [&](int t) {
+    const int64_t q0 = qlo + (int64_t)t * TQ;
+    const int cnt = (int)lmin(TQ, qhi - q0);
+    const int cnt4 = (cnt + 3) & ~3;
+    const int s = t & 1;
+    const uint32_t bq = (uint32_t)cnt * dq * 4, bs = (uint32_t)cnt4 * 4;
+    mbar_expect_tx(&bar[s], bq + (KER == FALKON_GAUSSIAN ? bs : 0) + bs);
+    bulk_g2s(smem_f + s * QF, Q + q0 * dq, bq, &bar[s]);
+    if (KER == FALKON_GAUSSIAN) bulk_g2s(SB + s * TQ, qb + q0, bs, &bar[s]);
+    bulk_g2s(SZ + s * TQ, z + q0, bs, &bar[s]);
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (ntiles > 0) issue(0);
+    if (ntiles > 1) issue(1);
+  }
+  const int64_t p_raw = (int64_t)blockIdx.x * KVP_THREADS + tid;
+  const int64_t p = min(p_raw, np - 1);
+  const float *prow = P + p * dq;
+  const float pav = (KER == FALKON_GAUSSIAN) ? pa[p] : 0.f;
+  double acc64 = 0.0;
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t & 1;
+    mbar_wait(&bar[s], (t >> 1) & 1);
+    const int cnt = (int)lmin(TQ, qhi - (qlo + (int64_t)t * TQ));
+    const float *sqs = smem_f + s * QF;
+    const float *sbs = SB + s * TQ;
+    const float *szs = SZ + s * TQ;
+    float e[TQ];
+#pragma unroll
+    for (int j = 0; j < TQ; ++j) e[j] = (KER == FALKON_GAUSSIAN) ? pav + sbs[j] : 0.f;
+    for (int k0 = 0; k0 < dq; k0 += 32) {
+      const int kc = min(32, dq - k0);  // multiple of 4
+      float pch[32];
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4) {
+        float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (4 * k4 < kc) v4 = __ldg(reinterpret_cast<const float4 *>(prow + k0) + k4);
+        pch[4 * k4 + 0] = v4.x;
+        pch[4 * k4 + 1] = v4.y;
+        pch[4 * k4 + 2] = v4.z;
+        pch[4 * k4 + 3] = v4.w;
+      }
+#pragma unroll
+      for (int j = 0; j < TQ; ++j) {
+        const float4 *qrow = reinterpret_cast<const float4 *>(sqs + j * dq + k0);
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4) {
+          if (4 * k4 < kc) {
+            const float4 q4 = qrow[k4];
+            if (KER == FALKON_GAUSSIAN) {
+              e[j] = fmaf(pch[4 * k4 + 0], q4.x, e[j]);
+              e[j] = fmaf(pch[4 * k4 + 1], q4.y, e[j]);
+              e[j] = fmaf(pch[4 * k4 + 2], q4.z, e[j]);
+              e[j] = fmaf(pch[4 * k4 + 3], q4.w, e[j]);
+            } else {
+              float df;
+              df = pch[4 * k4 + 0] - q4.x; e[j] = fmaf(df, df, e[j]);
+              df = pch[4 * k4 + 1] - q4.y; e[j] = fmaf(df, df, e[j]);
+              df = pch[4 * k4 + 2] - q4.z; e[j] = fmaf(df, df, e[j]);
+              df = pch[4 * k4 + 3] - q4.w; e[j] = fmaf(df, df, e[j]);
+            }
+          }
+        }
+      }
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < TQ; ++j) {
+      if (j < cnt) {
+        const float kv = (KER == FALKON_GAUSSIAN) ? ex2_approx(fminf(e[j], 0.f))
+                                                  : ex2_approx(-sqrt_approx(e[j]));
+        acc = fmaf(kv, szs[j], acc);
+      }
+    }
+    acc64 += (double)acc;
+    __syncthreads();
+    if (tid == 0 && t + 2 < ntiles) issue(t + 2);
+  }
+  if (p_raw < np) {
+    if (out64) out64[(int64_t)blockIdx.y * np + p_raw] = acc64;
+    if (out32) out32[p_raw] = (float)acc64;
+  }
+}
+
+// ------------------------------------------------------------------ reductions / conversions
+__global__ void reduce_splits_kernel(const double *__restrict__ part, int splits, int64_t np,
+                                     double *__restrict__ out64, float *__restrict__ out32) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  double s = 0.0;
+  for (int i = 0; i < splits; ++i) s += part[(int64_t)i * np + p];
+  if (out64) out64[p] = s;
+  if (out32) out32[p] = (float)s;
+}
+
+__global__ void f64_to_f32_kernel(const double *__restrict__ s, float *__restrict__ d, int64_t n,
+                                  int64_t n_pad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = (float)s[i];
+  else if (i < n_pad) d[i] = 0.f;
+}
+__global__ void f32_copy_pad_kernel(const float *__restrict__ s, float *__restrict__ d, int64_t n,
+                                    int64_t n_pad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = s[i];
+  else if (i < n_pad) d[i] = 0.f;
+}
+
+int f64_to_f32(falkon_ctx *ctx, const double *src, float *dst, int64_t n, int64_t n_pad) {
+  if (n_pad <= 0) return FALKON_OK;
+  LaunchScope ls(ctx, FALKON_T_PREP);
+  f64_to_f32_kernel<<<(unsigned)cdiv<int64_t>(n_pad, 256), 256, 0, ctx->stream>>>(src, dst, n,
+                                                                                    n_pad);
+  FK_LAUNCH_CHECK();
+  return FALKON_OK;
+}
+int f32_to_f32_pad(falkon_ctx *ctx, const float *src, float *dst, int64_t n, int64_t n_pad) {
+  if (n_pad <= 0) return FALKON_OK;
+  LaunchScope ls(ctx, FALKON_T_PREP);
+  f32_copy_pad_kernel<<<(unsigned)cdiv<int64_t>(n_pad, 256), 256, 0, ctx->stream>>>(src, dst, n,
+                                                                                      n_pad);
+  FK_LAUNCH_CHECK();
+  return FALKON_OK;
+}
+
+// ------------------------------------------------------------------ dispatch
+typedef void (*kvp_fn)(const float *, const float *, int64_t, const float *, const float *,
+                       const float *, int64_t, int64_t, double *, float *);
+
+template <int KER, int D>
+static kvp_fn pick_small_R(int R) {
+  if (R == 4) return kvp_small_kernel<KER, D, 4>;
+  if (R == 2) return kvp_small_kernel<KER, D, 2>;
+  return kvp_small_kernel<KER, D, 1>;
+}
+
+// exact D for d <= 16; multiples of 4 up to 32 (zero-padded coordinates add exact zeros)
+static int small_D(int64_t d) {
+  if (d <= 16) return (int)d;
+  return (int)round_up<int64_t>(d, 4);
+}
+static int small_R(int D) { return D <= 16 ? 4 : 2; }
+
+template <int KER>
+static kvp_fn pick_small(int D, int R) {
+  switch (D) {
+#define FK_CASE(DD) \
+  case DD: return pick_small_R<KER, DD>(R);
+    FK_CASE(1) FK_CASE(2) FK_CASE(3) FK_CASE(4) FK_CASE(5) FK_CASE(6) FK_CASE(7) FK_CASE(8)
+    FK_CASE(9) FK_CASE(10) FK_CASE(11) FK_CASE(12) FK_CASE(13) FK_CASE(14) FK_CASE(15)
+    FK_CASE(16) FK_CASE(20) FK_CASE(24) FK_CASE(28) FK_CASE(32)
+#undef FK_CASE
+    default: return nullptr;
+  }
+}
+
+static int occupancy(const void *fn, int threads, size_t smem) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  return std::max(nb, 1);
+}
+
+// One kvp launch (+ split reduction).  out64 (np, optional) / out32 (np, optional).
+static int kvp_launch(falkon_ctx *ctx, int kernel, int64_t d, int dq, const float *P,
+                      const float *pa, int64_t np, const float *Q, const float *qb, const float *z,
+                      int64_t nq, int cls, double *out64, float *out32) {
+  if (np <= 0) return FALKON_OK;
+  const bool small = d <= 32;
+  int D = 0, R = 1, TQ;
+  const void *fn;
+  size_t smem;
+  if (small) {
+    D = small_D(d);
+    R = small_R(D);
+    const int DQ = (D + 3) & ~3;
+    TQ = KVP_TQ;
+    fn = (const void *)(kernel == FALKON_GAUSSIAN ? pick_small<FALKON_GAUSSIAN>(D, R)
+                                                  : pick_small<FALKON_LAPLACIAN>(D, R));
+    smem = (size_t)(2 * TQ * DQ + 4 * TQ) * 4 + 16;
+  } else {
+    TQ = KVP_TQ_G;
+    fn = (const void *)(kernel == FALKON_GAUSSIAN ? kvp_generic_kernel<FALKON_GAUSSIAN>
+                                                  : kvp_generic_kernel<FALKON_LAPLACIAN>);
+    smem = (size_t)(2 * TQ * dq + 4 * TQ) * 4 + 16;
+  }
+  if (!fn) return fail(FALKON_EINVAL, "no kvp kernel for d=" + std::to_string(d));
+  FK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t per_cta = (int64_t)KVP_THREADS * R;
+  const int64_t gx = cdiv<int64_t>(np, per_cta);
+  const int64_t capacity = (int64_t)ctx->sm_count * occupancy(fn, KVP_THREADS, smem);
+  int64_t splits = 1;
+  if (gx < capacity) {
+    splits = std::max<int64_t>(1, capacity / gx);
+    const int64_t min_q = 4 * TQ;  // at least a few tiles per split
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, nq / min_q));
+    splits = std::min<int64_t>(splits, 65535);
+  }
+  int64_t qps = round_up<int64_t>(cdiv<int64_t>(nq, splits), TQ);
+  splits = std::max<int64_t>(1, cdiv<int64_t>(nq, qps));
+  if (gx > 0x7fffffffLL) return fail(FALKON_EINVAL, "too many rows for one launch");
+
+  double *part = out64;
+  if (splits > 1 || !out64) {
+    void *pp;
+    FK_TRY(ws_get(ctx, WS_PART, sizeof(double) * splits * np, &pp));
+    part = (double *)pp;
+  }
+  dim3 grid((unsigned)gx, (unsigned)splits);
+  {
+    LaunchScope ls(ctx, cls);
+    if (small) {
+      ((kvp_fn)fn)<<<grid, KVP_THREADS, smem, ctx->stream>>>(P, pa, np, Q, qb, z, nq, qps, part,
+                                                             splits == 1 ? out32 : nullptr);
+    } else {
+      auto g = (kernel == FALKON_GAUSSIAN ? kvp_generic_kernel<FALKON_GAUSSIAN>
+                                          : kvp_generic_kernel<FALKON_LAPLACIAN>);
+      g<<<grid, KVP_THREADS, smem, ctx->stream>>>(P, pa, np, Q, qb, z, nq, qps, dq, part,
+                                                  splits == 1 ? out32 : nullptr);
+    }
+  }
+  FK_LAUNCH_CHECK();
+  if (splits > 1 || (!out64 && !out32)) {
+    LaunchScope ls(ctx, FALKON_T_REDUCE);
+    reduce_splits_kernel<<<(unsigned)cdiv<int64_t>(np, 256), 256, 0, ctx->stream>>>(
+        part, (int)splits, np, out64, out32);
+    FK_LAUNCH_CHECK();
+  } else if (splits == 1 && !out64) {
+    // out32 already written by the kernel
+  }
+  return FALKON_OK;
+}
+
+// ------------------------------------------------------------------ public-ish entry points
+int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const float *C,
+                     int64_t m, int kernel, double sigma, Prepared *pp) {
+  pp->n = n;
+  pp->m = m;
+  pp->d = d;
+  pp->kernel = kernel;
+  double *mu;
+  FK_TRY(center_mean(ctx, C, m, d, &mu));
+  const bool use_tc = tc_supported(ctx, kernel, d);
+  if (use_tc) {
+    pp->path = FALKON_PATH_TENSOR;
+    return tc_prepare(ctx, X, n, d, C, m, sigma, mu, pp);
+  }
+  pp->path = FALKON_PATH_SIMT;
+  const int dq = d <= 32 ? ((small_D(d) + 3) & ~3) : (int)round_up<int64_t>(d, 4);
+  pp->dq = dq;
+  const double g = kernel == FALKON_GAUSSIAN ? std::sqrt(LOG2E) / sigma : LOG2E / sigma;
+  // padded to a multiple of 128 rows so tile loads may round up
+  const int64_t n_pad = round_up<int64_t>(std::max<int64_t>(n, 1), 128);
+  const int64_t m_pad = round_up<int64_t>(m, 128);
+  void *xp, *xa, *cp, *cb;
+  FK_TRY(ws_get(ctx, WS_XP, sizeof(float) * n_pad * dq, &xp));
+  FK_TRY(ws_get(ctx, WS_XA, sizeof(float) * n_pad, &xa));
+  FK_TRY(ws_get(ctx, WS_CP, sizeof(float) * m_pad * dq, &cp));
+  FK_TRY(ws_get(ctx, WS_CB, sizeof(float) * m_pad, &cb));
+  const int threads = 256;
+  {
+    LaunchScope ls(ctx, FALKON_T_PREP);
+    int64_t blocks = std::min<int64_t>(cdiv<int64_t>(m, threads / 32), 65535);
+    pack_rows_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(
+        C, m, d, mu, g, dq, (float *)cp, kernel == FALKON_GAUSSIAN ? (float *)cb : nullptr);
+  }
+  FK_LAUNCH_CHECK();
+  if (n > 0) {
+    LaunchScope ls(ctx, FALKON_T_PREP);
+    int64_t blocks = std::min<int64_t>(cdiv<int64_t>(n, threads / 32), (int64_t)ctx->sm_count * 64);
+    pack_rows_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(
+        X, n, d, mu, g, dq, (float *)xp, kernel == FALKON_GAUSSIAN ? (float *)xa : nullptr);
+    FK_LAUNCH_CHECK();
+  }
+  pp->Xp = xp;
+  pp->xa = (const float *)xa;
+  pp->Cp = cp;
+  pp->cb = (const float *)cb;
+  return FALKON_OK;
+}
+
+int pass_A(falkon_ctx *ctx, const Prepared &pp, const float *z, double *w64, float *w32) {
+  if (pp.n <= 0) return FALKON_OK;
+  if (pp.path == FALKON_PATH_TENSOR) return tc_pass(ctx, pp, true, z, w64, w32);
+  return kvp_launch(ctx, pp.kernel, pp.d, pp.dq, (const float *)pp.Xp, pp.xa, pp.n,
+                    (const float *)pp.Cp, pp.cb, z, pp.m, FALKON_T_PASS_A, w64, w32);
+}
+
+int pass_B(falkon_ctx *ctx, const Prepared &pp, const float *w, double *u) {
+  if (pp.n <= 0) {
+    FK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * pp.m, ctx->stream));
+    return FALKON_OK;
+  }
+  if (pp.path == FALKON_PATH_TENSOR) return tc_pass(ctx, pp, false, w, u, nullptr);
+  return kvp_launch(ctx, pp.kernel, pp.d, pp.dq, (const float *)pp.Cp, pp.cb, pp.m,
+                    (const float *)pp.Xp, pp.xa, w, pp.n, FALKON_T_PASS_B, u, nullptr);
+}
+
+}  // namespace falkon

@@ -1,0 +1,117 @@
+"""GPU parity of the fused products (rows a1-a6 of SURVEY.md §8(a)) against the oracle.
+
+Bar (north_star): Knm^T(Knm v) relative L2 error <= 1e-4 against the fp64 oracle on the
+same seeded inputs.  The one-sided products (Knm v, Knm^T w) are held to the same bar.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import dev, host, rel_l2, zeros
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+G, L = oracle.GAUSSIAN, oracle.LAPLACIAN
+
+
+def _problem(n, m, d, seed, scale=1.0):
+    X = synth.gen_X(seed, 0, n, d) * np.float32(scale)
+    C = X[synth.center_indices(seed, n, m)]
+    v = synth.gen_vec(seed, m).astype(np.float64)
+    return X.astype(np.float32), np.ascontiguousarray(C), v
+
+
+# shapes span several tiles and ragged tails of both kernels (SIMT small-d, generic d > 32)
+SHAPES = [
+    (2000, 100, 8, 1.0),      # tiny config (BASELINE.json configs[0])
+    (3001, 517, 9, 1.0),      # TAXI-like d, ragged
+    (2500, 333, 28, 3.8),     # HIGGS-like d
+    (1537, 129, 1, 0.7),      # d = 1
+    (777, 1000, 13, 2.0),     # m > n
+    (1200, 300, 90, 7.0),     # MSD-like d (tensor path when enabled)
+    (700, 250, 440, 14.5),    # TIMIT-like d
+    (500, 70, 33, 4.0),       # just above the small-d limit
+]
+
+
+@pytest.mark.parametrize("kernel", [G, L])
+@pytest.mark.parametrize("n,m,d,sigma", SHAPES)
+def test_knm_matvec_parity(ctx, kernel, n, m, d, sigma):
+    X, C, v = _problem(n, m, d, seed=n + m + d)
+    ref = oracle.knm_t_knm_vec(X, C, v, kernel, sigma)
+    u = ctx.knm_matvec(dev(X), dev(C), dev(v), kernel, sigma, zeros(m))
+    assert rel_l2(host(u), ref) <= TOL
+
+
+@pytest.mark.parametrize("kernel", [G, L])
+@pytest.mark.parametrize("n,m,d,sigma", SHAPES[:6])
+def test_one_sided_parity(ctx, kernel, n, m, d, sigma):
+    X, C, v = _problem(n, m, d, seed=3 * n + m + d)
+    w_ref = oracle.knm_vec(X, C, v, kernel, sigma)
+    w = ctx.kernel_vec(dev(X), dev(C), dev(v), kernel, sigma, zeros(n))
+    assert rel_l2(host(w), w_ref) <= TOL
+    wr = np.random.default_rng(n).standard_normal(n)
+    u_ref = oracle.knm_t_vec(X, C, wr, kernel, sigma)
+    u = ctx.kernel_tvec(dev(X), dev(C), dev(wr), kernel, sigma, zeros(m))
+    assert rel_l2(host(u), u_ref) <= TOL
+
+
+def test_host_pointer_path_matches_device_path(ctx):
+    X, C, v = _problem(4000, 300, 9, seed=5)
+    ud = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 1.0, zeros(300)))
+    uh = np.zeros(300)
+    ctx.knm_matvec(X, C, v, G, 1.0, uh)
+    assert np.array_equal(ud, uh)
+
+
+def test_deterministic_bitwise(ctx):
+    X, C, v = _problem(5000, 700, 28, seed=6)
+    a = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 3.8, zeros(700)))
+    b = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 3.8, zeros(700)))
+    assert np.array_equal(a, b)
+
+
+def test_zero_vector_and_unit_vectors(ctx):
+    X, C, _ = _problem(1000, 50, 9, seed=7)
+    u = host(ctx.knm_matvec(dev(X), dev(C), dev(np.zeros(50)), G, 1.0, zeros(50)))
+    assert np.all(u == 0.0)
+    e = np.zeros(1000)
+    e[17] = 1.0
+    row = host(ctx.kernel_tvec(dev(X), dev(C), dev(e), G, 1.0, zeros(50)))
+    ref = oracle.kernel_block(X[17:18], C, G, 1.0)[0]
+    assert rel_l2(row, ref) <= 1e-5
+
+
+def test_empty_rank_contributes_zero(ctx):
+    X = np.zeros((0, 9), np.float32)
+    C = synth.gen_X(1, 0, 40, 9)
+    u = host(ctx.knm_matvec(dev(X), dev(C), dev(np.ones(40)), G, 1.0, zeros(40)))
+    assert np.all(u == 0.0)
+
+
+def test_single_point(ctx):
+    X = synth.gen_X(2, 0, 1, 5)
+    C = X.copy()
+    u = host(ctx.knm_matvec(dev(X), dev(C), dev(np.array([2.5])), G, 1.0, zeros(1)))
+    assert abs(u[0] - 2.5) <= 1e-6
+
+
+def test_sigma_infinity_closed_form(ctx):
+    """sigma -> inf: K == 1 in fp32, u = n * sum(v) (SURVEY.md §8(c) pins), long sums."""
+    n, m = 200_000, 64
+    X, C, v = _problem(n, m, 9, seed=8)
+    v = np.abs(v)
+    u = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 1e5, zeros(m)))
+    assert np.max(np.abs(u - n * v.sum())) <= 1e-6 * n * v.sum()
+
+
+def test_translation_invariance(ctx):
+    """Shifting X and C by a large common offset (SPEC S:523 flavour) leaves the product
+    unchanged: centring removes the norm-expansion cancellation."""
+    X, C, v = _problem(3000, 200, 28, seed=9)
+    off = np.float32(100.0)
+    Xs, Cs = X + off, C + off
+    ref = oracle.knm_t_knm_vec(Xs, Cs, v, G, 3.8)
+    u = host(ctx.knm_matvec(dev(Xs), dev(Cs), dev(v), G, 3.8, zeros(200)))
+    assert rel_l2(u, ref) <= TOL
