@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override global n (debug)")
     ap.add_argument("--m", type=int, default=None, help="override m (debug)")
     ap.add_argument("--oracle-seconds", type=float, default=15.0)
+    ap.add_argument("--quick", action="store_true",
+                    help="timed product steps only (no e2e, cpu_baseline, fit): for ncu runs")
     return ap.parse_args()
 
 
@@ -140,6 +142,17 @@ def oracle_rate(cfg, n_global, m, seconds: float, rank_workers: int):
     oracle.knm_t_knm_vec(Xs, C, v, oracle.GAUSSIAN, cfg.sigma, workers=rank_workers)
     dt = time.perf_counter() - t0
     return n_s * m / dt, {"rows": n_s, "m": m, "seconds": dt}
+
+
+def kt_path_tensor(args, d):
+    """Mirror of libfalkon's path choice (tc_supported): tensor cores for the Gaussian kernel
+    when d > 32 and round_up(d + 2, 16) <= 192, unless --path forces one."""
+    if args.path == "simt":
+        return False
+    d16 = -(-(d + 2) // 16) * 16
+    if d16 > 192:
+        return False
+    return args.path == "tensor" or d > 32
 
 
 def host_cores():
@@ -261,7 +274,7 @@ def main():
     f_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     d = cfg.d
-    path = "tensor" if (args.path != "simt" and d > 32) else "simt"
+    path = "tensor" if kt_path_tensor(args, d) else "simt"
     if path == "simt":
         # FP32 pipe: d FMA (cross term) + 1 FADD (bias) + 1 FFMA (contraction) per entry
         # (Laplacian: 2d); MUFU: 1 ex2 per entry.  Binding pipe = the slower.
@@ -282,17 +295,19 @@ def main():
             "kernel_ms": dom_ms,
             "share_of_step": kt[dom][0] / ms_total if ms_total else None}
 
+    if args.quick:
+        args.no_fit = True
     # ---- e2e: same metric through the C-ABI with HOST (pinned) buffers ----
     uh = torch.zeros(m, dtype=torch.float64).pin_memory()
-    for _ in range(2):
+    e2e_steps = 0 if args.quick else max(3, min(args.steps, 10))
+    for _ in range(2 if e2e_steps else 0):
         ctx.knm_matvec(Xh, Ch, vh, kernel, sigma, uh)
     barrier()
     t0 = time.perf_counter()
-    e2e_steps = max(3, min(args.steps, 10))
     for _ in range(e2e_steps):
         ctx.knm_matvec(Xh, Ch, vh, kernel, sigma, uh)
     barrier()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_s = (time.perf_counter() - t0) / max(1, e2e_steps)
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -322,7 +337,7 @@ def main():
             fit = {"error": str(ex)}
 
     cpu = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.quick:
         rate, inf = oracle_rate(cfg, n_global, m, args.oracle_seconds, host_cores())
         cpu = {"value": rate, "unit": "n*m/s", "cores": host_cores(), "kind": "oracle",
                "sample": f"{inf['rows']} of {n_global} rows x all {m} centers, one product, "

@@ -107,8 +107,9 @@ int falkon_get_unique_id(unsigned char id[128]);
 int falkon_ctx_create(falkon_ctx **out, int device, int rank, int world, const unsigned char *id);
 int falkon_ctx_destroy(falkon_ctx *ctx);
 
-/* Make the context launch on `stream` (a cudaStream_t cast to void*; NULL = the context's
-   own stream).  The caller keeps ownership of the stream. */
+/* Make the context launch on `stream` (a cudaStream_t cast to void*; NULL = the legacy
+   default stream).  Until this is called the context uses its own non-blocking stream.
+   The caller keeps ownership of the stream. */
 int falkon_ctx_set_stream(falkon_ctx *ctx, void *stream);
 int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value);
 /* Accumulated per-class device times (ms) since the last reset; out has FALKON_T_COUNT

@@ -131,7 +131,10 @@ class Context:
     """One libfalkon context (one GPU, one rank)."""
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1,
-                 unique_id: Optional[bytes] = None):
+                 unique_id: Optional[bytes] = None, stream="torch"):
+        """stream="torch": launch on torch's current CUDA stream of `device` (so torch-side
+        reads of output tensors are ordered after the library's kernels); None: the
+        context's own stream; otherwise a torch.cuda.Stream or raw cudaStream_t int."""
         load()
         h = ctypes.c_void_p()
         uid = None
@@ -140,6 +143,11 @@ class Context:
         _check(_LIB.falkon_ctx_create(ctypes.byref(h), device, rank, world, uid))
         self.h = h
         self.device, self.rank, self.world = device, rank, world
+        if stream == "torch":
+            import torch
+            stream = torch.cuda.current_stream(device)
+        if stream is not None:
+            self.set_stream(stream)
 
     def close(self):
         if self.h:
@@ -153,11 +161,11 @@ class Context:
             pass
 
     # -- configuration
-    def set_stream(self, stream=None):
-        """stream: torch.cuda.Stream, raw cudaStream_t int, or None (own stream)."""
-        if stream is not None and not isinstance(stream, int):
+    def set_stream(self, stream):
+        """stream: torch.cuda.Stream or raw cudaStream_t int (0 = legacy default stream)."""
+        if not isinstance(stream, int):
             stream = stream.cuda_stream
-        _check(_LIB.falkon_ctx_set_stream(self.h, stream))
+        _check(_LIB.falkon_ctx_set_stream(self.h, stream or None))
 
     def set_option(self, option: int, value: int):
         _check(_LIB.falkon_ctx_set_option(self.h, option, int(value)))

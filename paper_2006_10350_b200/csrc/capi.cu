@@ -278,7 +278,7 @@ int falkon_ctx_destroy(falkon_ctx *ctx) {
 
 int falkon_ctx_set_stream(falkon_ctx *ctx, void *stream) {
   if (!ctx) return fail(FALKON_EINVAL, "ctx is NULL");
-  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  ctx->stream = (cudaStream_t)stream;  // NULL = the legacy default stream
   return FALKON_OK;
 }
 

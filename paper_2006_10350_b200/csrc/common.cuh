@@ -128,6 +128,7 @@ struct Prepared {
   const float *xa = nullptr;
   const void *Cp = nullptr;
   const float *cb = nullptr;
+  alignas(64) unsigned char tmaps[4 * 128];  // CUtensorMap x4 (tensor path)
 };
 
 int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const float *C,

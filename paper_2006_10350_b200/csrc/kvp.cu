@@ -355,6 +355,15 @@ __global__ void f32_copy_pad_kernel(const float *__restrict__ s, float *__restri
   else if (i < n_pad) d[i] = 0.f;
 }
 
+int reduce_partials(falkon_ctx *ctx, const double *part, int64_t splits, int64_t np,
+                    double *out64, float *out32) {
+  LaunchScope ls(ctx, FALKON_T_REDUCE);
+  reduce_splits_kernel<<<(unsigned)cdiv<int64_t>(np, 256), 256, 0, ctx->stream>>>(
+      part, (int)splits, np, out64, out32);
+  FK_LAUNCH_CHECK();
+  return FALKON_OK;
+}
+
 int f64_to_f32(falkon_ctx *ctx, const double *src, float *dst, int64_t n, int64_t n_pad) {
   if (n_pad <= 0) return FALKON_OK;
   LaunchScope ls(ctx, FALKON_T_PREP);

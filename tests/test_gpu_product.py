@@ -17,7 +17,10 @@ G, L = oracle.GAUSSIAN, oracle.LAPLACIAN
 
 def _problem(n, m, d, seed, scale=1.0):
     X = synth.gen_X(seed, 0, n, d) * np.float32(scale)
-    C = X[synth.center_indices(seed, n, m)]
+    if m <= n:
+        C = X[synth.center_indices(seed, n, m)]
+    else:  # more centers than rows: independent draws (C need not be a subset of X)
+        C = synth.gen_X(seed + 1, 0, m, d) * np.float32(scale)
     v = synth.gen_vec(seed, m).astype(np.float64)
     return X.astype(np.float32), np.ascontiguousarray(C), v
 
@@ -115,3 +118,39 @@ def test_translation_invariance(ctx):
     ref = oracle.knm_t_knm_vec(Xs, Cs, v, G, 3.8)
     u = host(ctx.knm_matvec(dev(Xs), dev(Cs), dev(v), G, 3.8, zeros(200)))
     assert rel_l2(u, ref) <= TOL
+
+
+TC_SHAPES = [
+    (1200, 300, 90, 7.0),     # MSD-like
+    (4100, 700, 90, 7.0),     # several P tiles and Q tiles, ragged
+    (100, 40, 90, 7.0),       # smaller than one tile on both sides
+    (900, 513, 33, 4.0),      # d16 = 48
+    (640, 260, 186, 10.0),    # largest d of the resident-A tensor kernel (d16 = 192)
+    (3000, 2000, 28, 3.8),    # HIGGS d forced onto tensor cores
+]
+
+
+@pytest.mark.parametrize("n,m,d,sigma", TC_SHAPES)
+def test_tensor_path_parity(ctx, n, m, d, sigma):
+    """tcgen05 fp16x3 cross-term path (forced) against the oracle, product and one-sided."""
+    from paper_2006_10350_b200 import binding
+    X, C, v = _problem(n, m, d, seed=7 * n + m + d)
+    ctx.set_option(binding.OPT_PATH, binding.PATH_TENSOR)
+    try:
+        u = ctx.knm_matvec(dev(X), dev(C), dev(v), G, sigma, zeros(m))
+        w = ctx.kernel_vec(dev(X), dev(C), dev(v), G, sigma, zeros(n))
+    finally:
+        ctx.set_option(binding.OPT_PATH, binding.PATH_AUTO)
+    assert rel_l2(host(w), oracle.knm_vec(X, C, v, G, sigma)) <= TOL
+    assert rel_l2(host(u), oracle.knm_t_knm_vec(X, C, v, G, sigma)) <= TOL
+
+
+def test_tensor_and_simt_paths_agree(ctx):
+    from paper_2006_10350_b200 import binding
+    X, C, v = _problem(20000, 3000, 90, seed=12)
+    out = {}
+    for path in (binding.PATH_SIMT, binding.PATH_TENSOR):
+        ctx.set_option(binding.OPT_PATH, path)
+        out[path] = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 7.0, zeros(3000)))
+    ctx.set_option(binding.OPT_PATH, binding.PATH_AUTO)
+    assert rel_l2(out[binding.PATH_TENSOR], out[binding.PATH_SIMT]) <= TOL
