@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override global n (debug)")
     ap.add_argument("--m", type=int, default=None, help="override m (debug)")
     ap.add_argument("--oracle-seconds", type=float, default=15.0)
+    ap.add_argument("--exp-offload", type=int, default=None,
+                    help="tensor path: exp2 share on the FMA pipe (0 none, 1 all, 2 1/4, 3 1/2)")
     ap.add_argument("--quick", action="store_true",
                     help="timed product steps only (no e2e, cpu_baseline, fit): for ncu runs")
     return ap.parse_args()
@@ -216,6 +218,8 @@ def main():
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream)
     ctx.set_option(binding.OPT_PATH, {"auto": 0, "simt": 1, "tensor": 2}[args.path])
+    if args.exp_offload is not None:
+        ctx.set_option(binding.OPT_EXP_OFFLOAD, args.exp_offload)
 
     n_global = args.n or cfg.n
     m = args.m or cfg.m

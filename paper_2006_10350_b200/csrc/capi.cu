@@ -300,6 +300,10 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
     case FALKON_OPT_KERNEL_TIMING:
       ctx->opt.kernel_timing = value ? 1 : 0;
       return FALKON_OK;
+    case FALKON_OPT_EXP_OFFLOAD:
+      if (value < 0 || value > 3) return fail(FALKON_EINVAL, "exp offload mode must be 0..3");
+      ctx->opt.exp_offload = (int)value;
+      return FALKON_OK;
     default:
       return fail(FALKON_EINVAL, "unknown option");
   }

@@ -67,6 +67,7 @@ struct Options {
   int tc_min_d = 32;
   int tc_terms = 3;
   int kernel_timing = 0;
+  int exp_offload = 0;  // tensor path: share of exp2 evaluated on the FMA pipe (0..3)
 };
 
 }  // namespace falkon

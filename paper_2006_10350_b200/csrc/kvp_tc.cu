@@ -28,6 +28,8 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -35,10 +37,11 @@
 namespace falkon {
 
 constexpr int TC_M = 128;
-constexpr int TC_N = 256;
+constexpr int TC_N = 256;                         // Q rows per tile, shared-memory A (SS)
+constexpr int TC_N_TS = 192;                      // Q rows per tile, A in TMEM (TS)
 constexpr int TC_BK = 64;                          // fp16 per K box (128 B = one swizzle row)
-constexpr int TC_STAGES = 4;
-constexpr int TC_THREADS = 256;
+constexpr int TC_THREADS = 128 + 32 * 8;          // 4 control warps + 8 epilogue warps
+constexpr int TC_SMEM_MAX = 227 * 1024;
 constexpr int TC_A_BOX = TC_M * TC_BK * 2;         // 16 KB
 constexpr int TC_B_BOX = TC_N * TC_BK * 2;         // 32 KB
 constexpr int TC_MAX_D16 = 192;                    // A (all K) resident: 128 x 2*d16 fp16 <= 96 KB
@@ -49,6 +52,14 @@ int reduce_partials(falkon_ctx *ctx, const double *part, int64_t splits, int64_t
 int center_mean(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, double **mu_out);
 
 static inline int tc_d16(int64_t d) { return (int)round_up<int64_t>(d + 2, 16); }
+// TS (A operand in TMEM) needs 2 accumulators of TC_N_TS columns + 16 columns per d16/16
+// chunk pair: 2*192 + 16*nk <= 512  <=>  d16 <= 128.
+// Measured on B200 (MSD shape): TS is ~5% slower than SS — the MMA rate, not shared-memory
+// bandwidth, binds — so it is opt-in (FALKON_TC_TS=1) and kept as a tested variant.
+static bool tc_use_ts(int d16) {
+  const char *e = getenv("FALKON_TC_TS");
+  return e && atoi(e) != 0 && 2 * TC_N_TS + 16 * (d16 / 16) <= 512;
+}
 
 bool tc_supported(const falkon_ctx *ctx, int kernel, int64_t d) {
   if (kernel != FALKON_GAUSSIAN) return false;  // Laplacian: direct differences only (reading c7)
@@ -101,6 +112,13 @@ __global__ void tc_pack_kernel(const float *__restrict__ in, int64_t rows, int64
 }
 
 // ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,
                                             uint64_t *bar) {
   asm volatile(
@@ -153,43 +171,128 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Waits for outstanding tcgen05.ld and ties the destination registers to the wait, so the
+// compiler cannot schedule their uses before the data has landed.
+__device__ __forceinline__ void tmem_wait_ld_regs(uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+        "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+        "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]),
+        "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]),
+        "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+      :
+      : "memory");
+}
+
 struct TcArgs {
   const float *z;
   int64_t np, nq, q_per_split;
   int nk;        // 16-wide K chunks per segment (d16 / 16)
   int nbox;      // 64-wide boxes covering one packed row (2*d16)
+  int stages;    // depth of the Q-box ring
   double *out64;
   float *out32;
 };
 
-__global__ void __launch_bounds__(TC_THREADS, 1)
+constexpr int TC_EPI_WARPS = 8;   // 2 per SM sub-partition: (TMEM lane group, column half)
+constexpr int TC_MAX_STAGES = 8;
+
+// exp2(x) for x <= 0 on the FMA pipe (FlashAttention-4-style MUFU offload): round-to-nearest
+// split x = j + f (magic-number add), 2^f by a degree-5 near-minimax polynomial on
+// [-0.5, 0.5] (max rel. error 2.3e-7 in fp32, same order as ex2.approx), 2^j by adding j to
+// the exponent field.  x is clamped at -126 so the result stays normal.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;        // 1.5 * 2^23: low mantissa bits = round(x)
+  const float r = t - 12582912.f;
+  const float f = x - r;
+  float p = 1.327646430581808e-3f;
+  p = fmaf(p, f, 9.675540961325169e-3f);
+  p = fmaf(p, f, 5.550713464617729e-2f);
+  p = fmaf(p, f, 2.4022120237350464e-1f);
+  p = fmaf(p, f, 6.931469440460205e-1f);
+  p = fmaf(p, f, 1.0000001192092896f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// Epilogue modes (template): 0 = every exp2 on MUFU; 1 = all on the FMA pipe; 2 = one of
+// four columns on the FMA pipe; 3 = two of four; 8/9 = diagnostics (no exp / no TMEM read).
+template <int MODE>
+__device__ __forceinline__ float tc_exp2(float t, int e) {
+  t = fminf(t, 0.f);
+  if (MODE == 1 || (MODE == 2 && e == 0) || (MODE == 3 && (e & 1) == 0)) return exp2_poly(t);
+  if (MODE == 8) return t;
+  return ex2_approx(t);
+}
+
+// 32 accumulator columns: k = exp2(min(t, 0)), acc += k * z (4 independent FFMA chains)
+template <int MODE, bool MASK>
+__device__ __forceinline__ void tc_epi_chunk(const uint32_t (&r)[32], const float *__restrict__ z,
+                                             int lim, float (&acc)[4]) {
+  const float4 *zp = reinterpret_cast<const float4 *>(z);
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const float4 zz = __ldg(zp + g);
+    float zv[4] = {zz.x, zz.y, zz.z, zz.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = 4 * g + e;
+      if (MASK && j >= lim) zv[e] = 0.f;
+      acc[e] = fmaf(tc_exp2<MODE>(__uint_as_float(r[j]), e), zv[e], acc[e]);
+    }
+  }
+}
+
+__device__ __forceinline__ void tc_mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// smem (matrix descriptor) -> TMEM copy of one 128-row x 16-fp16 chunk (8 TMEM columns)
+__device__ __forceinline__ void tc_cp_128x256b(uint32_t tmem_dst, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmem_dst), "l"(sdesc));
+}
+
+// NT: Q rows per MMA tile (accumulator columns).  TS: the resident P tile is copied once
+// into TMEM and used as the MMA's A operand (shared memory then only feeds B).
+template <int MODE, int NT, bool TS>
+__global__ void __launch_bounds__(128 + 32 * TC_EPI_WARPS, 1)
     tc_kvp_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                   TcArgs a) {
+  constexpr int BBOX = NT * TC_BK * 2;   // bytes of one Q box
+  constexpr int HALF = NT / 2;           // columns per epilogue warp
+  constexpr int NCH = HALF / 32;         // 32-column chunks per epilogue warp
+  static_assert(HALF % 32 == 0, "tile");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = a.stages;
   uint8_t *sA = smem;                                  // nbox x 16 KB (resident P tile)
-  uint8_t *sB = smem + a.nbox * TC_A_BOX;              // TC_STAGES x 32 KB
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sB + TC_STAGES * TC_B_BOX);
-  uint64_t *full = bars, *empty = bars + TC_STAGES, *tfull = bars + 2 * TC_STAGES,
+  uint8_t *sB = smem + a.nbox * TC_A_BOX;              // S x BBOX
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sB + S * BBOX);
+  uint64_t *full = bars, *empty = bars + TC_MAX_STAGES, *tfull = bars + 2 * TC_MAX_STAGES,
            *tempty = tfull + 2, *afull = tempty + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(afull + 1);
+  double *red = reinterpret_cast<double *>(tmem_slot + 4);  // [TC_M] fp64 half-row partials
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)blockIdx.x * TC_M;
   const int64_t qlo = (int64_t)blockIdx.y * a.q_per_split;
   const int64_t qhi = lmin(a.nq, qlo + a.q_per_split);
-  const int ntiles = qhi > qlo ? (int)cdiv<int64_t>(qhi - qlo, TC_N) : 0;
+  const int ntiles = qhi > qlo ? (int)cdiv<int64_t>(qhi - qlo, NT) : 0;
   const int nchunk = 2 * a.nk;  // valid 16-wide chunks of a packed row
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], TC_EPI_WARPS);
     }
     mbar_init(afull, 1);
     fence_mbar_init();
@@ -206,115 +309,142 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_a = tmem + 2 * NT;  // TS: P tile columns (8 per 16-wide chunk)
 
   if (warp == 0) {
-    if (lane == 0) {
-      // resident P tile (all K)
+    // TMA producer: the whole warp walks the ring, one elected lane issues the copies
+    if (elect_one()) {
       mbar_expect_tx(afull, (uint32_t)(a.nbox * TC_A_BOX));
       for (int b = 0; b < a.nbox; ++b) tma_load_2d(sA + b * TC_A_BOX, &tmP, b * TC_BK, (int)p0, afull);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = 0; t < ntiles; ++t) {
-        const int q0 = (int)(qlo + (int64_t)t * TC_N);
-        for (int b = 0; b < a.nbox; ++b) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], TC_B_BOX);
-          tma_load_2d(sB + stage * TC_B_BOX, &tmQ, b * TC_BK, q0, &full[stage]);
-          if (++stage == TC_STAGES) {
-            stage = 0;
-            phase ^= 1;
+    }
+    __syncwarp();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int q0 = (int)(qlo + (int64_t)t * NT);
+      for (int b = 0; b < a.nbox; ++b) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          if (MODE == 11) {  // diagnostic: no Q loads
+            mbar_arrive(&full[stage]);
+          } else {
+            mbar_expect_tx(&full[stage], BBOX);
+            tma_load_2d(sB + stage * BBOX, &tmQ, b * TC_BK, q0, &full[stage]);
           }
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
-      const uint32_t sA_addr = smem_u32(sA), sB_addr = smem_u32(sB);
-      auto adesc = [&](int c) {  // 16-wide chunk c of the resident A row block
-        return sw128_desc(sA_addr + (uint32_t)((c >> 2) * TC_A_BOX + (c & 3) * 32));
-      };
-      mbar_wait(afull, 0);
+    // MMA issuer: warp-uniform control flow, one elected lane issues tcgen05.mma.  The
+    // descriptors are linear in the shared-memory address (start address in the low bits),
+    // so chunk / stage offsets are plain integer adds on precomputed bases.
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(NT >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+    const uint64_t a0 = sw128_desc(smem_u32(sA)), b0 = sw128_desc(smem_u32(sB));
+    const int nk = a.nk;
+    auto adesc = [&](int c) -> uint64_t {
+      return a0 + (uint64_t)(((c >> 2) * TC_A_BOX + (c & 3) * 32) >> 4);
+    };
+    mbar_wait(afull, 0);
+    tc_fence_after();
+    if (TS) {
+      if (elect_one())
+        for (int c = 0; c < nchunk; ++c) tc_cp_128x256b(tmem_a + (uint32_t)(8 * c), adesc(c));
+      __syncwarp();
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int acc = t & 1;
+      mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
       tc_fence_after();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = 0; t < ntiles; ++t) {
-        const int acc = t & 1;
-        mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+      const uint32_t dtm = tmem + (uint32_t)(acc * NT);
+      for (int b = 0; b < a.nbox; ++b) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t dtm = tmem + (uint32_t)(acc * TC_N);
-        uint32_t accumulate = 0;
-        for (int b = 0; b < a.nbox; ++b) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
+        if (elect_one()) {
+          const uint64_t bs = b0 + (uint64_t)((stage * BBOX) >> 4);
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
             const int j = b * 4 + jj;  // chunk of the Q row held in this box
-            if (j < nchunk) {
-              const uint64_t bd = sw128_desc(sB_addr + (uint32_t)(stage * TC_B_BOX + jj * 32));
-              if (j < a.nk) {
-                tc_mma_f16(dtm, adesc(j), bd, idesc, accumulate);          // h_p . h_q
-                accumulate = 1;
-                tc_mma_f16(dtm, adesc(a.nk + j), bd, idesc, 1);            // l_p . h_q
-              } else {
-                tc_mma_f16(dtm, adesc(j - a.nk), bd, idesc, 1);            // h_p . l_q
+            if (j < nchunk && MODE != 10) {  // MODE 10: diagnostic without MMAs
+              const uint64_t bd = bs + (uint64_t)(jj * 2);  // +32 B
+              const int ca = j < nk ? j : j - nk;         // h_p chunk
+              const uint32_t first = (b | jj) ? 1u : 0u;  // first MMA of the tile overwrites
+              if (TS) tc_mma_f16_ts(dtm, tmem_a + (uint32_t)(8 * ca), bd, idesc, first);
+              else tc_mma_f16(dtm, adesc(ca), bd, idesc, first);  // h_p . h_q | h_p . l_q
+              if (j < nk) {                                        // l_p . h_q
+                if (TS) tc_mma_f16_ts(dtm, tmem_a + (uint32_t)(8 * (nk + j)), bd, idesc, 1u);
+                else tc_mma_f16(dtm, adesc(nk + j), bd, idesc, 1u);
               }
             }
           }
           tc_commit(&empty[stage]);
-          if (++stage == TC_STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        tc_commit(&tfull[acc]);
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      if (elect_one()) tc_commit(&tfull[acc]);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
-    const int row = ew * 32 + lane;
+    const int lg = ew & 3;        // TMEM lane group: warp % 4 == lg
+    const int half = ew >> 2;     // column half of the accumulator
+    const int row = lg * 32 + lane;
     const int64_t p = p0 + row;
+    const int col0 = half * HALF;
     double acc64 = 0.0;
+    uint32_t rr[2][32];
     for (int t = 0; t < ntiles; ++t) {
-      const int acc = t & 1;
-      mbar_wait(&tfull[acc], (t >> 1) & 1);
+      const int accb = t & 1;
+      mbar_wait(&tfull[accb], (t >> 1) & 1);
       tc_fence_after();
-      const int64_t q0 = qlo + (int64_t)t * TC_N;
-      const int cnt = (int)lmin(TC_N, qhi - q0);
-      const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * TC_N);
-      float accf = 0.f;
-      uint32_t r[32];
-      tmem_ld32(tbase, r);
-      tmem_wait_ld();
-      for (int c = 0; c < TC_N / 32; ++c) {
-        if (c * 32 >= cnt) break;
-        float e[32];
+      const int64_t q0 = qlo + (int64_t)t * NT;
+      const int cnt = (int)lmin(NT, qhi - q0) - col0;  // valid columns of this half
+      const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(accb * NT + col0);
+      const float *zt = a.z + q0 + col0;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      if (MODE == 9) {  // diagnostic: no TMEM traffic
 #pragma unroll
-        for (int j = 0; j < 32; ++j) e[j] = __uint_as_float(r[j]);
-        if ((c + 1) * 32 < cnt) tmem_ld32(tbase + (uint32_t)((c + 1) * 32), r);
-        const float4 *zp = reinterpret_cast<const float4 *>(a.z + q0 + c * 32);
-        const int lim = cnt - c * 32;
+        for (int j = 0; j < 32; ++j) rr[0][j] = __float_as_uint(-(float)j);
+        for (int c = 0; c * 32 < cnt; ++c) tc_epi_chunk<0, true>(rr[0], zt + c * 32, cnt - c * 32, acc);
+      } else if (cnt >= HALF) {
+        // software-pipelined: the next 32 columns load from TMEM while these are processed
+        tmem_ld32(tb, rr[0]);
+        tmem_wait_ld_regs(rr[0]);
 #pragma unroll
-        for (int g4 = 0; g4 < 8; ++g4) {
-          const float4 zz = __ldg(zp + g4);
-          const float zv[4] = {zz.x, zz.y, zz.z, zz.w};
-#pragma unroll
-          for (int e4 = 0; e4 < 4; ++e4) {
-            const int j = g4 * 4 + e4;
-            const float zj = j < lim ? zv[e4] : 0.f;
-            accf = fmaf(ex2_approx(fminf(e[j], 0.f)), zj, accf);
-          }
+        for (int c = 0; c < NCH; ++c) {
+          if (c + 1 < NCH) tmem_ld32(tb + (uint32_t)((c + 1) * 32), rr[(c + 1) & 1]);
+          tc_epi_chunk<MODE, false>(rr[c & 1], zt + c * 32, 32, acc);
+          if (c + 1 < NCH) tmem_wait_ld_regs(rr[(c + 1) & 1]);
         }
-        tmem_wait_ld();
+      } else {
+        for (int c = 0; c * 32 < cnt; ++c) {
+          tmem_ld32(tb + (uint32_t)(c * 32), rr[0]);
+          tmem_wait_ld_regs(rr[0]);
+          tc_epi_chunk<MODE, true>(rr[0], zt + c * 32, cnt - c * 32, acc);
+        }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      acc64 += (double)accf;
+      if (lane == 0) mbar_arrive(&tempty[accb]);
+      acc64 += (double)((acc[0] + acc[1]) + (acc[2] + acc[3]));
     }
-    if (p < a.np) {
-      if (a.out64) a.out64[(int64_t)blockIdx.y * a.np + p] = acc64;
-      if (a.out32) a.out32[p] = (float)acc64;
+    // combine the two column halves of each row in a fixed order (deterministic)
+    if (half == 1) red[row] = acc64;
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS) : "memory");
+    if (half == 0 && p < a.np) {
+      const double tot = acc64 + red[row];
+      if (a.out64) a.out64[(int64_t)blockIdx.y * a.np + p] = tot;
+      if (a.out32) a.out32[p] = (float)tot;
     }
   }
   tc_fence_before();
@@ -392,15 +522,22 @@ int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const floa
   pp->cb = nullptr;
   CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(pp->tmaps);
   FK_TRY(make_map(&maps[0], (const __half *)xp, n, kp, TC_M));  // X as P (pass A)
-  FK_TRY(make_map(&maps[1], (const __half *)cp, m, kp, TC_N));  // C as Q (pass A)
+  const int nt = tc_use_ts(d16) ? TC_N_TS : TC_N;
+  FK_TRY(make_map(&maps[1], (const __half *)cp, m, kp, nt));  // C as Q (pass A)
   FK_TRY(make_map(&maps[2], (const __half *)cp, m, kp, TC_M));  // C as P (pass B)
-  FK_TRY(make_map(&maps[3], (const __half *)xp, n, kp, TC_N));  // X as Q (pass B)
+  FK_TRY(make_map(&maps[3], (const __half *)xp, n, kp, nt));  // X as Q (pass B)
   return FALKON_OK;
 }
 
-static size_t tc_smem_bytes(int nbox) {
-  return 1024 + (size_t)nbox * TC_A_BOX + (size_t)TC_STAGES * TC_B_BOX + 256;
+static size_t tc_smem_bytes(int nbox, int stages, int nt) {
+  return 1024 + (size_t)nbox * TC_A_BOX + (size_t)stages * nt * TC_BK * 2 + 256 + 8 * TC_M;
 }
+static int tc_stages(int nbox, int nt) {
+  int s = 8;
+  while (s > 2 && tc_smem_bytes(nbox, s, nt) > (size_t)TC_SMEM_MAX) --s;
+  return s;
+}
+
 
 int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, double *out64,
             float *out32) {
@@ -409,16 +546,28 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   const int nbox = (int)cdiv<int64_t>(2 * d16, TC_BK);
   const int64_t np = passA ? pp.n : pp.m, nq = passA ? pp.m : pp.n;
   if (np <= 0) return FALKON_OK;
-  const size_t smem = tc_smem_bytes(nbox);
-  static bool attr = false;
-  if (!attr) {
-    FK_CUDA(cudaFuncSetAttribute(tc_kvp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)tc_smem_bytes(cdiv(2 * TC_MAX_D16, TC_BK))));
-    attr = true;
+  const bool ts = tc_use_ts(d16);
+  const int nt = ts ? TC_N_TS : TC_N;
+  const int stages = tc_stages(nbox, nt);
+  const size_t smem = tc_smem_bytes(nbox, stages, nt);
+  int mode = ctx->opt.exp_offload;
+  if (const char *e = getenv("FALKON_TC_MODE")) mode = atoi(e);  // diagnostics (8-11)
+  typedef void (*kfn)(const CUtensorMap, const CUtensorMap, TcArgs);
+  kfn fn;
+#define FK_TC(M)                                                                         \
+  case M:                                                                                \
+    fn = ts ? tc_kvp_kernel<M, TC_N_TS, true> : tc_kvp_kernel<M, TC_N, false>; \
+    break;
+  switch (mode) {
+    FK_TC(1) FK_TC(2) FK_TC(3) FK_TC(8) FK_TC(9) FK_TC(10) FK_TC(11)
+    default: fn = ts ? tc_kvp_kernel<0, TC_N_TS, true> : tc_kvp_kernel<0, TC_N, false>; break;
   }
+#undef FK_TC
+  FK_CUDA(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               TC_SMEM_MAX));
   // grid: P tiles x Q splits, sized to whole waves of one CTA per SM
   const int64_t gx = cdiv<int64_t>(np, TC_M);
-  const int64_t qt = cdiv<int64_t>(std::max<int64_t>(nq, 1), TC_N);
+  const int64_t qt = cdiv<int64_t>(std::max<int64_t>(nq, 1), nt);
   int64_t best_s = 1;
   double best_eff = -1.0;
   for (int64_t s = 1; s <= 32; ++s) {
@@ -432,7 +581,7 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
     }
     if (ctas >= 8 * ctx->sm_count && eff > 0.9) break;
   }
-  int64_t qps = round_up<int64_t>(cdiv<int64_t>(nq, best_s), TC_N);
+  int64_t qps = round_up<int64_t>(cdiv<int64_t>(nq, best_s), nt);
   const int64_t splits = std::max<int64_t>(1, cdiv<int64_t>(nq, qps));
   double *part = out64;
   if (splits > 1 || !out64) {
@@ -447,11 +596,12 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   args.q_per_split = qps;
   args.nk = d16 / 16;
   args.nbox = nbox;
+  args.stages = stages;
   args.out64 = part;
   args.out32 = splits == 1 ? out32 : nullptr;
   {
     LaunchScope ls(ctx, passA ? FALKON_T_PASS_A : FALKON_T_PASS_B);
-    tc_kvp_kernel<<<dim3((unsigned)gx, (unsigned)splits), TC_THREADS, smem, ctx->stream>>>(
+    fn<<<dim3((unsigned)gx, (unsigned)splits), TC_THREADS, smem, ctx->stream>>>(
         passA ? maps[0] : maps[2], passA ? maps[1] : maps[3], args);
   }
   FK_LAUNCH_CHECK();
