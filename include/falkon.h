@@ -142,8 +142,13 @@ int falkon_kernel_tvec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t
 
 /* ---- preconditioner (supporting machinery of the CG loop) ------------------------------ */
 
-/* Build the preconditioner into the caller-owned m x m fp64 row-major buffer `P` and the
-   two m-vectors diagT, diagA (Fig. 3):
+/* Number of fp64 elements of the `work` buffer of falkon_precond_build / _solve (the
+   inverses of the 64 x 64 diagonal blocks of T^T and A^T, 2 * ceil(m/64) * 4096). */
+int64_t falkon_precond_work_elems(int64_t m);
+
+/* Build the preconditioner into the caller-owned m x m fp64 row-major buffer `P`, the
+   two m-vectors diagT, diagA and `work` (falkon_precond_work_elems(m) doubles), all device
+   memory (Fig. 3):
      strictly-upper(P) = strictly-upper(T),  diagT = diag(T),   T^T T = Kmm + delta I
      strictly-lower(P) = strictly-lower(A^T), diagA = diag(A),  A^T A = T T^T/m + lambda I
    (T, A upper triangular; the diagonal of P is scratch).  delta = jitter (< 0: default
@@ -151,12 +156,15 @@ int falkon_kernel_tvec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t
    info->failed_factor/failed_column set when a pivot is <= 0 or non-finite. */
 int falkon_precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel,
                          double sigma, double lambda, double jitter,
-                         double *P, double *diagT, double *diagA, falkon_fit_info *info);
+                         double *P, double *diagT, double *diagA, double *work,
+                         falkon_fit_info *info);
 
 /* In-place triangular solve x <- op(F)^-1 x with F = T (which = 0) or A (which = 1) read
-   from a buffer built by falkon_precond_build; op = transpose if trans != 0. x: m fp64. */
+   from a buffer built by falkon_precond_build (with its work buffer); op = transpose if
+   trans != 0.  x: m fp64 device memory.  Stream-ordered. */
 int falkon_precond_solve(falkon_ctx *ctx, const double *P, const double *diagT,
-                         const double *diagA, int64_t m, int which, int trans, double *x);
+                         const double *diagA, const double *work, int64_t m, int which,
+                         int trans, double *x);
 
 /* ---- Falkon ---------------------------------------------------------------------------- */
 

@@ -31,7 +31,7 @@ ERRORS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ENONFINITE", 4: "ENOMEM", 5: "E
 EXPORTS = ["falkon_get_unique_id", "falkon_ctx_create", "falkon_ctx_destroy",
            "falkon_ctx_set_stream", "falkon_ctx_set_option", "falkon_ctx_timings",
            "falkon_ctx_launch_count", "falkon_knm_matvec", "falkon_kernel_vec",
-           "falkon_kernel_tvec", "falkon_precond_build", "falkon_precond_solve", "falkon_fit",
+           "falkon_kernel_tvec", "falkon_precond_work_elems", "falkon_precond_build", "falkon_precond_solve", "falkon_fit",
            "falkon_predict", "falkon_strerror", "falkon_last_error", "falkon_version"]
 
 
@@ -77,8 +77,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "falkon_knm_matvec": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
         "falkon_kernel_vec": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
         "falkon_kernel_tvec": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
-        "falkon_precond_build": (C, [P, P, I64, I64, C, D, D, D, P, P, P, P]),
-        "falkon_precond_solve": (C, [P, P, P, P, I64, C, C, P]),
+        "falkon_precond_work_elems": (I64, [I64]),
+        "falkon_precond_build": (C, [P, P, I64, I64, C, D, D, D, P, P, P, P, P]),
+        "falkon_precond_solve": (C, [P, P, P, P, P, I64, C, C, P]),
         "falkon_fit": (C, [P, P, P, I64, I64, P, I64, C, D, D, I32, D, P, P]),
         "falkon_predict": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
         "falkon_strerror": (ctypes.c_char_p, [C]),
@@ -215,25 +216,31 @@ class Context:
                                        pw, pu))
         return out
 
-    def precond_build(self, C, kernel, sigma, lam, jitter, P, diagT, diagA) -> dict:
+    @staticmethod
+    def precond_work_elems(m: int) -> int:
+        return int(_LIB.falkon_precond_work_elems(int(m)))
+
+    def precond_build(self, C, kernel, sigma, lam, jitter, P, diagT, diagA, work) -> dict:
         pc, _ = _ptr(C, "float32", "C")
         m, d = C.shape
         info = FitInfo()
         code = _LIB.falkon_precond_build(self.h, pc, m, d, _kernel_id(kernel), float(sigma),
                                          float(lam), float(jitter), _ptr(P, "float64", "P")[0],
                                          _ptr(diagT, "float64", "diagT")[0],
-                                         _ptr(diagA, "float64", "diagA")[0], ctypes.byref(info))
+                                         _ptr(diagA, "float64", "diagA")[0],
+                                         _ptr(work, "float64", "work")[0], ctypes.byref(info))
         if code != 0:
             e = FalkonError(code, (_LIB.falkon_last_error() or b"").decode())
             e.info = info.as_dict()
             raise e
         return info.as_dict()
 
-    def precond_solve(self, P, diagT, diagA, which: int, trans: bool, x):
+    def precond_solve(self, P, diagT, diagA, work, which: int, trans: bool, x):
         m = x.shape[0]
         _check(_LIB.falkon_precond_solve(self.h, _ptr(P, "float64", "P")[0],
                                          _ptr(diagT, "float64", "diagT")[0],
-                                         _ptr(diagA, "float64", "diagA")[0], m, int(which),
+                                         _ptr(diagA, "float64", "diagA")[0],
+                                         _ptr(work, "float64", "work")[0], m, int(which),
                                          int(bool(trans)), _ptr(x, "float64", "x")[0]))
         return x
 

@@ -416,27 +416,29 @@ int falkon_predict(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d, 
 }
 
 // ------------------------------------------------------------------ preconditioner API
+int64_t falkon_precond_work_elems(int64_t m) { return m > 0 ? precond_work_elems(m) : 0; }
+
 int falkon_precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel,
                          double sigma, double lambda, double jitter, double *P, double *diagT,
-                         double *diagA, falkon_fit_info *info) {
+                         double *diagA, double *work, falkon_fit_info *info) {
   FK_TRY(check_common(ctx, 0, d, m, kernel, sigma));
-  if (!C || !P || !diagT || !diagA) return fail(FALKON_EINVAL, "NULL array");
+  if (!C || !P || !diagT || !diagA || !work) return fail(FALKON_EINVAL, "NULL array");
   if (!(lambda >= 0.0) || !std::isfinite(lambda)) return fail(FALKON_EINVAL, "lambda must be >= 0");
-  if (!is_device_ptr(P) || !is_device_ptr(diagT) || !is_device_ptr(diagA))
-    return fail(FALKON_EINVAL, "P, diagT, diagA must be device memory");
+  if (!is_device_ptr(P) || !is_device_ptr(diagT) || !is_device_ptr(diagA) || !is_device_ptr(work))
+    return fail(FALKON_EINVAL, "P, diagT, diagA, work must be device memory");
   if (jitter < 0) jitter = 1e-8;
   const void *Cd;
   FK_TRY(stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd));
   return precond_build(ctx, (const float *)Cd, m, d, kernel, sigma, lambda, jitter, P, diagT, diagA,
-                       info);
+                       work, info);
 }
 
 int falkon_precond_solve(falkon_ctx *ctx, const double *P, const double *diagT, const double *diagA,
-                         int64_t m, int which, int trans, double *x) {
-  if (!ctx || !P || !diagT || !diagA || !x || m < 1 || (which != 0 && which != 1))
+                         const double *work, int64_t m, int which, int trans, double *x) {
+  if (!ctx || !P || !diagT || !diagA || !work || !x || m < 1 || (which != 0 && which != 1))
     return fail(FALKON_EINVAL, "bad arguments");
   FK_CUDA(cudaSetDevice(ctx->device));
-  return trsv(ctx, P, which == 0 ? diagT : diagA, m, which, trans, x);
+  return trsv(ctx, P, which == 0 ? diagT : diagA, work, m, which, trans, x);
 }
 
 // ------------------------------------------------------------------ Falkon fit
@@ -495,7 +497,7 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
       return fail(FALKON_ENOMEM, "preconditioner buffer of " + std::to_string(8.0 * m * m / 1e9) +
                                      " GB: " + cudaGetErrorString(e));
     }
-    e = cudaMalloc(&dT, sizeof(double) * 2 * (size_t)m);
+    e = cudaMalloc(&dT, sizeof(double) * (2 * (size_t)m + (size_t)precond_work_elems(m)));
     if (e != cudaSuccess) {
       cudaFree(P);
       for (auto &ee : ev) cudaEventDestroy(ee);
@@ -503,6 +505,7 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
     }
   }
   double *dA = dT ? dT + m : nullptr;
+  double *pw = dT ? dT + 2 * m : nullptr;  // inverse 64x64 diagonal blocks of T^T and A^T
   auto cleanup = [&]() {
     if (P) cudaFree(P);
     if (dT) cudaFree(dT);
@@ -516,7 +519,7 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
     if ((rc = stage_in(ctx, WS_STAGE_Y, y, sizeof(float) * n_local, &yd))) break;
     if ((rc = stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd))) break;
     if ((rc = precond_build(ctx, (const float *)Cd, m, d, kernel, sigma, lambda, jitter, P, dT, dA,
-                            &loc)))
+                            pw, &loc)))
       break;
     cudaEventRecord(ev[1], ctx->stream);
     // (2) RHS  R = A^-T T^-T Knm^T y   (Alg. 1 line 9)
@@ -531,8 +534,8 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
     }
     if ((rc = pass_B(ctx, F.pp, F.w32, r))) break;
     if ((rc = nccl_allreduce_f64(ctx, r, m))) break;
-    if ((rc = trsv(ctx, P, dT, m, 0, 1, r))) break;  // T^-T
-    if ((rc = trsv(ctx, P, dA, m, 1, 1, r))) break;  // A^-T
+    if ((rc = trsv(ctx, P, dT, pw, m, 0, 1, r))) break;  // T^-T
+    if ((rc = trsv(ctx, P, dA, pw, m, 1, 1, r))) break;  // A^-T
     cudaEventRecord(ev[2], ctx->stream);
     // (3) CG  (Alg. 1 line 10; reading c9)
     BRK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * m, ctx->stream));
@@ -546,16 +549,16 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
     for (int it = 1; it <= iters && rc == FALKON_OK; ++it) {
       // LinOp(p) = A^-T ( T^-T Knm^T Knm T^-1 A^-1 p + lambda n A^-1 p )   (Eq. (9))
       BRK_CUDA(cudaMemcpyAsync(t1, p, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
-      if ((rc = trsv(ctx, P, dA, m, 1, 0, t1))) break;  // t1 = A^-1 p
+      if ((rc = trsv(ctx, P, dA, pw, m, 1, 0, t1))) break;  // t1 = A^-1 p
       BRK_CUDA(cudaMemcpyAsync(t2, t1, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
-      if ((rc = trsv(ctx, P, dT, m, 0, 0, t2))) break;  // t2 = T^-1 t1
+      if ((rc = trsv(ctx, P, dT, pw, m, 0, 0, t2))) break;  // t2 = T^-1 t1
       if ((rc = product(ctx, F, t2, u))) break;          // u = Knm^T Knm t2 (allreduced)
-      if ((rc = trsv(ctx, P, dT, m, 0, 1, u))) break;   // u = T^-T u
+      if ((rc = trsv(ctx, P, dT, pw, m, 0, 1, u))) break;   // u = T^-T u
       {
         LaunchScope ls(ctx, FALKON_T_VEC);
         axpy_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(u, t1, lam_n, m);
       }
-      if ((rc = trsv(ctx, P, dA, m, 1, 1, u))) break;   // q = A^-T u
+      if ((rc = trsv(ctx, P, dA, pw, m, 1, 1, u))) break;   // q = A^-T u
       double *qv = u;
       if ((rc = dot(ctx, p, qv, m, dpart, sc + S_GAMMA))) break;
       {
@@ -575,8 +578,8 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
     cudaEventRecord(ev[3], ctx->stream);
     // (4) alpha = T^-1 A^-1 x   (Alg. 1 line 11)
     BRK_CUDA(cudaMemcpyAsync(ares, x, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
-    if ((rc = trsv(ctx, P, dA, m, 1, 0, ares))) break;
-    if ((rc = trsv(ctx, P, dT, m, 0, 0, ares))) break;
+    if ((rc = trsv(ctx, P, dA, pw, m, 1, 0, ares))) break;
+    if ((rc = trsv(ctx, P, dT, pw, m, 0, 0, ares))) break;
   } while (0);
   if (rc != FALKON_OK) {
     if (info) *info = loc;

@@ -151,10 +151,11 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
 // ------------------------------------------------------------------ preconditioner (precond.cu)
 int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel, double sigma,
                   double lambda, double jitter, double *P, double *diagT, double *diagA,
-                  falkon_fit_info *info);
-// x <- op(F)^-1 x, F = T (which 0) or A (which 1)
-int trsv(falkon_ctx *ctx, const double *P, const double *diag, int64_t m, int which, int trans,
-         double *x);
+                  double *work, falkon_fit_info *info);
+int64_t precond_work_elems(int64_t m);
+// x <- op(F)^-1 x, F = T (which 0) or A (which 1); work = the build's work buffer
+int trsv(falkon_ctx *ctx, const double *P, const double *diag, const double *work, int64_t m,
+         int which, int trans, double *x);
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {

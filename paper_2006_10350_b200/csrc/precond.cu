@@ -34,8 +34,21 @@ namespace falkon {
 constexpr int NB = 128;        // factorization block
 constexpr int GT = 128;        // GEMM CTA tile
 constexpr int GK = 16;         // GEMM k-chunk
-constexpr int GPAD = 2;        // smem row padding (doubles)
+constexpr int GSTAGES = 4;     // cp.async pipeline depth of the fp64 GEMM
+constexpr int GPAD = 8;        // smem row padding (doubles): conflict-free DMMA fragments
 constexpr int TB = 64;         // TRSV block
+
+int64_t precond_work_elems(int64_t m);
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // ------------------------------------------------------------------ views
 // Logical matrix element (r, c) of a view.  tri: 0 = dense; 1 = lower (r > c from
@@ -141,6 +154,7 @@ __global__ void __launch_bounds__(256) kmm_kernel(const float *__restrict__ C, i
 // diagonal) to `W`.  Pivot failures record the first global column in *fail.
 __global__ void __launch_bounds__(512) potrf_diag_kernel(View S, int64_t k0, int nb,
                                                          double *__restrict__ W,
+                                                         double *__restrict__ Dinv,
                                                          unsigned long long *fail) {
   extern __shared__ double sL[];  // nb x (nb+1)
   const int ld = nb + 1;
@@ -197,6 +211,18 @@ __global__ void __launch_bounds__(512) potrf_diag_kernel(View S, int64_t k0, int
     const int r = e / nb, c = e % nb;
     W[(int64_t)r * NB + c] = (r >= c) ? sL[r * ld + c] : 0.0;
   }
+  // the 64 x 64 diagonal sub-blocks of W are the inverses of the 64 x 64 diagonal blocks of
+  // L (block-triangular inverse): kept for the triangular solves of the CG loop
+  if (Dinv) {
+    for (int e = tid; e < NB * TB; e += nt) {
+      const int r = e / TB, c = e % TB;  // r in [0, 128), c in [0, 64)
+      const int h = r / TB, rr = r % TB;
+      const int gc = h * TB + c;
+      double v = 0.0;
+      if (r < nb && gc < nb && rr >= c) v = sL[r * ld + gc];
+      if (h * TB < nb) Dinv[(k0 / TB + h) * (int64_t)(TB * TB) + rr * TB + c] = v;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ fp64 GEMM through views
@@ -248,6 +274,133 @@ __device__ __forceinline__ void gemm_store_chunk(const View &v, double (*s)[GT +
   }
 }
 
+// Asynchronous (cp.async, LDGSTS) staging of a GT x GK chunk of a view into shared memory:
+// masked elements are zero-filled (src-size 0), diagonal elements read from the view's dvec.
+__device__ __forceinline__ void cp_async8z(void *smem, const void *gmem, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ const double *vsrc(const View &v, int64_t r, int64_t c, bool &valid) {
+  if (v.tri == 1) {
+    if (r < c) { valid = false; return v.base; }
+    if (r == c) { valid = true; return v.dvec + r; }
+  } else if (v.tri == 2) {
+    if (c < r) { valid = false; return v.base; }
+    if (r == c) { valid = true; return v.dvec + r; }
+  }
+  valid = true;
+  return v.base + vidx(v, r, c);
+}
+// true iff every element (r, c), r in [r0, r0+nr), c in [c0, c0+nc) lies in the stored
+// (strict) triangle of the view, i.e. needs neither masking nor the diagonal vector
+__device__ __forceinline__ bool view_dense(const View &v, int64_t r0, int64_t nr, int64_t c0,
+                                           int64_t nc) {
+  if (v.tri == 1) return r0 > c0 + nc - 1;
+  if (v.tri == 2) return c0 > r0 + nr - 1;
+  return true;
+}
+// masked / diagonal-touching chunks (rare): kept out of line to keep the hot loop small
+__device__ __noinline__ void gemm_async_chunk_masked(const View v, double (*s)[GT + GPAD],
+                                                     int64_t row0, int64_t rmax, int64_t k,
+                                                     int64_t kmax) {
+  const int tid = threadIdx.x;
+  if (!v.trans) {
+    const int kk = tid & 15, rr = tid >> 4;
+    for (int p = 0; p < 8; ++p) {
+      const int64_t r = row0 + rr + 16 * p, kg = k + kk;
+      bool ok = r < rmax && kg < kmax;
+      const double *src = ok ? vsrc(v, r, kg, ok) : v.base;
+      cp_async8z(&s[kk][rr + 16 * p], src, ok);
+    }
+  } else {
+    const int rr = tid & 127, kk = tid >> 7;
+    for (int p = 0; p < 8; ++p) {
+      const int64_t r = row0 + rr, kg = k + kk + 2 * p;
+      bool ok = r < rmax && kg < kmax;
+      const double *src = ok ? vsrc(v, r, kg, ok) : v.base;
+      cp_async8z(&s[kk + 2 * p][rr], src, ok);
+    }
+  }
+}
+
+__device__ __forceinline__ void gemm_async_chunk(const View &v, double (*s)[GT + GPAD],
+                                                 int64_t row0, int64_t rmax, int64_t k,
+                                                 int64_t kmax) {
+  const int tid = threadIdx.x;
+  if (view_dense(v, row0, GT, k, GK)) {
+    // branch-free: out-of-range rows/columns are zero-filled from a clamped address
+    if (!v.trans) {
+      const int kk = tid & 15, rr = tid >> 4;
+      const int64_t kg = k + kk;
+      const bool kok = kg < kmax;
+      const int64_t kc = kok ? kg : k;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int64_t r = row0 + rr + 16 * p;
+        const bool ok = kok && r < rmax;
+        cp_async8z(&s[kk][rr + 16 * p], v.base + (ok ? r : row0) * v.ld + kc, ok);
+      }
+    } else {
+      const int rr = tid & 127, kk = tid >> 7;
+      const int64_t r = row0 + rr;
+      const bool rok = r < rmax;
+      const int64_t rc = rok ? r : row0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int64_t kg = k + kk + 2 * p;
+        const bool ok = rok && kg < kmax;
+        cp_async8z(&s[kk + 2 * p][rr], v.base + (ok ? kg : k) * v.ld + rc, ok);
+      }
+    }
+    return;
+  }
+  gemm_async_chunk_masked(v, s, row0, rmax, k, kmax);
+}
+
+__device__ __noinline__ void gemm_epilogue(const GemmArgs a, const double *sC, int64_t i0,
+                                           int64_t j0) {
+  constexpr int CLD = GT + 1;
+  constexpr int BATCH = 8;  // independent reads in flight per thread
+  for (int e0 = threadIdx.x; e0 < GT * GT; e0 += BATCH * blockDim.x) {
+    double cv[BATCH];
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const int li_t = a.C.trans ? (e % GT) : (e / GT);
+      const int lj_t = a.C.trans ? (e / GT) : (e % GT);
+      const int64_t li = i0 + li_t, lj = j0 + lj_t;
+      cv[u] = 0.0;
+      if (e < GT * GT && li < a.M && lj < a.N && a.beta != 0.0)
+        cv[u] = vget(a.C, a.rc + li, a.cc + lj);
+    }
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      // storage order: consecutive threads walk the contiguous dimension of C's storage
+      const int e = e0 + u * blockDim.x;
+      const int li_t = a.C.trans ? (e % GT) : (e / GT);
+      const int lj_t = a.C.trans ? (e / GT) : (e % GT);
+      const int64_t li = i0 + li_t, lj = j0 + lj_t;
+      if (e >= GT * GT || li >= a.M || lj >= a.N) continue;
+      const int64_t r = a.rc + li, c = a.cc + lj;
+      if (a.C.tri == 1 && r < c) continue;
+      if (a.C.tri == 2 && c < r) continue;
+      vset(a.C, r, c, a.alpha * sC[li_t * CLD + lj_t] + a.beta * cv[u]);
+    }
+  }
+}
+
+// D(8x8) += A(8x4) B(4x8) on the FP64 tensor path (DMMA).  Fragments (lane t):
+//   a = A[t/4][t%4], b = B[t%4][t/4], d = {D[t/4][2(t%4)], D[t/4][2(t%4)+1]}
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// CTA tile 128 x 128, 8 warps (4 x 2), warp tile 32 x 64 = 4 x 8 DMMA tiles; per k4 step a
+// warp loads 12 fragments from shared memory for 32 MMAs.  k-chunks of GK are staged
+// global -> registers -> shared (double-buffered) through the views.
 __global__ void __launch_bounds__(256) gemm_f64_kernel(GemmArgs a) {
   int64_t ti, tj;
   if (a.tri_tiles) {
@@ -262,86 +415,110 @@ __global__ void __launch_bounds__(256) gemm_f64_kernel(GemmArgs a) {
   }
   const int64_t i0 = ti * GT, j0 = tj * GT;
   if (i0 >= a.M || j0 >= a.N) return;
-  const int64_t kb = a.k_from_row ? max(a.k0, a.ra + i0) : a.k0;
+  const int64_t kb = a.k_from_row ? lmax(a.k0, a.ra + i0) : a.k0;
   const int64_t ke = a.k1;
 
   extern __shared__ __align__(16) double gsm[];
   double(*As)[GK][GT + GPAD] = reinterpret_cast<double(*)[GK][GT + GPAD]>(gsm);
-  double(*Bs)[GK][GT + GPAD] = reinterpret_cast<double(*)[GK][GT + GPAD]>(gsm + 2 * GK * (GT + GPAD));
+  double(*Bs)[GK][GT + GPAD] =
+      reinterpret_cast<double(*)[GK][GT + GPAD]>(gsm + GSTAGES * GK * (GT + GPAD));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int rbase = (warp >> 1) * 32 + (lane >> 3) * 8;
-  const int cbase = (warp & 1) * 64 + (lane & 7) * 8;
-  double acc[8][8];
+  const int wr = warp >> 1, wc = warp & 1;
+  const int g = lane >> 2, q = lane & 3;
+  double acc[4][8][2];
+  // Tiles strictly inside C's triangle (the vast majority) accumulate on top of C itself:
+  // acc starts at (beta/alpha) C, loaded here so the loads overlap the pipeline fill, and the
+  // epilogue is a plain store of alpha * acc (no read-modify-write round trips).
+  const bool cdense = view_dense(a.C, a.rc + i0, GT, a.cc + j0, GT) && i0 + GT <= a.M &&
+                      j0 + GT <= a.N;
+  const int64_t csr = a.C.trans ? 1 : a.C.ld, csc = a.C.trans ? a.C.ld : 1;
+  double *cfrag = a.C.base + (a.rc + i0 + wr * 32 + g) * csr + (a.cc + j0 + wc * 64 + 2 * q) * csc;
+  if (cdense && a.beta != 0.0) {
+    const double sb = a.beta / a.alpha;
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[mt][nt][h] = sb * cfrag[(mt * 8) * csr + (nt * 8 + h) * csc];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  }
 
   const int64_t ra = a.ra + i0, rb = a.rb + j0;
   const int64_t ramax = a.ra + a.M, rbmax = a.rb + a.N;
-  double ra_reg[8], rb_reg[8];
-  int st = 0;
-  if (kb < ke) {
-    gemm_load_chunk(a.A, ra, ramax, kb, ke, ra_reg);
-    gemm_load_chunk(a.B, rb, rbmax, kb, ke, rb_reg);
-    gemm_store_chunk(a.A, As[0], ra_reg);
-    gemm_store_chunk(a.B, Bs[0], rb_reg);
+  const int nch = ke > kb ? (int)cdiv<int64_t>(ke - kb, GK) : 0;
+  // GSTAGES-deep cp.async pipeline: chunk c+GSTAGES-1 loads while chunk c is multiplied
+#pragma unroll
+  for (int c = 0; c < GSTAGES - 1; ++c) {
+    if (c < nch) {
+      gemm_async_chunk(a.A, As[c], ra, ramax, kb + (int64_t)c * GK, ke);
+      gemm_async_chunk(a.B, Bs[c], rb, rbmax, kb + (int64_t)c * GK, ke);
+    }
+    cp_async_commit();
+  }
+  for (int c = 0; c < nch; ++c) {
+    cp_async_wait<GSTAGES - 2>();
+    __syncthreads();
+    {
+      const int cn = c + GSTAGES - 1;
+      if (cn < nch) {
+        gemm_async_chunk(a.A, As[cn % GSTAGES], ra, ramax, kb + (int64_t)cn * GK, ke);
+        gemm_async_chunk(a.B, Bs[cn % GSTAGES], rb, rbmax, kb + (int64_t)cn * GK, ke);
+      }
+      cp_async_commit();
+    }
+    const int st = c % GSTAGES;
+#pragma unroll
+    for (int ks = 0; ks < GK / 4; ++ks) {
+      double af[4], bf[8];
+      const double *arow = &As[st][ks * 4 + q][wr * 32 + g];
+      const double *brow = &Bs[st][ks * 4 + q][wc * 64 + g];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) af[mt] = arow[mt * 8];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) bf[nt] = brow[nt * 8];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) dmma_8x8x4(acc[mt][nt], af[mt], bf[nt]);
+    }
+  }
+  cp_async_wait<0>();
+  // epilogue: the accumulator tile is staged in shared memory (the pipeline buffers are
+  // free now), then written through the C view in storage order (coalesced), with the
+  // view's triangle mask and diagonal vector applied element-wise.
+  if (cdense) {
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          cfrag[(mt * 8) * csr + (nt * 8 + h) * csc] = a.alpha * acc[mt][nt][h];
+    return;
   }
   __syncthreads();
-  for (int64_t k = kb; k < ke; k += GK) {
-    const bool more = k + GK < ke;
-    if (more) {
-      gemm_load_chunk(a.A, ra, ramax, k + GK, ke, ra_reg);
-      gemm_load_chunk(a.B, rb, rbmax, k + GK, ke, rb_reg);
-    }
+  double *sC = gsm;  // [GT][GT + 1]
+  constexpr int CLD = GT + 1;
 #pragma unroll
-    for (int kk = 0; kk < GK; ++kk) {
-      double av[8], bv[8];
-      const double2 *pa = reinterpret_cast<const double2 *>(&As[st][kk][rbase]);
-      const double2 *pb = reinterpret_cast<const double2 *>(&Bs[st][kk][cbase]);
+  for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double2 x = pa[q], y = pb[q];
-        av[2 * q] = x.x;
-        av[2 * q + 1] = x.y;
-        bv[2 * q] = y.x;
-        bv[2 * q + 1] = y.y;
-      }
+    for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
-    }
-    if (more) {
-      gemm_store_chunk(a.A, As[st ^ 1], ra_reg);
-      gemm_store_chunk(a.B, Bs[st ^ 1], rb_reg);
-    }
-    __syncthreads();
-    st ^= 1;
-  }
-  // epilogue through the C view (masked by its triangle)
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t li = i0 + rbase + i;
-    if (li >= a.M) continue;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t lj = j0 + cbase + j;
-      if (lj >= a.N) continue;
-      const int64_t r = a.rc + li, c = a.cc + lj;
-      if (a.C.tri == 1 && r < c) continue;
-      if (a.C.tri == 2 && c < r) continue;
-      double x = a.alpha * acc[i][j];
-      if (a.beta != 0.0) x += a.beta * vget(a.C, r, c);
-      vset(a.C, r, c, x);
-    }
-  }
+      for (int h = 0; h < 2; ++h)
+        sC[(wr * 32 + mt * 8 + g) * CLD + wc * 64 + nt * 8 + 2 * q + h] = acc[mt][nt][h];
+  __syncthreads();
+  gemm_epilogue(a, sC, i0, j0);
 }
 
 static int gemm(falkon_ctx *ctx, const GemmArgs &a) {
   if (a.M <= 0 || a.N <= 0) return FALKON_OK;
-  const size_t smem = sizeof(double) * 4 * GK * (GT + GPAD);
+  const size_t smem = sizeof(double) * 2 * GSTAGES * GK * (GT + GPAD);
   static bool attr_set = false;
   if (!attr_set) {
     FK_CUDA(cudaFuncSetAttribute(gemm_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -360,7 +537,8 @@ static int gemm(falkon_ctx *ctx, const GemmArgs &a) {
 }
 
 // ------------------------------------------------------------------ blocked Cholesky
-static int potrf(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, unsigned long long *fail) {
+static int potrf(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, double *Dinv,
+                 unsigned long long *fail) {
   const size_t dsm = sizeof(double) * NB * (NB + 1);
   static bool attr_set = false;
   if (!attr_set) {
@@ -373,7 +551,7 @@ static int potrf(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, unsigned long
     const int nb = (int)std::min<int64_t>(NB, m - k0);
     {
       LaunchScope ls(ctx, FALKON_T_PRECOND);
-      potrf_diag_kernel<<<1, 512, dsm, ctx->stream>>>(S, k0, nb, Wbuf, fail);
+      potrf_diag_kernel<<<1, 512, dsm, ctx->stream>>>(S, k0, nb, Wbuf, Dinv, fail);
     }
     FK_LAUNCH_CHECK();
     const int64_t k1 = k0 + nb, rem = m - k1;
@@ -425,7 +603,8 @@ __global__ void add_diag_kernel(double *dvec, int64_t m, double scale, double ad
 
 int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel, double sigma,
                   double lambda, double jitter, double *P, double *diagT, double *diagA,
-                  falkon_fit_info *info) {
+                  double *work, falkon_fit_info *info) {
+  double *dinvT = work, *dinvA = work ? work + precond_work_elems(m) / 2 : nullptr;
   void *flags, *wb;
   FK_TRY(ws_get(ctx, WS_FLAGS, 64, &flags));
   FK_TRY(ws_get(ctx, WS_PW, sizeof(double) * NB * NB, &wb));
@@ -443,7 +622,7 @@ int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int ker
   }
   FK_LAUNCH_CHECK();
   // (c) T
-  FK_TRY(potrf(ctx, L1, m, (double *)wb, failf));
+  FK_TRY(potrf(ctx, L1, m, (double *)wb, dinvT, failf));
   // (d) M = T T^T / m + lambda I  -> lower triangle + diagA:  M(i,j) = sum_{k>=i} T(i,k) T(j,k)
   {
     GemmArgs g{};
@@ -465,7 +644,7 @@ int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int ker
   }
   FK_LAUNCH_CHECK();
   // (e) A^T
-  FK_TRY(potrf(ctx, L2, m, (double *)wb, failf + 1));
+  FK_TRY(potrf(ctx, L2, m, (double *)wb, dinvA, failf + 1));
   unsigned long long hf[2];
   FK_CUDA(cudaMemcpyAsync(hf, failf, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
   FK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -488,19 +667,49 @@ int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int ker
 }
 
 // ------------------------------------------------------------------ sync-free blocked TRSV
-// Solves L z = r (forward) or L^T z = r (backward) in place for the lower-triangular view L.
-// CTA with ticket b owns row block I (forward: I = b, backward: I = nb-1-b).  Off-diagonal
-// tiles are streamed from HBM as soon as the needed z_J is flagged ready; the 64 x 64
-// diagonal block is then solved by one warp.  flags[J] == gen marks z_J final.
+// Solves L z = r (forward) or L^T z = r (backward) in place for the lower-triangular view L,
+// with Dinv = the inverses of L's 64 x 64 diagonal blocks (written by the factorization).
+// CTA with ticket b owns row block I (forward: I = b, backward: I = nb-1-b): it streams its
+// off-diagonal 64 x 64 tiles from HBM into shared memory with cp.async one tile ahead of the
+// dependency front, multiplies each by z_J as soon as flags[J] == gen, then finishes its
+// block with the 64 x 64 inverse (a parallel mat-vec, no sequential substitution), so the
+// serial chain per block is a few L2 round trips and the solve streams at HBM rate.
+constexpr int TS_LD = TB + 2;  // smem row stride (doubles), 16 B aligned rows
+
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+// copy a 64 x 64 stored block (rows of 64 contiguous doubles, leading dimension ld) to smem;
+// 16-byte copies when every row start is 16-byte aligned (even ld), else 8-byte copies
+__device__ __forceinline__ void tile_async(double *dst, const double *src, int64_t ld, int rows,
+                                           int cols) {
+  if ((ld & 1) == 0) {
+    for (int e = threadIdx.x; e < TB * (TB / 2); e += blockDim.x) {
+      const int r = e / (TB / 2), c2 = (e % (TB / 2)) * 2;
+      if (r < rows && c2 < cols) cp_async16(dst + r * TS_LD + c2, src + (int64_t)r * ld + c2);
+    }
+  } else {
+    for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
+      const int r = e / TB, c = e % TB;
+      if (r < rows && c < cols) cp_async8(dst + r * TS_LD + c, src + (int64_t)r * ld + c);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) trsv_kernel(View L, int64_t m, int forward,
                                                    double *__restrict__ z,
+                                                   const double *__restrict__ Dinv,
                                                    unsigned int *__restrict__ counter,
                                                    unsigned int *__restrict__ flags,
                                                    unsigned int gen) {
+  extern __shared__ __align__(16) double tsm[];
+  double *sT[2] = {tsm, tsm + TB * TS_LD};
+  double *sD = tsm + 2 * TB * TS_LD;
+  double *sz = sD + TB * TS_LD;     // [TB] z_J
+  double *sx = sz + TB;             // [TB] rhs - acc
   __shared__ unsigned int s_ticket;
-  __shared__ double szj[TB];
-  __shared__ double part[4][TB];
-  __shared__ double sdiag[TB][TB + 1];
   const int tid = threadIdx.x;
   const int64_t nblk = cdiv<int64_t>(m, TB);
   if (tid == 0) s_ticket = atomicAdd(counter, 1u);
@@ -509,19 +718,40 @@ __global__ void __launch_bounds__(256) trsv_kernel(View L, int64_t m, int forwar
   const int64_t I = forward ? b : nblk - 1 - b;
   const int64_t i0 = I * TB;
   const int nI = (int)lmin(TB, m - i0);
-  // preload the diagonal tile: sdiag[i][j] = L(i0+i, i0+j) for i >= j
-  for (int e = tid; e < TB * TB; e += 256) {
-    const int i = e / TB, j = e % TB;
-    sdiag[i][j] = (i < nI && j < nI && i >= j) ? vget(L, i0 + i, i0 + j) : 0.0;
-  }
-  // thread -> (row i, quarter q) of the off-diagonal tile mat-vec
-  const int ri = tid & 63, q = tid >> 6;
-  double acc = 0.0;
+  // output row index ii is the stored row of each tile iff (forward && !trans) || (!forward && trans)
+  const bool rowmaj = (forward != 0) == (L.trans == 0);
+  auto tile_src = [&](int64_t j0) -> const double * {
+    return rowmaj ? L.base + i0 * L.ld + j0 : L.base + j0 * L.ld + i0;
+  };
   const int64_t nJ = forward ? I : nblk - 1 - I;
-  for (int64_t s = 0; s < nJ; ++s) {
-    const int64_t J = forward ? s : nblk - 1 - s;
-    const int64_t j0 = J * TB;
+  auto Jof = [&](int64_t s) { return forward ? s : nblk - 1 - s; };
+  // prologue: inverse diagonal block + first tile
+  {
+    const double *dsrc = Dinv + I * (int64_t)(TB * TB);
+    for (int e = tid; e < TB * (TB / 2); e += blockDim.x) {
+      const int r = e / (TB / 2), c2 = (e % (TB / 2)) * 2;
+      cp_async16(sD + r * TS_LD + c2, dsrc + r * TB + c2);
+    }
+  }
+  if (nJ > 0) {
+    const int64_t j0 = Jof(0) * TB;
     const int nJc = (int)lmin(TB, m - j0);
+    tile_async(sT[0], tile_src(j0), L.ld, rowmaj ? nI : nJc, rowmaj ? nJc : nI);
+  }
+  cp_async_commit();
+  // mat-vec thread mapping (conflict-free for both smem orientations)
+  const int ri = rowmaj ? (tid >> 2) : (tid & 63);
+  const int qq = rowmaj ? (tid & 3) : (tid >> 6);
+  double acc = 0.0;
+  for (int64_t s = 0; s < nJ; ++s) {
+    const int64_t J = Jof(s), j0 = J * TB;
+    const int nJc = (int)lmin(TB, m - j0);
+    if (s + 1 < nJ) {
+      const int64_t j1 = Jof(s + 1) * TB;
+      const int n1 = (int)lmin(TB, m - j1);
+      tile_async(sT[(s + 1) & 1], tile_src(j1), L.ld, rowmaj ? nI : n1, rowmaj ? n1 : nI);
+    }
+    cp_async_commit();
     if (tid == 0) {
       volatile unsigned int *f = flags + J;
       while (*f != gen) {
@@ -529,69 +759,65 @@ __global__ void __launch_bounds__(256) trsv_kernel(View L, int64_t m, int forwar
       __threadfence();
     }
     __syncthreads();
-    if (tid < TB) szj[tid] = (tid < nJc) ? ((volatile double *)z)[j0 + tid] : 0.0;
+    if (tid < TB) sz[tid] = (tid < nJc) ? __ldcg(z + j0 + tid) : 0.0;
+    cp_async_wait<1>();
     __syncthreads();
+    const double *T = sT[s & 1];
     if (ri < nI) {
-      // forward: acc_i += L(i0+ri, j0+j) z_j ; backward: acc_i += L(j0+j, i0+ri) z_j
-      for (int jj = 0; jj < 16; ++jj) {
-        const int j = q * 16 + jj;
-        if (j < nJc) {
-          const double lv = forward ? L.base[vidx(L, i0 + ri, j0 + j)]
-                                    : L.base[vidx(L, j0 + j, i0 + ri)];
-          acc = fma(lv, szj[j], acc);
+      if (rowmaj) {
+#pragma unroll
+        for (int k = 0; k < TB / 4; ++k) {
+          const int jj = qq + 4 * k;
+          if (jj < nJc) acc = fma(T[ri * TS_LD + jj], sz[jj], acc);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < TB / 4; ++k) {
+          const int jj = qq * (TB / 4) + k;
+          if (jj < nJc) acc = fma(T[jj * TS_LD + ri], sz[jj], acc);
         }
       }
     }
     __syncthreads();
   }
-  part[q][ri] = acc;
+  cp_async_wait<0>();
+  // reduce the 4 partial sums of each row, form x = r_I - acc
+  double *part = sT[0];  // reuse: [4][TB]
   __syncthreads();
-  // one warp solves the diagonal block: rows 2*lane, 2*lane+1
-  if (tid < 32) {
-    const int lane = tid;
-    double x[2];
-    for (int h = 0; h < 2; ++h) {
-      const int i = 2 * lane + h;
-      x[h] = (i < nI) ? z[i0 + i] - (part[0][i] + part[1][i] + part[2][i] + part[3][i]) : 0.0;
+  part[qq * TB + ri] = acc;
+  __syncthreads();
+  if (tid < TB)
+    sx[tid] = (tid < nI) ? z[i0 + tid] - (part[tid] + part[TB + tid] + part[2 * TB + tid] +
+                                         part[3 * TB + tid])
+                         : 0.0;
+  __syncthreads();
+  // z_I = D x (forward, D = Dinv_I) or D^T x (backward)
+  {
+    const int r = tid & 63, q4 = tid >> 6;
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < TB / 4; ++k) {
+      const int c = q4 * (TB / 4) + k;
+      v = fma(forward ? sD[r * TS_LD + c] : sD[c * TS_LD + r], sx[c], v);
     }
-    if (forward) {
-      for (int j = 0; j < nI; ++j) {
-        const int owner = j >> 1;
-        double xj = __shfl_sync(0xffffffffu, (j & 1) ? x[1] : x[0], owner);
-        xj /= sdiag[j][j];
-        if (lane == owner) x[j & 1] = xj;
-        for (int h = 0; h < 2; ++h) {
-          const int i = 2 * lane + h;
-          if (i > j && i < nI) x[h] -= sdiag[i][j] * xj;
-        }
-      }
-    } else {
-      for (int j = nI - 1; j >= 0; --j) {
-        const int owner = j >> 1;
-        double xj = __shfl_sync(0xffffffffu, (j & 1) ? x[1] : x[0], owner);
-        xj /= sdiag[j][j];
-        if (lane == owner) x[j & 1] = xj;
-        for (int h = 0; h < 2; ++h) {
-          const int i = 2 * lane + h;
-          if (i < j) x[h] -= sdiag[j][i] * xj;  // (L^T)(i, j) = L(j, i)
-        }
-      }
-    }
-    for (int h = 0; h < 2; ++h) {
-      const int i = 2 * lane + h;
-      if (i < nI) z[i0 + i] = x[h];
-    }
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) atomicExch(flags + I, gen);
+    __syncthreads();
+    part[q4 * TB + r] = v;
   }
+  __syncthreads();
+  if (tid < nI) z[i0 + tid] = part[tid] + part[TB + tid] + part[2 * TB + tid] + part[3 * TB + tid];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) atomicExch(flags + I, gen);
 }
 
-int trsv(falkon_ctx *ctx, const double *P, const double *diag, int64_t m, int which, int trans,
-         double *x) {
+int64_t precond_work_elems(int64_t m) { return 2 * cdiv<int64_t>(m, TB) * (int64_t)(TB * TB); }
+
+int trsv(falkon_ctx *ctx, const double *P, const double *diag, const double *work, int64_t m,
+         int which, int trans, double *x) {
   // which 0: T = L1^T (L1 = view trans=1 of the upper triangle); which 1: A = L2^T.
   // T x = r  <=> L1^T x = r (backward);  T^T x = r <=> L1 x = r (forward); same for A.
   View L{const_cast<double *>(P), m, which == 0 ? 1 : 0, 1, const_cast<double *>(diag)};
+  const double *dinv = work + (which == 0 ? 0 : precond_work_elems(m) / 2);
   const int forward = trans ? 1 : 0;
   const int64_t nblk = cdiv<int64_t>(m, TB);
   void *fl;
@@ -601,9 +827,16 @@ int trsv(falkon_ctx *ctx, const double *P, const double *diag, int64_t m, int wh
   static unsigned int gen_counter = 0;  // monotone generation id (flags never need clearing)
   unsigned int gen = ++gen_counter;
   if (gen == 0) gen = ++gen_counter;
+  const size_t smem = sizeof(double) * (3 * TB * TS_LD + 2 * TB);
+  static bool attr = false;
+  if (!attr) {
+    FK_CUDA(cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
   FK_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), ctx->stream));
   LaunchScope ls(ctx, FALKON_T_TRSV);
-  trsv_kernel<<<(unsigned)nblk, 256, 0, ctx->stream>>>(L, m, forward, x, counter, flags, gen);
+  trsv_kernel<<<(unsigned)nblk, 256, smem, ctx->stream>>>(L, m, forward, x, dinv, counter, flags,
+                                                          gen);
   FK_LAUNCH_CHECK();
   return FALKON_OK;
 }

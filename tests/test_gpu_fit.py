@@ -23,11 +23,12 @@ def _build(ctx, C, kernel, sigma, lam, jitter):
     m = C.shape[0]
     P = torch.zeros((m, m), dtype=torch.float64, device="cuda")
     dT, dA = zeros(m), zeros(m)
-    info = ctx.precond_build(dev(C), kernel, sigma, lam, jitter, P, dT, dA)
+    W = zeros(ctx.precond_work_elems(m))
+    info = ctx.precond_build(dev(C), kernel, sigma, lam, jitter, P, dT, dA, W)
     Ph, dTh, dAh = host(P), host(dT), host(dA)
     T = np.triu(Ph, 1) + np.diag(dTh)
     A = (np.tril(Ph, -1) + np.diag(dAh)).T
-    return T, A, (P, dT, dA), info
+    return T, A, (P, dT, dA, W), info
 
 
 @pytest.mark.parametrize("m,d,kernel,sigma", [(100, 8, G, 1.0), (300, 9, G, 1.0),
@@ -64,15 +65,15 @@ def test_preconditioner_not_pd(ctx):
     assert e.value.info["failed_column"] == 1
 
 
-@pytest.mark.parametrize("m", [100, 300, 1000])
+@pytest.mark.parametrize("m", [100, 300, 1000, 2085])
 def test_triangular_solves(ctx, m):
     C = synth.gen_X(m, 0, m, 9)
-    T, A, (P, dT, dA), _ = _build(ctx, C, G, 1.0, 1e-6, 1e-8)
+    T, A, (P, dT, dA, W), _ = _build(ctx, C, G, 1.0, 1e-6, 1e-8)
     rng = np.random.default_rng(m)
     for which, F in ((0, T), (1, A)):
         for trans in (False, True):
             b = rng.standard_normal(m)
-            x = host(ctx.precond_solve(P, dT, dA, which, trans, dev(b)))
+            x = host(ctx.precond_solve(P, dT, dA, W, which, trans, dev(b)))
             ref = sla.solve_triangular(F, b, lower=False, trans="T" if trans else "N")
             assert rel_l2(x, ref) <= 1e-10
 
