@@ -157,6 +157,55 @@ def kt_path_tensor(args, d):
     return args.path == "tensor" or d > 32
 
 
+def roofline(args, cfg, kt, ms_total, n_local, m, sms):
+    """Roofline of the dominant kernel (the pass with the larger device time in the timed
+    region; both passes evaluate every Knm entry once).  Algorithmic work per launch and
+    per entry is SURVEY.md §8(d): the cross term x.c is 2d flops; the exp, bias and
+    contraction are 1 exp + 5 flops.
+
+    * tensor path (Gaussian, d > 32): bound "tensor".  The cross term must be fp32-accurate
+      (fp16/TF32 single pass fails parity), which tcgen05 delivers as three fp16
+      MMAs (fp16x3).  peak = measured bf16/fp16 dense peak / 3 (the fp32-class rate of the
+      tensor cores); achieved = 2*d*n*m / kernel time.  `issued_frac` also reports the issued
+      fp16 MMA work (3 terms x padded K) against the plain fp16 peak.
+    * SIMT path (d <= 32): bound "alu".  Per entry the FP32 pipe executes d FFMA + 1 FADD + 1
+      FFMA and the MUFU 1 ex2; peak = min over the two pipes of unit rate x 148 SMs x clock
+      (B200: 128 FP32 lanes, 16 MUFU/clk per SM; clock = sm_max_mhz)."""
+    peaks, peak_src = measured_peaks()
+    dom = max(("pass_a", "pass_b"), key=lambda k: kt[k][0])
+    dom_ms = kt[dom][0] / max(1, kt[dom][1])
+    evals = n_local * m
+    d = cfg.d
+    f_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(f"{cfg.name}:{dom}:{n_local}:{m}")
+    common = {"kernel": dom, "kernel_ms": dom_ms, "launches": kt[dom][1],
+              "share_of_step": kt[dom][0] / ms_total if ms_total else None,
+              "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)"}
+    if kt_path_tensor(args, d):
+        d16 = -(-(d + 2) // 16) * 16
+        peak_tf = float(peaks["bf16_tflops"]) / 3.0
+        ach_tf = 2.0 * d * evals / (dom_ms * 1e-3) / 1e12
+        issued_tf = 3 * 2.0 * d16 * evals / (dom_ms * 1e-3) / 1e12
+        return {"bound": "tensor", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": ach_tf / peak_tf,
+                "peak_source": f"{peak_src} bf16 dense {peaks['bf16_tflops']} TF/s / 3 "
+                               "(fp16x3 = fp32-class cross term)",
+                "issued_frac": issued_tf / float(peaks["bf16_tflops"]),
+                "evals_per_s": evals / (dom_ms * 1e-3), **common}
+    fp32 = sms * 128 * f_hz / (d + 2)
+    mufu = sms * 16 * f_hz
+    peak, pipe = min((fp32, "fp32"), (mufu, "mufu"))
+    ach = evals / (dom_ms * 1e-3)
+    return {"bound": "alu", "pipe": pipe, "achieved": ach / 1e9, "peak": peak / 1e9,
+            "unit": "G kernel-evals/s", "frac": ach / peak,
+            "peak_source": f"{peak_src} sm_max_mhz {f_hz/1e6:.0f} MHz x {sms} SM x "
+                           "(128 FP32 lanes/(d+2) | 16 MUFU) per clk", **common}
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -207,16 +256,13 @@ def main():
     import torch.distributed as dist
     from paper_2006_10350_b200 import binding
 
+    from paper_2006_10350_b200 import parallel
+
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        obj = [binding.get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctx = binding.Context(device=local, rank=rank, world=world, unique_id=obj[0])
-    else:
-        ctx = binding.Context(device=local)
     stream = torch.cuda.current_stream()
-    ctx.set_stream(stream)
+    ctx = parallel.make_context(local, world, rank, stream=stream)
     ctx.set_option(binding.OPT_PATH, {"auto": 0, "simt": 1, "tensor": 2}[args.path])
     if args.exp_offload is not None:
         ctx.set_option(binding.OPT_EXP_OFFLOAD, args.exp_offload)
@@ -271,33 +317,8 @@ def main():
     value = n_global * m / (ms_step * 1e-3)
 
     # ---- roofline of the dominant kernel (device-timed inside the timed region) ----
-    peaks, peak_src = measured_peaks()
-    dom = max(("pass_a", "pass_b"), key=lambda k: kt[k][0])
-    dom_ms = kt[dom][0] / max(1, kt[dom][1])
-    evals = n_local * m  # algorithmic units per launch of either pass (one kernel eval each)
-    f_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    sms = torch.cuda.get_device_properties(local).multi_processor_count
-    d = cfg.d
-    path = "tensor" if kt_path_tensor(args, d) else "simt"
-    if path == "simt":
-        # FP32 pipe: d FMA (cross term) + 1 FADD (bias) + 1 FFMA (contraction) per entry
-        # (Laplacian: 2d); MUFU: 1 ex2 per entry.  Binding pipe = the slower.
-        fp32_peak = sms * 128 * f_hz / (d + 2)
-        mufu_peak = sms * 16 * f_hz
-        peak_evals, pipe = min((fp32_peak, "fp32"), (mufu_peak, "mufu"))
-    else:
-        mufu_peak = sms * 16 * f_hz
-        tc_peak = float(peaks["bf16_tflops"]) * 1e12 / (2.0 * d)  # algorithmic 2d flops/entry
-        peak_evals, pipe = min((tc_peak, "tensor"), (mufu_peak, "mufu"))
-    achieved = evals / (dom_ms * 1e-3)
-    roof = {"bound": "alu" if pipe != "tensor" else "tensor", "pipe": pipe,
-            "kernel": dom, "achieved": achieved / 1e9, "peak": peak_evals / 1e9,
-            "unit": "G kernel-evals/s (one exp-evaluated Knm entry = 2d+5 flops + 1 exp)",
-            "frac": achieved / peak_evals, "traffic": None,
-            "peak_source": f"{peak_src} sm_max_mhz x unit counts (148 SM x 128 FP32 / 16 MUFU "
-                           f"per clk) / bf16 tensor peak",
-            "kernel_ms": dom_ms,
-            "share_of_step": kt[dom][0] / ms_total if ms_total else None}
+    roof = roofline(args, cfg, kt, ms_total, n_local, m,
+                    torch.cuda.get_device_properties(local).multi_processor_count)
 
     if args.quick:
         args.no_fit = True
@@ -355,7 +376,8 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (synth/, seeded; "
             "X ~ N(0,1) fp32, C = uniform rows of X; shapes of BASELINE.json)",
             "config": {"workload": cfg.name, "n": n_global, "d": cfg.d, "m": m,
-                       "sigma": cfg.sigma, "kernel": "gaussian", "path": path,
+                       "sigma": cfg.sigma, "kernel": "gaussian",
+                       "path": "tensor" if kt_path_tensor(args, cfg.d) else "simt",
                        "parallelism": f"rows sharded dp{world}, allreduce(m) per product",
                        "l2": "inputs larger than L2 (X packed %.0f MB)" % (n_local * cfg.d * 4 / 1e6)},
             "clocks": clk, "gpu_launches": int(launches), "roofline": roof, "e2e": e2e,

@@ -698,92 +698,108 @@ __device__ __forceinline__ void tile_async(double *dst, const double *src, int64
   }
 }
 
+constexpr int TRSV_ZR = 16;  // z blocks fetched per L2 round trip (ring of ready z_J)
+
 __global__ void __launch_bounds__(256) trsv_kernel(View L, int64_t m, int forward,
                                                    double *__restrict__ z,
                                                    const double *__restrict__ Dinv,
                                                    unsigned int *__restrict__ counter,
-                                                   unsigned int *__restrict__ flags,
-                                                   unsigned int gen) {
+                                                   unsigned int *__restrict__ done) {
+  // Blocks finish strictly in dependency order, so one monotone counter `done` (number of
+  // finished blocks, in solve order) tells every CTA which z_J are final.  Tiles of L do not
+  // depend on z, so they are prefetched (cp.async, 2 deep) regardless of the front; the
+  // final z_J are fetched in batches of up to TRSV_ZR blocks per L2 round trip, and the
+  // counter is polled only when a CTA reaches the dependency front.
   extern __shared__ __align__(16) double tsm[];
-  double *sT[2] = {tsm, tsm + TB * TS_LD};
+  double *sT0 = tsm, *sT1 = tsm + TB * TS_LD;
   double *sD = tsm + 2 * TB * TS_LD;
-  double *sz = sD + TB * TS_LD;     // [TB] z_J
-  double *sx = sz + TB;             // [TB] rhs - acc
-  __shared__ unsigned int s_ticket;
+  double *zr = sD + TB * TS_LD;   // [TRSV_ZR * TB]
+  double *sx = zr + TRSV_ZR * TB;  // [TB]
+  __shared__ unsigned int s_ticket, s_known;
   const int tid = threadIdx.x;
   const int64_t nblk = cdiv<int64_t>(m, TB);
-  if (tid == 0) s_ticket = atomicAdd(counter, 1u);
+  if (tid == 0) {
+    s_ticket = atomicAdd(counter, 1u);
+    s_known = 0;
+  }
   __syncthreads();
-  const int64_t b = s_ticket;
+  const int64_t b = s_ticket;  // this block's rank in solve order
   const int64_t I = forward ? b : nblk - 1 - b;
   const int64_t i0 = I * TB;
   const int nI = (int)lmin(TB, m - i0);
-  // output row index ii is the stored row of each tile iff (forward && !trans) || (!forward && trans)
   const bool rowmaj = (forward != 0) == (L.trans == 0);
-  auto tile_src = [&](int64_t j0) -> const double * {
-    return rowmaj ? L.base + i0 * L.ld + j0 : L.base + j0 * L.ld + i0;
+  const int64_t nJ = b;  // steps: the b blocks before this one in solve order
+  auto j0of = [&](int64_t s) { return (forward ? s : nblk - 1 - s) * TB; };
+  auto issue = [&](int64_t s) {
+    const int64_t j0 = j0of(s);
+    const int nJc = (int)lmin(TB, m - j0);
+    tile_async((s & 1) ? sT1 : sT0, rowmaj ? L.base + i0 * L.ld + j0 : L.base + j0 * L.ld + i0,
+               L.ld, rowmaj ? nI : nJc, rowmaj ? nJc : nI);
+    cp_async_commit();
   };
-  const int64_t nJ = forward ? I : nblk - 1 - I;
-  auto Jof = [&](int64_t s) { return forward ? s : nblk - 1 - s; };
-  // prologue: inverse diagonal block + first tile
   {
     const double *dsrc = Dinv + I * (int64_t)(TB * TB);
     for (int e = tid; e < TB * (TB / 2); e += blockDim.x) {
       const int r = e / (TB / 2), c2 = (e % (TB / 2)) * 2;
       cp_async16(sD + r * TS_LD + c2, dsrc + r * TB + c2);
     }
+    cp_async_commit();
   }
-  if (nJ > 0) {
-    const int64_t j0 = Jof(0) * TB;
-    const int nJc = (int)lmin(TB, m - j0);
-    tile_async(sT[0], tile_src(j0), L.ld, rowmaj ? nI : nJc, rowmaj ? nJc : nI);
-  }
-  cp_async_commit();
-  // mat-vec thread mapping (conflict-free for both smem orientations)
+  if (nJ > 0) issue(0);
   const int ri = rowmaj ? (tid >> 2) : (tid & 63);
   const int qq = rowmaj ? (tid & 3) : (tid >> 6);
   double acc = 0.0;
+  int64_t zlo = 0, zhi = 0;
   for (int64_t s = 0; s < nJ; ++s) {
-    const int64_t J = Jof(s), j0 = J * TB;
-    const int nJc = (int)lmin(TB, m - j0);
-    if (s + 1 < nJ) {
-      const int64_t j1 = Jof(s + 1) * TB;
-      const int n1 = (int)lmin(TB, m - j1);
-      tile_async(sT[(s + 1) & 1], tile_src(j1), L.ld, rowmaj ? nI : n1, rowmaj ? n1 : nI);
-    }
-    cp_async_commit();
-    if (tid == 0) {
-      volatile unsigned int *f = flags + J;
-      while (*f != gen) {
+    if (s + 1 < nJ) issue(s + 1);
+    if (s >= zhi) {
+      if (s >= (int64_t)s_known) {  // at the dependency front: poll the counter
+        if (tid == 0) {
+          volatile unsigned int *d = done;
+          unsigned int v;
+          while ((v = *d) <= (unsigned int)s) {
+          }
+          __threadfence();
+          s_known = v;
+        }
+        __syncthreads();
       }
-      __threadfence();
+      zlo = s;
+      zhi = lmin((int64_t)s_known, s + TRSV_ZR);
+      for (int e = tid; e < (zhi - zlo) * TB; e += blockDim.x) {
+        const int64_t st = zlo + e / TB;
+        const int jj = e % TB;
+        const int64_t jg = j0of(st) + jj;
+        zr[e] = jg < m ? __ldcg(z + jg) : 0.0;
+      }
     }
+    if (s + 1 < nJ) cp_async_wait<1>();
+    else cp_async_wait<0>();
     __syncthreads();
-    if (tid < TB) sz[tid] = (tid < nJc) ? __ldcg(z + j0 + tid) : 0.0;
-    cp_async_wait<1>();
-    __syncthreads();
-    const double *T = sT[s & 1];
+    const double *T = (s & 1) ? sT1 : sT0;
+    const double *zz = zr + (s - zlo) * TB;
+    const int nJc = (int)lmin(TB, m - j0of(s));
     if (ri < nI) {
       if (rowmaj) {
 #pragma unroll
         for (int k = 0; k < TB / 4; ++k) {
           const int jj = qq + 4 * k;
-          if (jj < nJc) acc = fma(T[ri * TS_LD + jj], sz[jj], acc);
+          if (jj < nJc) acc = fma(T[ri * TS_LD + jj], zz[jj], acc);
         }
       } else {
 #pragma unroll
         for (int k = 0; k < TB / 4; ++k) {
           const int jj = qq * (TB / 4) + k;
-          if (jj < nJc) acc = fma(T[jj * TS_LD + ri], sz[jj], acc);
+          if (jj < nJc) acc = fma(T[jj * TS_LD + ri], zz[jj], acc);
         }
       }
     }
     __syncthreads();
   }
   cp_async_wait<0>();
-  // reduce the 4 partial sums of each row, form x = r_I - acc
-  double *part = sT[0];  // reuse: [4][TB]
   __syncthreads();
+  // reduce the 4 partial sums of each row, form x = r_I - acc
+  double *part = sT0;  // reuse: [4][TB]
   part[qq * TB + ri] = acc;
   __syncthreads();
   if (tid < TB)
@@ -791,7 +807,7 @@ __global__ void __launch_bounds__(256) trsv_kernel(View L, int64_t m, int forwar
                                          part[3 * TB + tid])
                          : 0.0;
   __syncthreads();
-  // z_I = D x (forward, D = Dinv_I) or D^T x (backward)
+  // z_I = D x (forward, D = Dinv_I) or D^T x (backward): parallel, no substitution
   {
     const int r = tid & 63, q4 = tid >> 6;
     double v = 0.0;
@@ -807,7 +823,7 @@ __global__ void __launch_bounds__(256) trsv_kernel(View L, int64_t m, int forwar
   if (tid < nI) z[i0 + tid] = part[tid] + part[TB + tid] + part[2 * TB + tid] + part[3 * TB + tid];
   __threadfence();
   __syncthreads();
-  if (tid == 0) atomicExch(flags + I, gen);
+  if (tid == 0) atomicMax(done, (unsigned int)(b + 1));
 }
 
 int64_t precond_work_elems(int64_t m) { return 2 * cdiv<int64_t>(m, TB) * (int64_t)(TB * TB); }
@@ -822,21 +838,17 @@ int trsv(falkon_ctx *ctx, const double *P, const double *diag, const double *wor
   const int64_t nblk = cdiv<int64_t>(m, TB);
   void *fl;
   FK_TRY(ws_get(ctx, WS_FLAGS, 64 + sizeof(unsigned int) * (nblk + 64), &fl));
-  unsigned int *counter = (unsigned int *)((char *)fl + 32);
-  unsigned int *flags = counter + 8;
-  static unsigned int gen_counter = 0;  // monotone generation id (flags never need clearing)
-  unsigned int gen = ++gen_counter;
-  if (gen == 0) gen = ++gen_counter;
-  const size_t smem = sizeof(double) * (3 * TB * TS_LD + 2 * TB);
+  unsigned int *counter = (unsigned int *)((char *)fl + 32);  // [0] ticket, [1] done
+  const size_t smem = sizeof(double) * (3 * TB * TS_LD + (TRSV_ZR + 1) * TB);
   static bool attr = false;
   if (!attr) {
     FK_CUDA(cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  FK_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), ctx->stream));
+  FK_CUDA(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned int), ctx->stream));
   LaunchScope ls(ctx, FALKON_T_TRSV);
-  trsv_kernel<<<(unsigned)nblk, 256, smem, ctx->stream>>>(L, m, forward, x, dinv, counter, flags,
-                                                          gen);
+  trsv_kernel<<<(unsigned)nblk, 256, smem, ctx->stream>>>(L, m, forward, x, dinv, counter,
+                                                          counter + 1);
   FK_LAUNCH_CHECK();
   return FALKON_OK;
 }
