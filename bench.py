@@ -148,11 +148,8 @@ def oracle_rate(cfg, n_global, m, seconds: float, rank_workers: int):
 
 def kt_path_tensor(args, d):
     """Mirror of libfalkon's path choice (tc_supported): tensor cores for the Gaussian kernel
-    when d > 32 and round_up(d + 2, 16) <= 192, unless --path forces one."""
+    when d > 32, unless --path forces one."""
     if args.path == "simt":
-        return False
-    d16 = -(-(d + 2) // 16) * 16
-    if d16 > 192:
         return False
     return args.path == "tensor" or d > 32
 
@@ -187,6 +184,8 @@ def roofline(args, cfg, kt, ms_total, n_local, m, sms):
               "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)"}
     if kt_path_tensor(args, d):
         d16 = -(-(d + 2) // 16) * 16
+        if d16 > 192:  # streaming kernel: 64-aligned segments
+            d16 = -(-(d + 2) // 64) * 64
         peak_tf = float(peaks["bf16_tflops"]) / 3.0
         ach_tf = 2.0 * d * evals / (dom_ms * 1e-3) / 1e12
         issued_tf = 3 * 2.0 * d16 * evals / (dom_ms * 1e-3) / 1e12
@@ -337,7 +336,7 @@ def main():
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": n_global * m / e2e_s, "unit": "n*m/s",
+    e2e = None if not e2e_steps else {"value": n_global * m / e2e_s, "unit": "n*m/s",
            "h2d_bytes_per_step": int(Xh.numel() * 4 + Ch.numel() * 4 + vh.numel() * 8),
            "d2h_bytes_per_step": int(uh.numel() * 8)}
 

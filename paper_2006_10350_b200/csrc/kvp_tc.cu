@@ -52,6 +52,12 @@ int reduce_partials(falkon_ctx *ctx, const double *part, int64_t splits, int64_t
 int center_mean(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, double **mu_out);
 
 static inline int tc_d16(int64_t d) { return (int)round_up<int64_t>(d + 2, 16); }
+// segment length of the packed [h | l] row: 16-aligned when the P tile stays resident in
+// shared memory (2 * d16 <= 384), else 64-aligned for the streaming kernel
+static inline bool tc_stream(int64_t d) { return tc_d16(d) > TC_MAX_D16; }
+static inline int tc_seg(int64_t d) {
+  return tc_stream(d) ? (int)round_up<int64_t>(d + 2, 64) : tc_d16(d);
+}
 // TS (A operand in TMEM) needs 2 accumulators of TC_N_TS columns + 16 columns per d16/16
 // chunk pair: 2*192 + 16*nk <= 512  <=>  d16 <= 128.
 // Measured on B200 (MSD shape): TS is ~5% slower than SS — the MMA rate, not shared-memory
@@ -64,7 +70,7 @@ static bool tc_use_ts(int d16) {
 bool tc_supported(const falkon_ctx *ctx, int kernel, int64_t d) {
   if (kernel != FALKON_GAUSSIAN) return false;  // Laplacian: direct differences only (reading c7)
   if (ctx->opt.path == FALKON_PATH_SIMT) return false;
-  if (tc_d16(d) > TC_MAX_D16) return false;
+  if (tc_seg(d) > 4096) return false;
   if (ctx->opt.path == FALKON_PATH_TENSOR) return true;
   return d > ctx->opt.tc_min_d;
 }
@@ -258,11 +264,15 @@ __device__ __forceinline__ void tc_cp_128x256b(uint32_t tmem_dst, uint64_t sdesc
 
 // NT: Q rows per MMA tile (accumulator columns).  TS: the resident P tile is copied once
 // into TMEM and used as the MMA's A operand (shared memory then only feeds B).
-template <int MODE, int NT, bool TS>
+// STREAM: large d (2*d16 > 384): the P tile cannot stay resident, so each pipeline stage
+// carries the matching 64-wide K box of BOTH segments of P and Q ([h|l] layout with
+// 64-aligned segments): 16 + 16 + 32 + 32 KB, three MMAs per 16-wide chunk.
+template <int MODE, int NT, bool TS, bool STREAM = false>
 __global__ void __launch_bounds__(128 + 32 * TC_EPI_WARPS, 1)
     tc_kvp_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                   TcArgs a) {
-  constexpr int BBOX = NT * TC_BK * 2;   // bytes of one Q box
+  static_assert(!(TS && STREAM), "TS needs the resident P tile");
+  constexpr int BBOX = STREAM ? 2 * (TC_A_BOX + NT * TC_BK * 2) : NT * TC_BK * 2;  // stage bytes
   constexpr int HALF = NT / 2;           // columns per epilogue warp
   constexpr int NCH = HALF / 32;         // 32-column chunks per epilogue warp
   static_assert(HALF % 32 == 0, "tile");
@@ -271,7 +281,7 @@ __global__ void __launch_bounds__(128 + 32 * TC_EPI_WARPS, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = a.stages;
   uint8_t *sA = smem;                                  // nbox x 16 KB (resident P tile)
-  uint8_t *sB = smem + a.nbox * TC_A_BOX;              // S x BBOX
+  uint8_t *sB = smem + (STREAM ? 0 : a.nbox * TC_A_BOX);  // S x BBOX
   uint64_t *bars = reinterpret_cast<uint64_t *>(sB + S * BBOX);
   uint64_t *full = bars, *empty = bars + TC_MAX_STAGES, *tfull = bars + 2 * TC_MAX_STAGES,
            *tempty = tfull + 2, *afull = tempty + 2;
@@ -313,11 +323,12 @@ __global__ void __launch_bounds__(128 + 32 * TC_EPI_WARPS, 1)
 
   if (warp == 0) {
     // TMA producer: the whole warp walks the ring, one elected lane issues the copies
-    if (elect_one()) {
+    if (!STREAM && elect_one()) {
       mbar_expect_tx(afull, (uint32_t)(a.nbox * TC_A_BOX));
       for (int b = 0; b < a.nbox; ++b) tma_load_2d(sA + b * TC_A_BOX, &tmP, b * TC_BK, (int)p0, afull);
     }
     __syncwarp();
+    const int segk = a.nk * 16;  // STREAM: elements per segment
     int stage = 0;
     uint32_t phase = 0;
     for (int t = 0; t < ntiles; ++t) {
@@ -327,6 +338,14 @@ __global__ void __launch_bounds__(128 + 32 * TC_EPI_WARPS, 1)
         if (elect_one()) {
           if (MODE == 11) {  // diagnostic: no Q loads
             mbar_arrive(&full[stage]);
+          } else if (STREAM) {
+            uint8_t *st = sB + stage * BBOX;
+            mbar_expect_tx(&full[stage], BBOX);
+            tma_load_2d(st, &tmP, b * TC_BK, (int)p0, &full[stage]);                     // h_p
+            tma_load_2d(st + TC_A_BOX, &tmP, segk + b * TC_BK, (int)p0, &full[stage]);   // l_p
+            tma_load_2d(st + 2 * TC_A_BOX, &tmQ, b * TC_BK, q0, &full[stage]);           // h_q
+            tma_load_2d(st + 2 * TC_A_BOX + NT * TC_BK * 2, &tmQ, segk + b * TC_BK, q0,
+                        &full[stage]);                                                   // l_q
           } else {
             mbar_expect_tx(&full[stage], BBOX);
             tma_load_2d(sB + stage * BBOX, &tmQ, b * TC_BK, q0, &full[stage]);
@@ -349,7 +368,7 @@ __global__ void __launch_bounds__(128 + 32 * TC_EPI_WARPS, 1)
     auto adesc = [&](int c) -> uint64_t {
       return a0 + (uint64_t)(((c >> 2) * TC_A_BOX + (c & 3) * 32) >> 4);
     };
-    mbar_wait(afull, 0);
+    if (!STREAM) mbar_wait(afull, 0);
     tc_fence_after();
     if (TS) {
       if (elect_one())
@@ -366,7 +385,22 @@ __global__ void __launch_bounds__(128 + 32 * TC_EPI_WARPS, 1)
       for (int b = 0; b < a.nbox; ++b) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (elect_one()) {
+        if (STREAM && elect_one()) {
+          const uint64_t ah = b0 + (uint64_t)((stage * BBOX) >> 4);
+          const uint64_t al = ah + (uint64_t)(TC_A_BOX >> 4);
+          const uint64_t bh = ah + (uint64_t)((2 * TC_A_BOX) >> 4);
+          const uint64_t bl = bh + (uint64_t)((NT * TC_BK * 2) >> 4);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            if (b * 4 + jj < nk && MODE != 10) {
+              const uint64_t o = (uint64_t)(jj * 2);  // +32 B within the 128 B swizzle row
+              tc_mma_f16(dtm, ah + o, bh + o, idesc, (b | jj) ? 1u : 0u);  // h_p . h_q
+              tc_mma_f16(dtm, al + o, bh + o, idesc, 1u);                  // l_p . h_q
+              tc_mma_f16(dtm, ah + o, bl + o, idesc, 1u);                  // h_p . l_q
+            }
+          }
+          tc_commit(&empty[stage]);
+        } else if (!STREAM && elect_one()) {
           const uint64_t bs = b0 + (uint64_t)((stage * BBOX) >> 4);
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
@@ -494,7 +528,7 @@ static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
 
 int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const float *C, int64_t m,
                double sigma, const double *mu, Prepared *pp) {
-  const int d16 = tc_d16(d);
+  const int d16 = tc_seg(d);
   const int kp = 2 * d16;
   const double g = std::sqrt(TC_LOG2E) / sigma;
   const int64_t n_pad = round_up<int64_t>(std::max<int64_t>(n, 1), TC_N);
@@ -522,7 +556,7 @@ int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const floa
   pp->cb = nullptr;
   CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(pp->tmaps);
   FK_TRY(make_map(&maps[0], (const __half *)xp, n, kp, TC_M));  // X as P (pass A)
-  const int nt = tc_use_ts(d16) ? TC_N_TS : TC_N;
+  const int nt = (!tc_stream(d) && tc_use_ts(d16)) ? TC_N_TS : TC_N;
   FK_TRY(make_map(&maps[1], (const __half *)cp, m, kp, nt));  // C as Q (pass A)
   FK_TRY(make_map(&maps[2], (const __half *)cp, m, kp, TC_M));  // C as P (pass B)
   FK_TRY(make_map(&maps[3], (const __half *)xp, n, kp, nt));  // X as Q (pass B)
@@ -543,13 +577,16 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
             float *out32) {
   const CUtensorMap *maps = reinterpret_cast<const CUtensorMap *>(pp.tmaps);
   const int d16 = pp.dq;
-  const int nbox = (int)cdiv<int64_t>(2 * d16, TC_BK);
+  const bool stream = tc_stream(pp.d);
+  // resident: boxes of a whole packed row; streaming: boxes of one segment
+  const int nbox = stream ? d16 / TC_BK : (int)cdiv<int64_t>(2 * d16, TC_BK);
   const int64_t np = passA ? pp.n : pp.m, nq = passA ? pp.m : pp.n;
   if (np <= 0) return FALKON_OK;
-  const bool ts = tc_use_ts(d16);
+  const bool ts = !stream && tc_use_ts(d16);
   const int nt = ts ? TC_N_TS : TC_N;
-  const int stages = tc_stages(nbox, nt);
-  const size_t smem = tc_smem_bytes(nbox, stages, nt);
+  const int stages = stream ? 2 : tc_stages(nbox, nt);
+  const size_t smem = stream ? 1024 + (size_t)2 * 2 * (TC_A_BOX + TC_B_BOX) + 256 + 8 * TC_M
+                             : tc_smem_bytes(nbox, stages, nt);
   int mode = ctx->opt.exp_offload;
   if (const char *e = getenv("FALKON_TC_MODE")) mode = atoi(e);  // diagnostics (8-11)
   typedef void (*kfn)(const CUtensorMap, const CUtensorMap, TcArgs);
@@ -563,6 +600,7 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
     default: fn = ts ? tc_kvp_kernel<0, TC_N_TS, true> : tc_kvp_kernel<0, TC_N, false>; break;
   }
 #undef FK_TC
+  if (stream) fn = mode == 11 ? tc_kvp_kernel<11, TC_N, false, true> : tc_kvp_kernel<0, TC_N, false, true>;
   FK_CUDA(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                TC_SMEM_MAX));
   // grid: P tiles x Q splits, sized to whole waves of one CTA per SM

@@ -127,6 +127,8 @@ TC_SHAPES = [
     (900, 513, 33, 4.0),      # d16 = 48
     (640, 260, 186, 10.0),    # largest d of the resident-A tensor kernel (d16 = 192)
     (3000, 2000, 28, 3.8),    # HIGGS d forced onto tensor cores
+    (1500, 700, 440, 14.5),   # TIMIT d: streaming-P tensor kernel (64-aligned segments)
+    (300, 90, 250, 10.0),     # streaming kernel, sub-tile sizes
 ]
 
 
