@@ -148,10 +148,10 @@ def oracle_rate(cfg, n_global, m, seconds: float, rank_workers: int):
 
 def kt_path_tensor(args, d):
     """Mirror of libfalkon's path choice (tc_supported): tensor cores for the Gaussian kernel
-    when d > 32, unless --path forces one."""
+    when d > 8 (measured crossover), unless --path forces one."""
     if args.path == "simt":
         return False
-    return args.path == "tensor" or d > 32
+    return args.path == "tensor" or d > 8
 
 
 def roofline(args, cfg, kt, ms_total, n_local, m, sms):
@@ -187,14 +187,25 @@ def roofline(args, cfg, kt, ms_total, n_local, m, sms):
         if d16 > 192:  # streaming kernel: 64-aligned segments
             d16 = -(-(d + 2) // 64) * 64
         peak_tf = float(peaks["bf16_tflops"]) / 3.0
-        ach_tf = 2.0 * d * evals / (dom_ms * 1e-3) / 1e12
-        issued_tf = 3 * 2.0 * d16 * evals / (dom_ms * 1e-3) / 1e12
-        return {"bound": "tensor", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": ach_tf / peak_tf,
-                "peak_source": f"{peak_src} bf16 dense {peaks['bf16_tflops']} TF/s / 3 "
-                               "(fp16x3 = fp32-class cross term)",
-                "issued_frac": issued_tf / float(peaks["bf16_tflops"]),
-                "evals_per_s": evals / (dom_ms * 1e-3), **common}
+        ach_eval = evals / (dom_ms * 1e-3)
+        tc_eval_peak = peak_tf * 1e12 / (2.0 * d)       # fp32-class cross term bound
+        mufu_eval_peak = sms * 16 * f_hz               # one ex2 per entry on the MUFU
+        issued_tf = 3 * 2.0 * d16 * ach_eval / 1e12
+        extra = {"issued_frac": issued_tf / float(peaks["bf16_tflops"]),
+                 "evals_per_s": ach_eval, "tensor_evals_peak": tc_eval_peak,
+                 "mufu_evals_peak": mufu_eval_peak}
+        if tc_eval_peak <= mufu_eval_peak:
+            ach_tf = 2.0 * d * ach_eval / 1e12
+            return {"bound": "tensor", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": ach_tf / peak_tf,
+                    "peak_source": f"{peak_src} bf16 dense {peaks['bf16_tflops']} TF/s / 3 "
+                                   "(fp16x3 = fp32-class cross term)", **extra, **common}
+        return {"bound": "alu", "pipe": "mufu", "achieved": ach_eval / 1e9,
+                "peak": mufu_eval_peak / 1e9, "unit": "G kernel-evals/s",
+                "frac": ach_eval / mufu_eval_peak,
+                "peak_source": f"{peak_src} sm_max_mhz {f_hz/1e6:.0f} MHz x {sms} SM x 16 MUFU ex2"
+                               " per clk (tensor cross term not binding at this d)",
+                **extra, **common}
     fp32 = sms * 128 * f_hz / (d + 2)
     mufu = sms * 16 * f_hz
     peak, pipe = min((fp32, "fp32"), (mufu, "mufu"))

@@ -65,7 +65,7 @@ enum { FALKON_PATH_AUTO = 0, FALKON_PATH_SIMT = 1, FALKON_PATH_TENSOR = 2 };
 /* Options (falkon_ctx_set_option). */
 enum {
   FALKON_OPT_PATH = 1,          /* FALKON_PATH_*; AUTO = tensor cores for Gaussian with d > threshold */
-  FALKON_OPT_TC_MIN_D = 2,      /* AUTO threshold on d for the tensor path (default 32) */
+  FALKON_OPT_TC_MIN_D = 2,      /* AUTO threshold on d for the tensor path (default 8: measured crossover) */
   FALKON_OPT_TC_TERMS = 3,      /* fp16 split terms of the tensor cross term: 1, 2 or 3 (default 3) */
   FALKON_OPT_KERNEL_TIMING = 4, /* 1: record CUDA events around every launch (falkon_ctx_timings) */
   FALKON_OPT_EXP_OFFLOAD = 5    /* tensor path: exp2 on the FMA pipe for 0 = none, 1 = all,

@@ -156,3 +156,16 @@ def test_tensor_and_simt_paths_agree(ctx):
         out[path] = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 7.0, zeros(3000)))
     ctx.set_option(binding.OPT_PATH, binding.PATH_AUTO)
     assert rel_l2(out[binding.PATH_TENSOR], out[binding.PATH_SIMT]) <= TOL
+
+
+@pytest.mark.parametrize("n,m,d,sigma", [s for s in SHAPES if s[2] <= 33])
+def test_simt_path_parity(ctx, n, m, d, sigma):
+    """FP32/MUFU SIMT kernels forced (they serve the Laplacian kernel and d <= 8 by default)."""
+    from paper_2006_10350_b200 import binding
+    X, C, v = _problem(n, m, d, seed=11 * n + m + d)
+    ctx.set_option(binding.OPT_PATH, binding.PATH_SIMT)
+    try:
+        u = ctx.knm_matvec(dev(X), dev(C), dev(v), G, sigma, zeros(m))
+    finally:
+        ctx.set_option(binding.OPT_PATH, binding.PATH_AUTO)
+    assert rel_l2(host(u), oracle.knm_t_knm_vec(X, C, v, G, sigma)) <= TOL
