@@ -103,8 +103,10 @@ typedef struct {
    ranks (e.g. with torch.distributed), then call falkon_ctx_create on every rank. */
 int falkon_get_unique_id(unsigned char id[128]);
 
-/* Create a context on CUDA device `device` for rank `rank` of `world` ranks.  `id` must be
-   NULL iff world == 1.  Requires an sm_100 device (returns FALKON_EUNSUPPORTED otherwise).
+/* Create a context on CUDA device `device` for rank `rank` of `world` ranks.  `id` is
+   required when world > 1; with world == 1 a non-NULL id creates a 1-rank NCCL communicator
+   (every m-vector still goes through ncclAllReduce: used to test the collective path on one
+   GPU).  Requires an sm_100 device (returns FALKON_EUNSUPPORTED otherwise).
    The context owns a CUDA stream, a device workspace and (world > 1) an NCCL communicator. */
 int falkon_ctx_create(falkon_ctx **out, int device, int rank, int world, const unsigned char *id);
 int falkon_ctx_destroy(falkon_ctx *ctx);

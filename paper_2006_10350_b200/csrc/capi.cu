@@ -220,7 +220,7 @@ int falkon_ctx_create(falkon_ctx **out, int device, int rank, int world, const u
   if (!out) return fail(FALKON_EINVAL, "out is NULL");
   *out = nullptr;
   if (world < 1 || rank < 0 || rank >= world) return fail(FALKON_EINVAL, "bad rank/world");
-  if ((world == 1) != (id == nullptr)) return fail(FALKON_EINVAL, "id must be NULL iff world == 1");
+  if (world > 1 && id == nullptr) return fail(FALKON_EINVAL, "id is required when world > 1");
   int ndev = 0;
   FK_CUDA(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(FALKON_EINVAL, "bad device ordinal");
@@ -244,7 +244,7 @@ int falkon_ctx_create(falkon_ctx **out, int device, int rank, int world, const u
     return fail(FALKON_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
   }
   c->stream = c->own_stream;
-  if (world > 1) {
+  if (id != nullptr) {  // world == 1 with an id: a 1-rank NCCL communicator (tests the collective path)
     int r = nccl_comm_init(c, id);
     if (r != FALKON_OK) {
       cudaStreamDestroy(c->own_stream);
@@ -461,7 +461,7 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
   const bool host_out = !is_device_ptr(alpha);
   // global n (reading c15)
   int64_t n_global = n_local;
-  if (ctx->world > 1) {
+  if (ctx->nccl_comm) {
     void *p;
     FK_TRY(ws_get(ctx, WS_SCALARS, 64, &p));
     FK_CUDA(cudaMemcpyAsync(p, &n_global, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));

@@ -547,47 +547,73 @@ static int potrf(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, double *Dinv,
     attr_set = true;
   }
   View W{Wbuf, NB, 0, 0, nullptr};
-  for (int64_t k0 = 0; k0 < m; k0 += NB) {
-    const int nb = (int)std::min<int64_t>(NB, m - k0);
-    {
-      LaunchScope ls(ctx, FALKON_T_PRECOND);
-      potrf_diag_kernel<<<1, 512, dsm, ctx->stream>>>(S, k0, nb, Wbuf, Dinv, fail);
+  // Two-level right-looking blocking: inner NB = 128 steps (diagonal factor + inverse, panel
+  // solve as a GEMM with W = L_kk^-1, update of the rest of the NBO-wide outer panel only),
+  // then one trailing update of the remaining matrix with K = NBO = 256 (halves the passes
+  // over the trailing matrix and doubles the GEMM depth per tile).
+  constexpr int NBO = 2 * NB;
+  for (int64_t K0 = 0; K0 < m; K0 += NBO) {
+    const int64_t K1 = std::min<int64_t>(K0 + NBO, m);
+    for (int64_t k0 = K0; k0 < K1; k0 += NB) {
+      const int nb = (int)std::min<int64_t>(NB, m - k0);
+      {
+        LaunchScope ls(ctx, FALKON_T_PRECOND);
+        potrf_diag_kernel<<<1, 512, dsm, ctx->stream>>>(S, k0, nb, Wbuf, Dinv, fail);
+      }
+      FK_LAUNCH_CHECK();
+      const int64_t k1 = k0 + nb, rem = m - k1;
+      if (rem <= 0) break;
+      // panel: L(k1:, k0:k1) = S(k1:, k0:k1) W^T, W(j, k) at Wbuf[j*NB + (k - k0)]
+      GemmArgs p{};
+      p.A = S;
+      p.B = W;
+      p.C = S;
+      p.M = rem;
+      p.N = nb;
+      p.ra = k1;
+      p.rb = 0;
+      p.rc = k1;
+      p.cc = k0;
+      p.k0 = k0;
+      p.k1 = k1;
+      p.B.base = Wbuf - k0;
+      p.alpha = 1.0;
+      p.beta = 0.0;
+      FK_TRY(gemm(ctx, p));
+      if (k1 < K1) {
+        // update the rest of the outer panel: S(k1:, k1:K1) -= L(k1:, k0:k1) L(k1:K1, k0:k1)^T
+        GemmArgs u{};
+        u.A = S;
+        u.B = S;
+        u.C = S;
+        u.M = rem;
+        u.N = K1 - k1;
+        u.ra = k1;
+        u.rb = k1;
+        u.rc = k1;
+        u.cc = k1;
+        u.k0 = k0;
+        u.k1 = k1;
+        u.alpha = -1.0;
+        u.beta = 1.0;
+        FK_TRY(gemm(ctx, u));
+      }
     }
-    FK_LAUNCH_CHECK();
-    const int64_t k1 = k0 + nb, rem = m - k1;
+    const int64_t rem = m - K1;
     if (rem <= 0) break;
-    // panel: L(k1:, k0:k1) = S(k1:, k0:k1) * W^T
-    GemmArgs p{};
-    p.A = S;
-    p.B = W;
-    p.C = S;
-    p.M = rem;
-    p.N = nb;
-    p.ra = k1;
-    p.rb = 0;
-    p.rc = k1;
-    p.cc = k0;
-    // A(r, k) = S(r, k0 + k'): express k in S coordinates; B(j, k) = W(j, k - k0)
-    // -> use a shifted W view: W is addressed with column k - k0 via base offset trick
-    p.k0 = k0;
-    p.k1 = k1;
-    p.B.base = Wbuf - k0;  // W(j, k) at Wbuf[j*NB + (k - k0)]
-    p.alpha = 1.0;
-    p.beta = 0.0;
-    FK_TRY(gemm(ctx, p));
-    // trailing: S(k1:, k1:) -= L(k1:, k0:k1) L(k1:, k0:k1)^T   (lower tiles)
+    // trailing: S(K1:, K1:) -= L(K1:, K0:K1) L(K1:, K0:K1)^T   (lower tiles)
     GemmArgs t{};
     t.A = S;
     t.B = S;
     t.C = S;
     t.M = rem;
     t.N = rem;
-    t.ra = k1;
-    t.rb = k1;
-    t.rc = k1;
-    t.cc = k1;
-    t.k0 = k0;
-    t.k1 = k1;
+    t.ra = K1;
+    t.rb = K1;
+    t.rc = K1;
+    t.cc = K1;
+    t.k0 = K0;
+    t.k1 = K1;
     t.tri_tiles = 1;
     t.alpha = -1.0;
     t.beta = 1.0;

@@ -1,6 +1,7 @@
 // runtime.cu — context plumbing of libfalkon: errors, workspace arena, launch accounting
 // and CUDA-event timing, pointer classification, NCCL (dlopen'ed) communicator.
 #include <dlfcn.h>
+#include <nccl.h>
 #include <string.h>
 
 #include <mutex>
@@ -110,8 +111,9 @@ static struct {
   fn_errstr errstr = nullptr;
 } g_nccl;
 
-// ncclDataType_t / ncclRedOp_t values (nccl.h): ncclInt64 = 5, ncclFloat64 = 8, ncclSum = 0
-static const int NCCL_INT64 = 5, NCCL_FLOAT64 = 8, NCCL_SUM = 0;
+// enum values from nccl.h (types only: the functions are resolved with dlsym)
+static const int NCCL_INT64 = (int)ncclInt64, NCCL_FLOAT64 = (int)ncclFloat64,
+                 NCCL_SUM = (int)ncclSum;
 
 static int nccl_load() {
   std::call_once(g_nccl.once, [] {
@@ -163,7 +165,7 @@ int nccl_comm_destroy(falkon_ctx *ctx) {
 }
 
 int nccl_allreduce_f64(falkon_ctx *ctx, double *buf, int64_t count) {
-  if (ctx->world <= 1 || count == 0) return FALKON_OK;
+  if (!ctx->nccl_comm || count == 0) return FALKON_OK;
   LaunchScope ls(ctx, FALKON_T_ALLREDUCE);
   return nccl_check(g_nccl.allreduce(buf, buf, (size_t)count, NCCL_FLOAT64, NCCL_SUM,
                                      ctx->nccl_comm, ctx->stream),
@@ -171,7 +173,7 @@ int nccl_allreduce_f64(falkon_ctx *ctx, double *buf, int64_t count) {
 }
 
 int nccl_allreduce_i64(falkon_ctx *ctx, int64_t *buf, int64_t count) {
-  if (ctx->world <= 1 || count == 0) return FALKON_OK;
+  if (!ctx->nccl_comm || count == 0) return FALKON_OK;
   LaunchScope ls(ctx, FALKON_T_ALLREDUCE);
   return nccl_check(g_nccl.allreduce(buf, buf, (size_t)count, NCCL_INT64, NCCL_SUM,
                                      ctx->nccl_comm, ctx->stream),

@@ -169,3 +169,27 @@ def test_simt_path_parity(ctx, n, m, d, sigma):
     finally:
         ctx.set_option(binding.OPT_PATH, binding.PATH_AUTO)
     assert rel_l2(host(u), oracle.knm_t_knm_vec(X, C, v, G, sigma)) <= TOL
+
+
+def test_nccl_collective_path_single_rank():
+    """A 1-rank NCCL communicator routes every m-vector through ncclAllReduce (dlopen'ed
+    libnccl, ncclCommInitRank, stream-ordered allreduce): results must equal the no-NCCL
+    context bit for bit (allreduce over one rank is the identity)."""
+    from paper_2006_10350_b200 import binding
+    X, C, v = _problem(6000, 700, 28, seed=21)
+    y = synth.gen_y(3, X, 0)
+    plain = binding.Context(0)
+    coll = binding.Context(0, rank=0, world=1, unique_id=binding.get_unique_id())
+    try:
+        outs = []
+        for c in (plain, coll):
+            u = host(c.knm_matvec(dev(X), dev(C), dev(v), G, 3.8, zeros(700)))
+            a, info = c.fit(dev(X), dev(y), dev(C), G, 3.8, 1e-6, 5, zeros(700))
+            outs.append((u, host(a)))
+        assert np.array_equal(outs[0][0], outs[1][0])
+        assert np.array_equal(outs[0][1], outs[1][1])
+        t = coll.timings()
+        assert t["allreduce"][1] > 0  # the collective was issued
+    finally:
+        plain.close()
+        coll.close()
