@@ -222,14 +222,14 @@ def _solve_upper(U, b, trans: bool):
 # Alg. 1, LinOp read as Eq. (9) (reading c1)
 # --------------------------------------------------------------------------------------
 def linop(beta, X, C, T, A, lam: float, kernel: int, sigma: float, n_global: int | None = None,
-          block_rows: int | None = None):
+          block_rows: int | None = None, workers: int = 1):
     """Alg. 1 lines 4-8 as Eq. (9):
         v = A^-1 beta                     (line 5)
         c = Knm^T Knm T^-1 v              (line 6)
         return A^-T (T^-T c + lam n v)    (line 7, Eq. (9) parenthesisation)"""
     n = X.shape[0] if n_global is None else n_global
     v = _solve_upper(A, beta, trans=False)
-    c = knm_t_knm_vec(X, C, _solve_upper(T, v, trans=False), kernel, sigma, block_rows)
+    c = knm_t_knm_vec(X, C, _solve_upper(T, v, trans=False), kernel, sigma, block_rows, workers)
     return _solve_upper(A, _solve_upper(T, c, trans=True) + lam * n * v, trans=True)
 
 
@@ -268,16 +268,19 @@ def conjugate_gradient(op, b, t: int):
 
 
 def fit(X, y, C, kernel: int, sigma: float, lam: float, iters: int,
-        jitter: float = DEFAULT_JITTER, block_rows: int | None = None, return_info: bool = False):
+        jitter: float = DEFAULT_JITTER, block_rows: int | None = None, return_info: bool = False,
+        workers: int = 1):
     """Falkon, Alg. 1 (PAPER.md:105-117): preconditioner, R, CG(LinOp, R, t),
-    alpha = T^-1 A^-1 beta.  C (= X_m) is an input (sampling lives in synth, reading c11)."""
+    alpha = T^-1 A^-1 beta.  C (= X_m) is an input (sampling lives in synth, reading c11).
+    `workers` only parallelises the row blocks of the products (knm_t_knm_vec)."""
     X = np.asarray(X, dtype=np.float64)
     y = np.asarray(y, dtype=np.float64)
     C = np.asarray(C, dtype=np.float64)
     T, A = preconditioner(C, kernel, sigma, lam, jitter)
     R = rhs(X, y, C, T, A, kernel, sigma, block_rows)
     beta, it = conjugate_gradient(
-        lambda b: linop(b, X, C, T, A, lam, kernel, sigma, block_rows=block_rows), R, iters)
+        lambda b: linop(b, X, C, T, A, lam, kernel, sigma, block_rows=block_rows, workers=workers),
+        R, iters)
     alpha = _solve_upper(T, _solve_upper(A, beta, trans=False), trans=False)
     if return_info:
         return alpha, {"T": T, "A": A, "R": R, "beta": beta, "iters_run": it}

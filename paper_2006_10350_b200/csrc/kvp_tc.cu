@@ -267,15 +267,16 @@ __device__ __forceinline__ void tc_cp_128x256b(uint32_t tmem_dst, uint64_t sdesc
 // STREAM: large d (2*d16 > 384): the P tile cannot stay resident, so each pipeline stage
 // carries the matching 64-wide K box of BOTH segments of P and Q ([h|l] layout with
 // 64-aligned segments): 16 + 16 + 32 + 32 KB, three MMAs per 16-wide chunk.
-template <int MODE, int NT, bool TS, bool STREAM = false>
-__global__ void __launch_bounds__(128 + 32 * TC_EPI_WARPS, 1)
+template <int MODE, int NT, bool TS, bool STREAM = false, int EPIW = TC_EPI_WARPS>
+__global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     tc_kvp_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                   TcArgs a) {
   static_assert(!(TS && STREAM), "TS needs the resident P tile");
   constexpr int BBOX = STREAM ? 2 * (TC_A_BOX + NT * TC_BK * 2) : NT * TC_BK * 2;  // stage bytes
-  constexpr int HALF = NT / 2;           // columns per epilogue warp
+  constexpr int GRP = EPIW / 4;          // column groups (epilogue warps per TMEM lane group)
+  constexpr int HALF = NT / GRP;         // columns per epilogue warp
   constexpr int NCH = HALF / 32;         // 32-column chunks per epilogue warp
-  static_assert(HALF % 32 == 0, "tile");
+  static_assert(HALF % 32 == 0 && EPIW % 4 == 0, "tile");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(128 + 32 * TC_EPI_WARPS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], TC_EPI_WARPS);
+      mbar_init(&tempty[i], EPIW);
     }
     mbar_init(afull, 1);
     fence_mbar_init();
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(128 + 32 * TC_EPI_WARPS, 1)
   } else if (warp >= 4) {
     const int ew = warp - 4;
     const int lg = ew & 3;        // TMEM lane group: warp % 4 == lg
-    const int half = ew >> 2;     // column half of the accumulator
+    const int half = ew >> 2;     // column group of the accumulator
     const int row = lg * 32 + lane;
     const int64_t p = p0 + row;
     const int col0 = half * HALF;
@@ -472,11 +473,13 @@ __global__ void __launch_bounds__(128 + 32 * TC_EPI_WARPS, 1)
       if (lane == 0) mbar_arrive(&tempty[accb]);
       acc64 += (double)((acc[0] + acc[1]) + (acc[2] + acc[3]));
     }
-    // combine the two column halves of each row in a fixed order (deterministic)
-    if (half == 1) red[row] = acc64;
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS) : "memory");
+    // combine the column groups of each row in a fixed order (deterministic)
+    if (half > 0) red[(half - 1) * TC_M + row] = acc64;
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * EPIW) : "memory");
     if (half == 0 && p < a.np) {
-      const double tot = acc64 + red[row];
+      double tot = acc64;
+#pragma unroll
+      for (int g2 = 1; g2 < GRP; ++g2) tot += red[(g2 - 1) * TC_M + row];
       if (a.out64) a.out64[(int64_t)blockIdx.y * a.np + p] = tot;
       if (a.out32) a.out32[p] = (float)tot;
     }
@@ -564,7 +567,7 @@ int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const floa
 }
 
 static size_t tc_smem_bytes(int nbox, int stages, int nt) {
-  return 1024 + (size_t)nbox * TC_A_BOX + (size_t)stages * nt * TC_BK * 2 + 256 + 8 * TC_M;
+  return 1024 + (size_t)nbox * TC_A_BOX + (size_t)stages * nt * TC_BK * 2 + 256 + 3 * 8 * TC_M;
 }
 static int tc_stages(int nbox, int nt) {
   int s = 8;
@@ -585,7 +588,7 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   const bool ts = !stream && tc_use_ts(d16);
   const int nt = ts ? TC_N_TS : TC_N;
   const int stages = stream ? 2 : tc_stages(nbox, nt);
-  const size_t smem = stream ? 1024 + (size_t)2 * 2 * (TC_A_BOX + TC_B_BOX) + 256 + 8 * TC_M
+  const size_t smem = stream ? 1024 + (size_t)2 * 2 * (TC_A_BOX + TC_B_BOX) + 256 + 3 * 8 * TC_M
                              : tc_smem_bytes(nbox, stages, nt);
   int mode = ctx->opt.exp_offload;
   if (const char *e = getenv("FALKON_TC_MODE")) mode = atoi(e);  // diagnostics (8-11)
@@ -601,6 +604,16 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   }
 #undef FK_TC
   if (stream) fn = mode == 11 ? tc_kvp_kernel<11, TC_N, false, true> : tc_kvp_kernel<0, TC_N, false, true>;
+  int epiw = 8;
+  if (const char *e = getenv("FALKON_TC_EPIW")) epiw = atoi(e);  // experiment: 16 epilogue warps
+  if (!stream && !ts && epiw == 16) {
+    switch (mode) {
+      case 2: fn = tc_kvp_kernel<2, TC_N, false, false, 16>; break;
+      case 3: fn = tc_kvp_kernel<3, TC_N, false, false, 16>; break;
+      default: fn = tc_kvp_kernel<0, TC_N, false, false, 16>; break;
+    }
+  }
+  const int threads = 128 + 32 * ((!stream && !ts && epiw == 16) ? 16 : TC_EPI_WARPS);
   FK_CUDA(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                TC_SMEM_MAX));
   // grid: P tiles x Q splits, sized to whole waves of one CTA per SM
@@ -639,7 +652,7 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   args.out32 = splits == 1 ? out32 : nullptr;
   {
     LaunchScope ls(ctx, passA ? FALKON_T_PASS_A : FALKON_T_PASS_B);
-    fn<<<dim3((unsigned)gx, (unsigned)splits), TC_THREADS, smem, ctx->stream>>>(
+    fn<<<dim3((unsigned)gx, (unsigned)splits), threads, smem, ctx->stream>>>(
         passA ? maps[0] : maps[2], passA ? maps[1] : maps[3], args);
   }
   FK_LAUNCH_CHECK();
