@@ -281,13 +281,21 @@ def main():
     m = args.m or cfg.m
     lo, hi = synth.shard_range(n_global, world, rank)
     n_local = hi - lo
-    # ---- inputs (seeded, synthetic; generated on the host, uploaded once) ----
-    Xh = torch.from_numpy(synth.gen_X(cfg.seed, lo, n_local, cfg.d)).pin_memory()
+    # ---- inputs (seeded, synthetic; generated on the host and uploaded once, or generated
+    # on the device with the same hash when too large for the host, e.g. TAXI 1e9 x 9) ----
+    big = n_local * cfg.d > 600_000_000
     Ch = torch.from_numpy(synth.gen_rows(cfg.seed, synth.STREAM_X,
                                          synth.center_indices(cfg.seed, n_global, m), cfg.d)
                           ).pin_memory()
     vh = torch.from_numpy(synth.gen_vec(cfg.seed, m).astype(np.float64)).pin_memory()
-    X, C, v = Xh.cuda(), Ch.cuda(), vh.cuda()
+    if big:
+        Xh = None
+        X = synth.gen_X_torch(cfg.seed, lo, n_local, cfg.d, device="cuda")
+        args.no_fit = args.no_fit or args.fit_iters is None
+    else:
+        Xh = torch.from_numpy(synth.gen_X(cfg.seed, lo, n_local, cfg.d)).pin_memory()
+        X = Xh.cuda()
+    C, v = Ch.cuda(), vh.cuda()
     u = torch.zeros(m, dtype=torch.float64, device="cuda")
     kernel, sigma = binding.GAUSSIAN, cfg.sigma
 
@@ -334,7 +342,7 @@ def main():
         args.no_fit = True
     # ---- e2e: same metric through the C-ABI with HOST (pinned) buffers ----
     uh = torch.zeros(m, dtype=torch.float64).pin_memory()
-    e2e_steps = 0 if args.quick else max(3, min(args.steps, 10))
+    e2e_steps = 0 if (args.quick or Xh is None) else max(3, min(args.steps, 10))
     for _ in range(2 if e2e_steps else 0):
         ctx.knm_matvec(Xh, Ch, vh, kernel, sigma, uh)
     barrier()
@@ -354,7 +362,8 @@ def main():
     # ---- one full Falkon fit (rows a1-a9) ----
     fit = None
     if not args.no_fit:
-        yh = torch.from_numpy(synth.gen_y(cfg.seed, Xh.numpy(), lo, cfg.task))
+        yh = torch.from_numpy(synth.gen_y(cfg.seed, X.cpu().numpy() if Xh is None else Xh.numpy(),
+                                          lo, cfg.task))
         y = yh.cuda()
         alpha = torch.zeros(m, dtype=torch.float64, device="cuda")
         iters = args.fit_iters if args.fit_iters is not None else cfg.iters

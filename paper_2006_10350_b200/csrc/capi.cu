@@ -572,7 +572,7 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
         cg_p_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(p, r, m, sc);
         ctx->launches++;
       }
-      FK_LAUNCH_CHECK();
+      BRK_CUDA(cudaGetLastError());
     }
     if (rc) break;
     cudaEventRecord(ev[3], ctx->stream);

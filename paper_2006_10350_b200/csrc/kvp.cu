@@ -221,6 +221,178 @@ __global__ void __launch_bounds__(KVP_THREADS)
   }
 }
 
+// ------------------------------------------------------------------ fused kvp, d <= 32, packed FP32x2
+// Tile-transposed layout "TT": points are grouped in tiles of 128; a tile stores coordinate k
+// of its 128 points contiguously ([k][128]), so (a) a Q tile is one contiguous bulk copy,
+// (b) one LDS.128 yields coordinate k of 4 consecutive Q points and (c) the P-side register
+// load is coalesced.  Each thread owns R P points with coordinates duplicated into float2
+// pairs and evaluates 2 Q points per packed FFMA2 (fma.rn.f32x2): the FP32 pipe, not the
+// issue slot, becomes the limit.  Laplacian tiles store NEGATED coordinates so the direct
+// difference x - c is one packed add.
+template <int D>
+__device__ __forceinline__ int64_t tt_idx(int64_t p, int k) {
+  return (p >> 7) * (int64_t)(128 * D) + (int64_t)k * 128 + (p & 127);
+}
+
+__global__ void pack_rows_tt_kernel(const float *__restrict__ in, int64_t rows, int64_t rows_pad,
+                                    int d, int dpad, const double *__restrict__ mu, double g,
+                                    int negate, float *__restrict__ out,
+                                    float *__restrict__ bias) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows_pad) return;
+  const int64_t base = (r >> 7) * (int64_t)(128 * dpad) + (r & 127);
+  double s = 0.0;
+  for (int k = 0; k < dpad; ++k) {
+    float v = 0.f;
+    if (r < rows && k < d) v = (float)(((double)in[r * d + k] - mu[k]) * g);
+    s += (double)v * (double)v;
+    out[base + (int64_t)k * 128] = negate ? -v : v;
+  }
+  if (bias) bias[r] = r < rows ? (float)(-0.5 * s) : 0.f;
+}
+
+template <int KER, int D, int R>
+__global__ void __launch_bounds__(KVP_THREADS)
+    kvp_pk_kernel(const float *__restrict__ P, const float *__restrict__ pa, int64_t np,
+                  const float *__restrict__ Q, const float *__restrict__ qb,
+                  const float *__restrict__ z, int64_t nq, int64_t q_per_split,
+                  double *__restrict__ out64, float *__restrict__ out32) {
+  constexpr int QF = KVP_TQ * D;  // floats of one Q tile
+  extern __shared__ __align__(128) float smem_f[];
+  float *const SB = smem_f + 2 * QF;
+  float *const SZ = SB + 2 * KVP_TQ;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(SZ + 2 * KVP_TQ);
+
+  const int tid = threadIdx.x;
+  const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
+  const int64_t qhi = lmin(nq, qlo + q_per_split);
+  const int ntiles = qhi > qlo ? (int)cdiv<int64_t>(qhi - qlo, KVP_TQ) : 0;
+  auto issue = [&](int t) {
+    const int64_t q0 = qlo + (int64_t)t * KVP_TQ;  // multiple of 128: one whole TT tile
+    const int s = t & 1;
+    const uint32_t bq = (uint32_t)QF * 4, bs = (uint32_t)KVP_TQ * 4;
+    mbar_expect_tx(&bar[s], bq + (KER == FALKON_GAUSSIAN ? bs : 0) + bs);
+    bulk_g2s(smem_f + s * QF, Q + (q0 >> 7) * (int64_t)QF, bq, &bar[s]);
+    if (KER == FALKON_GAUSSIAN) bulk_g2s(SB + s * KVP_TQ, qb + q0, bs, &bar[s]);
+    bulk_g2s(SZ + s * KVP_TQ, z + q0, bs, &bar[s]);
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (ntiles > 0) issue(0);
+    if (ntiles > 1) issue(1);
+  }
+  // owned points -> registers, duplicated pairs (x, x)
+  float2 xd[R][D];
+  float2 ad[R];
+  const int64_t pbase = (int64_t)blockIdx.x * (KVP_THREADS * R) + tid;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t p = lmin(pbase + (int64_t)r * KVP_THREADS, np - 1);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      float v = P[tt_idx<D>(p, k)];
+      if (KER == FALKON_LAPLACIAN) v = -v;  // stored negated
+      xd[r][k] = make_float2(v, v);
+    }
+    const float a = (KER == FALKON_GAUSSIAN) ? pa[p] : 0.f;
+    ad[r] = make_float2(a, a);
+  }
+  double acc64[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc64[r] = 0.0;
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t & 1;
+    mbar_wait(&bar[s], (t >> 1) & 1);
+    const int cnt = (int)lmin(KVP_TQ, qhi - (qlo + (int64_t)t * KVP_TQ));
+    const float *q = smem_f + s * QF;
+    const float4 *b4p = reinterpret_cast<const float4 *>(SB + s * KVP_TQ);
+    const float4 *z4p = reinterpret_cast<const float4 *>(SZ + s * KVP_TQ);
+    float2 acc[R][2];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+    for (int j4 = 0; j4 < cnt; j4 += 4) {
+      float4 zz = z4p[j4 >> 2];
+      if (j4 + 4 > cnt) {  // ragged tail of the last tile
+        if (j4 + 1 >= cnt) zz.y = 0.f;
+        if (j4 + 2 >= cnt) zz.z = 0.f;
+        if (j4 + 3 >= cnt) zz.w = 0.f;
+      }
+      float2 e[R][2];
+      if (KER == FALKON_GAUSSIAN) {
+        const float4 bb = b4p[j4 >> 2];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          e[r][0] = __fadd2_rn(ad[r], make_float2(bb.x, bb.y));
+          e[r][1] = __fadd2_rn(ad[r], make_float2(bb.z, bb.w));
+        }
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const float4 q4 = *reinterpret_cast<const float4 *>(q + k * KVP_TQ + j4);
+          const float2 qa = make_float2(q4.x, q4.y), qb2 = make_float2(q4.z, q4.w);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            e[r][0] = __ffma2_rn(xd[r][k], qa, e[r][0]);
+            e[r][1] = __ffma2_rn(xd[r][k], qb2, e[r][1]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            e[r][h].x = ex2_approx(fminf(e[r][h].x, 0.f));
+            e[r][h].y = ex2_approx(fminf(e[r][h].y, 0.f));
+          }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) e[r][0] = e[r][1] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const float4 q4 = *reinterpret_cast<const float4 *>(q + k * KVP_TQ + j4);  // -c
+          const float2 qa = make_float2(q4.x, q4.y), qb2 = make_float2(q4.z, q4.w);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const float2 d0 = __fadd2_rn(xd[r][k], qa), d1 = __fadd2_rn(xd[r][k], qb2);
+            e[r][0] = __ffma2_rn(d0, d0, e[r][0]);
+            e[r][1] = __ffma2_rn(d1, d1, e[r][1]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            e[r][h].x = ex2_approx(-sqrt_approx(e[r][h].x));
+            e[r][h].y = ex2_approx(-sqrt_approx(e[r][h].y));
+          }
+      }
+      const float2 za = make_float2(zz.x, zz.y), zb = make_float2(zz.z, zz.w);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc[r][0] = __ffma2_rn(e[r][0], za, acc[r][0]);
+        acc[r][1] = __ffma2_rn(e[r][1], zb, acc[r][1]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      acc64[r] += (double)((acc[r][0].x + acc[r][0].y) + (acc[r][1].x + acc[r][1].y));
+    __syncthreads();
+    if (tid == 0 && t + 2 < ntiles) issue(t + 2);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t p = pbase + (int64_t)r * KVP_THREADS;
+    if (p < np) {
+      if (out64) out64[(int64_t)blockIdx.y * np + p] = acc64[r];
+      if (out32) out32[p] = (float)acc64[r];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ fused kvp, any d (SIMT)
 // Each thread owns one P point; a tile of 32 Q points is in shared memory; the 32 exponents
 // of the tile are accumulated in registers over 32-wide chunks of the dimension.
@@ -387,9 +559,8 @@ typedef void (*kvp_fn)(const float *, const float *, int64_t, const float *, con
 
 template <int KER, int D>
 static kvp_fn pick_small_R(int R) {
-  if (R == 4) return kvp_small_kernel<KER, D, 4>;
-  if (R == 2) return kvp_small_kernel<KER, D, 2>;
-  return kvp_small_kernel<KER, D, 1>;
+  if (R == 4) return kvp_pk_kernel<KER, D, 4>;
+  return kvp_pk_kernel<KER, D, 2>;
 }
 
 // exact D for d <= 16; multiples of 4 up to 32 (zero-padded coordinates add exact zeros)
@@ -397,7 +568,7 @@ static int small_D(int64_t d) {
   if (d <= 16) return (int)d;
   return (int)round_up<int64_t>(d, 4);
 }
-static int small_R(int D) { return D <= 16 ? 4 : 2; }
+static int small_R(int D) { return D <= 12 ? 4 : 2; }
 
 template <int KER>
 static kvp_fn pick_small(int D, int R) {
@@ -437,7 +608,8 @@ static int kvp_launch(falkon_ctx *ctx, int kernel, int64_t d, int dq, const floa
     TQ = KVP_TQ;
     fn = (const void *)(kernel == FALKON_GAUSSIAN ? pick_small<FALKON_GAUSSIAN>(D, R)
                                                   : pick_small<FALKON_LAPLACIAN>(D, R));
-    smem = (size_t)(2 * TQ * DQ + 4 * TQ) * 4 + 16;
+    smem = (size_t)(2 * TQ * D + 4 * TQ) * 4 + 16;
+    (void)DQ;
   } else {
     TQ = KVP_TQ_G;
     fn = (const void *)(kernel == FALKON_GAUSSIAN ? kvp_generic_kernel<FALKON_GAUSSIAN>
@@ -506,7 +678,8 @@ int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, cons
     return tc_prepare(ctx, X, n, d, C, m, sigma, mu, pp);
   }
   pp->path = FALKON_PATH_SIMT;
-  const int dq = d <= 32 ? ((small_D(d) + 3) & ~3) : (int)round_up<int64_t>(d, 4);
+  const bool tt = d <= 32;  // packed-FFMA2 kernel: tile-transposed layout, D = small_D(d)
+  const int dq = tt ? small_D(d) : (int)round_up<int64_t>(d, 4);
   pp->dq = dq;
   const double g = kernel == FALKON_GAUSSIAN ? std::sqrt(LOG2E) / sigma : LOG2E / sigma;
   // padded to a multiple of 128 rows so tile loads may round up
@@ -518,6 +691,28 @@ int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, cons
   FK_TRY(ws_get(ctx, WS_CP, sizeof(float) * m_pad * dq, &cp));
   FK_TRY(ws_get(ctx, WS_CB, sizeof(float) * m_pad, &cb));
   const int threads = 256;
+  if (tt) {
+    const int neg = kernel == FALKON_LAPLACIAN;
+    {
+      LaunchScope ls(ctx, FALKON_T_PREP);
+      pack_rows_tt_kernel<<<(unsigned)cdiv<int64_t>(m_pad, 256), 256, 0, ctx->stream>>>(
+          C, m, m_pad, (int)d, dq, mu, g, neg, (float *)cp,
+          kernel == FALKON_GAUSSIAN ? (float *)cb : nullptr);
+    }
+    FK_LAUNCH_CHECK();
+    if (n > 0) {
+      LaunchScope ls(ctx, FALKON_T_PREP);
+      pack_rows_tt_kernel<<<(unsigned)cdiv<int64_t>(n_pad, 256), 256, 0, ctx->stream>>>(
+          X, n, n_pad, (int)d, dq, mu, g, neg, (float *)xp,
+          kernel == FALKON_GAUSSIAN ? (float *)xa : nullptr);
+      FK_LAUNCH_CHECK();
+    }
+    pp->Xp = xp;
+    pp->xa = (const float *)xa;
+    pp->Cp = cp;
+    pp->cb = (const float *)cb;
+    return FALKON_OK;
+  }
   {
     LaunchScope ls(ctx, FALKON_T_PREP);
     int64_t blocks = std::min<int64_t>(cdiv<int64_t>(m, threads / 32), 65535);

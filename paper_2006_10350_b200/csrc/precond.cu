@@ -33,7 +33,7 @@ namespace falkon {
 
 constexpr int NB = 128;        // factorization block
 constexpr int GT = 128;        // GEMM CTA tile
-constexpr int GK = 16;         // GEMM k-chunk
+constexpr int GK = 16;         // GEMM k-chunk (32 with 3 stages measured 7% slower)
 constexpr int GSTAGES = 4;     // cp.async pipeline depth of the fp64 GEMM
 constexpr int GPAD = 8;        // smem row padding (doubles): conflict-free DMMA fragments
 constexpr int TB = 64;         // TRSV block
@@ -239,41 +239,6 @@ struct GemmArgs {
   double alpha, beta;
 };
 
-__device__ __forceinline__ void gemm_load_chunk(const View &v, int64_t row0, int64_t rmax,
-                                                int64_t k, int64_t kmax, double (&reg)[8]) {
-  const int tid = threadIdx.x;
-  if (!v.trans) {
-    // storage contiguous along k: 16 threads per row, 16 rows per pass, 8 passes
-    const int kk = tid & 15, rr = tid >> 4;
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      const int64_t r = row0 + rr + 16 * p, kg = k + kk;
-      reg[p] = (r < rmax && kg < kmax) ? vget(v, r, kg) : 0.0;
-    }
-  } else {
-    // storage contiguous along rows: 128 threads per k, 2 k per pass, 8 passes
-    const int rr = tid & 127, kk = tid >> 7;
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      const int64_t r = row0 + rr, kg = k + kk + 2 * p;
-      reg[p] = (r < rmax && kg < kmax) ? vget(v, r, kg) : 0.0;
-    }
-  }
-}
-__device__ __forceinline__ void gemm_store_chunk(const View &v, double (*s)[GT + GPAD],
-                                                 const double (&reg)[8]) {
-  const int tid = threadIdx.x;
-  if (!v.trans) {
-    const int kk = tid & 15, rr = tid >> 4;
-#pragma unroll
-    for (int p = 0; p < 8; ++p) s[kk][rr + 16 * p] = reg[p];
-  } else {
-    const int rr = tid & 127, kk = tid >> 7;
-#pragma unroll
-    for (int p = 0; p < 8; ++p) s[kk + 2 * p][rr] = reg[p];
-  }
-}
-
 // Asynchronous (cp.async, LDGSTS) staging of a GT x GK chunk of a view into shared memory:
 // masked elements are zero-filled (src-size 0), diagonal elements read from the view's dvec.
 __device__ __forceinline__ void cp_async8z(void *smem, const void *gmem, bool valid) {
@@ -305,17 +270,18 @@ __device__ __noinline__ void gemm_async_chunk_masked(const View v, double (*s)[G
                                                      int64_t row0, int64_t rmax, int64_t k,
                                                      int64_t kmax) {
   const int tid = threadIdx.x;
+  constexpr int RP = 256 / GK;  // rows per pass (storage contiguous along k)
   if (!v.trans) {
-    const int kk = tid & 15, rr = tid >> 4;
-    for (int p = 0; p < 8; ++p) {
-      const int64_t r = row0 + rr + 16 * p, kg = k + kk;
+    const int kk = tid % GK, rr = tid / GK;
+    for (int p = 0; p < GT / RP; ++p) {
+      const int64_t r = row0 + rr + RP * p, kg = k + kk;
       bool ok = r < rmax && kg < kmax;
       const double *src = ok ? vsrc(v, r, kg, ok) : v.base;
-      cp_async8z(&s[kk][rr + 16 * p], src, ok);
+      cp_async8z(&s[kk][rr + RP * p], src, ok);
     }
   } else {
     const int rr = tid & 127, kk = tid >> 7;
-    for (int p = 0; p < 8; ++p) {
+    for (int p = 0; p < GK / 2; ++p) {
       const int64_t r = row0 + rr, kg = k + kk + 2 * p;
       bool ok = r < rmax && kg < kmax;
       const double *src = ok ? vsrc(v, r, kg, ok) : v.base;
@@ -330,16 +296,17 @@ __device__ __forceinline__ void gemm_async_chunk(const View &v, double (*s)[GT +
   const int tid = threadIdx.x;
   if (view_dense(v, row0, GT, k, GK)) {
     // branch-free: out-of-range rows/columns are zero-filled from a clamped address
+    constexpr int RP = 256 / GK;
     if (!v.trans) {
-      const int kk = tid & 15, rr = tid >> 4;
+      const int kk = tid % GK, rr = tid / GK;
       const int64_t kg = k + kk;
       const bool kok = kg < kmax;
       const int64_t kc = kok ? kg : k;
 #pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const int64_t r = row0 + rr + 16 * p;
+      for (int p = 0; p < GT / RP; ++p) {
+        const int64_t r = row0 + rr + RP * p;
         const bool ok = kok && r < rmax;
-        cp_async8z(&s[kk][rr + 16 * p], v.base + (ok ? r : row0) * v.ld + kc, ok);
+        cp_async8z(&s[kk][rr + RP * p], v.base + (ok ? r : row0) * v.ld + kc, ok);
       }
     } else {
       const int rr = tid & 127, kk = tid >> 7;
@@ -347,7 +314,7 @@ __device__ __forceinline__ void gemm_async_chunk(const View &v, double (*s)[GT +
       const bool rok = r < rmax;
       const int64_t rc = rok ? r : row0;
 #pragma unroll
-      for (int p = 0; p < 8; ++p) {
+      for (int p = 0; p < GK / 2; ++p) {
         const int64_t kg = k + kk + 2 * p;
         const bool ok = rok && kg < kmax;
         cp_async8z(&s[kk + 2 * p][rr], v.base + (ok ? kg : k) * v.ld + rc, ok);
@@ -519,12 +486,8 @@ __global__ void __launch_bounds__(256) gemm_f64_kernel(GemmArgs a) {
 static int gemm(falkon_ctx *ctx, const GemmArgs &a) {
   if (a.M <= 0 || a.N <= 0) return FALKON_OK;
   const size_t smem = sizeof(double) * 2 * GSTAGES * GK * (GT + GPAD);
-  static bool attr_set = false;
-  if (!attr_set) {
-    FK_CUDA(cudaFuncSetAttribute(gemm_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    attr_set = true;
-  }
+  FK_CUDA(cudaFuncSetAttribute(gemm_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
   const int64_t tm = cdiv<int64_t>(a.M, GT), tn = cdiv<int64_t>(a.N, GT);
   LaunchScope ls(ctx, FALKON_T_PRECOND);
   if (a.tri_tiles) {
@@ -540,12 +503,8 @@ static int gemm(falkon_ctx *ctx, const GemmArgs &a) {
 static int potrf(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, double *Dinv,
                  unsigned long long *fail) {
   const size_t dsm = sizeof(double) * NB * (NB + 1);
-  static bool attr_set = false;
-  if (!attr_set) {
-    FK_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)dsm));
-    attr_set = true;
-  }
+  FK_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)dsm));
   View W{Wbuf, NB, 0, 0, nullptr};
   // Two-level right-looking blocking: inner NB = 128 steps (diagonal factor + inverse, panel
   // solve as a GEMM with W = L_kk^-1, update of the rest of the NBO-wide outer panel only),
@@ -866,11 +825,7 @@ int trsv(falkon_ctx *ctx, const double *P, const double *diag, const double *wor
   FK_TRY(ws_get(ctx, WS_FLAGS, 64 + sizeof(unsigned int) * (nblk + 64), &fl));
   unsigned int *counter = (unsigned int *)((char *)fl + 32);  // [0] ticket, [1] done
   const size_t smem = sizeof(double) * (3 * TB * TS_LD + (TRSV_ZR + 1) * TB);
-  static bool attr = false;
-  if (!attr) {
-    FK_CUDA(cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  FK_CUDA(cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   FK_CUDA(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned int), ctx->stream));
   LaunchScope ls(ctx, FALKON_T_TRSV);
   trsv_kernel<<<(unsigned)nblk, 256, smem, ctx->stream>>>(L, m, forward, x, dinv, counter,

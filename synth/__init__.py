@@ -150,3 +150,45 @@ def make_problem(name_or_cfg, n: int | None = None, m: int | None = None,
     y = gen_y(cfg.seed, X, row0, cfg.task)
     C = gen_rows(cfg.seed, STREAM_X, row0 + center_indices(cfg.seed, nn, mm), cfg.d)
     return cfg, X, y, C
+
+
+# ---------------------------------------------------------------------------------------
+# Device-side generation (torch) of the same stream, for inputs too large to build on the
+# host (TAXI: 1e9 x 9).  Same splitmix64 hash and Box-Muller; uint64 arithmetic is emulated
+# on int64 (wrapping multiply, masked logical shifts).  The fp64 log/cos of the device may
+# differ from NumPy's in the last ulp, so a few fp32 values can differ by one ulp from
+# gen_X; tests that compare against the oracle read the rows back from the device tensor.
+def _t_splitmix64(z):
+    import torch
+    gold = torch.tensor(0x9E3779B97F4A7C15 - (1 << 64), dtype=torch.int64, device=z.device)
+    c1 = torch.tensor(0xBF58476D1CE4E5B9 - (1 << 64), dtype=torch.int64, device=z.device)
+    c2 = torch.tensor(0x94D049BB133111EB - (1 << 64), dtype=torch.int64, device=z.device)
+
+    def srl(x, s):  # logical right shift on int64
+        return (x >> s) & ((1 << (64 - s)) - 1)
+
+    z = z + gold
+    z = (z ^ srl(z, 30)) * c1
+    z = (z ^ srl(z, 27)) * c2
+    return z ^ srl(z, 31)
+
+
+def gen_X_torch(seed: int, row0: int, nrows: int, d: int, device="cuda", stream: int = STREAM_X,
+                chunk_rows: int = 1 << 22):
+    """fp32 tensor (nrows x d) on `device` with rows [row0, row0+nrows) of the generator."""
+    import torch
+    key = (seed * 0x100000001B3 + stream * 0x5851F42D4C957F2D) & 0xFFFFFFFFFFFFFFFF
+    if key >= 1 << 63:
+        key -= 1 << 64
+    out = torch.empty((nrows, d), dtype=torch.float32, device=device)
+    cols = torch.arange(d, dtype=torch.int64, device=device)
+    for s in range(0, nrows, chunk_rows):
+        r = torch.arange(row0 + s, row0 + min(nrows, s + chunk_rows), dtype=torch.int64,
+                         device=device)
+        idx = r[:, None] * d + cols[None, :]
+        h = _t_splitmix64(_t_splitmix64(idx ^ key))
+        u1 = (((h >> 32) & 0xFFFFFFFF).to(torch.float64) + 1.0) / 4294967296.0
+        u2 = (h & 0xFFFFFFFF).to(torch.float64) / 4294967296.0
+        out[s:s + r.numel()] = (torch.sqrt(-2.0 * torch.log(u1)) *
+                                torch.cos(2.0 * torch.pi * u2)).to(torch.float32)
+    return out

@@ -354,3 +354,12 @@ def test_synth_random_access_and_distribution():
     assert np.array_equal(Ct, Xt[idx])
     lo, hi = synth.shard_range(10, 3, 0), synth.shard_range(10, 3, 2)
     assert lo == (0, 4) and hi == (7, 10)
+
+
+def test_synth_device_generator_matches_host():
+    """synth.gen_X_torch (used for inputs too large for the host, e.g. TAXI) reproduces
+    synth.gen_X bit for bit on the CPU torch backend."""
+    torch = pytest.importorskip("torch")
+    a = synth.gen_X(4, 987654321, 3000, 9)
+    b = synth.gen_X_torch(4, 987654321, 3000, 9, device="cpu").numpy()
+    assert np.array_equal(a, b)
