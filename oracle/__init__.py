@@ -6,3 +6,4 @@ legs may import this package.  See falkon_oracle.py for the citations and pins.
 from .falkon_oracle import *  # noqa: F401,F403
 from .falkon_oracle import (GAUSSIAN, LAPLACIAN, DEFAULT_JITTER, NotPositiveDefinite,  # noqa: F401
                             NonFinite)
+from . import gsc_oracle as gsc  # noqa: F401,E402  (Alg. 2, GSC-Falkon / LogFalkon)
