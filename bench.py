@@ -33,6 +33,9 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 
+L2_BYTES = 126 << 20  # B200 L2
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -48,6 +51,9 @@ def parse():
     ap.add_argument("--oracle-seconds", type=float, default=15.0)
     ap.add_argument("--exp-offload", type=int, default=None,
                     help="tensor path: exp2 share on the FMA pipe (0 none, 1 all, 2 1/4, 3 1/2)")
+    ap.add_argument("--gsc-config", default=None, choices=[None] + list(synth.GSC_CONFIGS),
+                    help="also time one GSC-Falkon / LogFalkon fit (Alg. 2) on this workload")
+    ap.add_argument("--gsc-n", type=int, default=None, help="override the GSC workload's n")
     ap.add_argument("--quick", action="store_true",
                     help="timed product steps only (no e2e, cpu_baseline, fit): for ncu runs")
     return ap.parse_args()
@@ -254,6 +260,43 @@ def run_reference(args, cfg, world, rank):
     print(json.dumps(out), flush=True)
 
 
+def run_gsc(args, ctx, world, rank, barrier):
+    """One GSC-Falkon / LogFalkon fit (Alg. 2) on this rank's shard of
+    a GSC workload (synth.GSC_CONFIGS), timed host call -> return (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    g = synth.GSC_CONFIGS[args.gsc_config]
+    base = synth.CONFIGS[g.base]
+    n_global = args.gsc_n or base.n
+    lo, hi = synth.shard_range(n_global, world, rank)
+    X = synth.gen_X(base.seed, lo, hi - lo, base.d)
+    y = synth.gen_y(base.seed, X, lo, "cls")
+    idx = synth.center_indices(base.seed, n_global, g.m)
+    C = synth.gen_rows(base.seed, synth.STREAM_X, idx, base.d)
+    yC = synth.gen_y_rows(base.seed, C, idx, "cls")
+    Xd, yd, Cd, yCd = (torch.from_numpy(a).cuda() for a in (X, y, C, yC))
+    alpha = torch.zeros(g.m, dtype=torch.float64, device="cuda")
+    try:
+        barrier()
+        t0 = time.perf_counter()
+        _, info = ctx.gsc_fit(Xd, yd, Cd, yCd, "gaussian", g.sigma, "logistic", list(g.mus),
+                              list(g.iters), alpha)
+        barrier()
+        wall = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall = float(t.item())
+        return {"workload": g.name, "n": n_global, "d": base.d, "m": g.m, "sigma": g.sigma,
+                "newton_steps": len(g.mus), "cg_iters": int(sum(g.iters)), "seconds": wall,
+                "t_precond_s": info["t_precond_s"], "t_rhs_s": info["t_rhs_s"],
+                "t_cg_s": info["t_cg_s"], "iters_run": info["iters_run"],
+                "paper_context": "Table 2 (PAPER.md:571-573): LogFalkon HIGGS 2267 s "
+                                 "(2x Titan Xp, full HIGGS)"}
+    except Exception as ex:  # report, do not hide
+        return {"workload": g.name, "error": str(ex)}
+
+
 def main():
     args = parse()
     cfg = synth.CONFIGS[args.config]
@@ -315,15 +358,29 @@ def main():
     l0 = ctx.launch_count()
     clocks = ClockSampler(local)
     clocks.start()
+    # Inputs smaller than 2x L2 (e.g. a rank's shard at N > 1) get an L2 flush between the
+    # timed steps (a 512 MB write, outside the per-step events); larger inputs stream anyway.
+    packed = n_local * (2 * 2 * (-(-(cfg.d + 2) // 16) * 16) if kt_path_tensor(args, cfg.d)
+                        else 4 * (-(-cfg.d // 4) * 4))
+    flush = packed < 2 * L2_BYTES
+    fbuf = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if flush else None
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps if flush else 1)]
+    if flush:
+        for i in range(args.steps):
+            fbuf.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+    else:
+        evs[0][0].record(stream)
+        for _ in range(args.steps):
+            step()
+        evs[0][1].record(stream)
     barrier()
     clk = clocks.stop()
-    ms_total = e0.elapsed_time(e1)
+    ms_total = sum(a.elapsed_time(b) for a, b in evs)
     kt = ctx.timings(reset=True)
     launches = ctx.launch_count() - l0 - kt["allreduce"][1]
     ctx.set_option(binding.OPT_KERNEL_TIMING, 0)
@@ -380,6 +437,10 @@ def main():
         except Exception as ex:  # report, do not hide
             fit = {"error": str(ex)}
 
+    gsc_fit = None
+    if args.gsc_config and not args.quick:
+        gsc_fit = run_gsc(args, ctx, world, rank, barrier)
+
     cpu = None
     if rank == 0 and world == 1 and not args.quick:
         rate, inf = oracle_rate(cfg, n_global, m, args.oracle_seconds, host_cores())
@@ -398,9 +459,11 @@ def main():
                        "sigma": cfg.sigma, "kernel": "gaussian",
                        "path": "tensor" if kt_path_tensor(args, cfg.d) else "simt",
                        "parallelism": f"rows sharded dp{world}, allreduce(m) per product",
-                       "l2": "inputs larger than L2 (X packed %.0f MB)" % (n_local * cfg.d * 4 / 1e6)},
+                       "l2": ("L2 flushed between timed steps (512 MB write, untimed; packed X "
+                              "%.0f MB < 2x L2)" if flush else "inputs larger than L2 (packed X "
+                              "%.0f MB)") % (packed / 1e6)},
             "clocks": clk, "gpu_launches": int(launches), "roofline": roof, "e2e": e2e,
-            "cpu_baseline": cpu, "fit": fit,
+            "cpu_baseline": cpu, "fit": fit, "gsc_fit": gsc_fit,
             "kernel_ms": {k: v[0] for k, v in kt.items()},
         }
         print(json.dumps(out), flush=True)

@@ -68,8 +68,11 @@ enum {
   FALKON_OPT_TC_MIN_D = 2,      /* AUTO threshold on d for the tensor path (default 8: measured crossover) */
   FALKON_OPT_TC_TERMS = 3,      /* fp16 split terms of the tensor cross term: 1, 2 or 3 (default 3) */
   FALKON_OPT_KERNEL_TIMING = 4, /* 1: record CUDA events around every launch (falkon_ctx_timings) */
-  FALKON_OPT_EXP_OFFLOAD = 5    /* tensor path: exp2 on the FMA pipe for 0 = none, 1 = all,
+  FALKON_OPT_EXP_OFFLOAD = 5,   /* tensor path: exp2 on the FMA pipe for 0 = none, 1 = all,
                                    2 = 1/4, 3 = 1/2 of the entries (rest on MUFU) */
+  FALKON_OPT_POTRF_OUTER = 6,   /* blocked Cholesky: depth of the trailing fp64 GEMM updates in
+                                   units of 128 columns (1..64, default 8) */
+  FALKON_OPT_GEMM_WARPS = 7     /* fp64 DMMA GEMM CTA: 8 (32 x 64 warp tiles) or 16 (32 x 32) */
 };
 
 /* Per-launch-class accumulated device times in ms (falkon_ctx_timings). */
@@ -183,6 +186,33 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
 int falkon_predict(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d,
                    const float *C, int64_t m, int kernel, double sigma,
                    const double *alpha, double *f);
+
+/* ---- GSC-Falkon / LogFalkon (Appendix B, Alg. 2) ------------------- */
+
+/* Losses of falkon_gsc_fit (Def. 1 / Example 1). */
+enum {
+  FALKON_LOSS_LOGISTIC = 0, /* l(z,y) = log(1 + exp(-y z)), y in {-1,+1} (Example 1(a)) */
+  FALKON_LOSS_SQUARED = 1   /* l(z,y) = (z - y)^2 / 2: one step from 0 is exactly falkon_fit */
+};
+
+/* alpha = GSC-Falkon(X, y, C, y_C, loss, path)  (Alg. 2, DESIGN.md
+   readings g1-g7).  Starting from alpha = 0, runs n_steps approximate Newton steps
+   ("WeightedFalkon"); step k, at level mu[k] > 0 with iters[k] >= 0 CG iterations, solves
+     (Knm^T D Knm + mu n (Kmm + delta I)) alpha_new = Knm^T (D z - g)
+   preconditioned by T^-1 A^-1 with A^T A = (1/m) T D~ T^T + mu I, where z = Knm alpha,
+   g_i = l'(z_i, y_i), D = diag(l''(z_i, y_i)) on the rows and D~ = diag(l''((Kmm alpha)_j,
+   yC_j)) on the centres.  CG runs on the correction from the warm
+   start beta_0 = A T alpha (reading g4; same iterates as CG from beta_0).
+   X: n_local x d fp32 (row shard).  y: n_local fp32 labels (+-1 for the logistic loss).
+   C: m x d fp32, yC: m fp32 labels of the centres (replicated).  mu, iters: n_steps HOST
+   arrays (Alg. 2's geometric path is built by the caller, e.g. binding.newton_path).
+   alpha: m fp64 (replicated).  T = chol(Kmm + delta I) is built once; A is rebuilt per step
+   in the same m x m fp64 buffer.  info: phase times summed over steps, iters_run = total CG
+   iterations.  Errors: as falkon_fit; EINVAL also for n_steps < 1, unknown loss, mu <= 0. */
+int falkon_gsc_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local, int64_t d,
+                   const float *C, const float *yC, int64_t m, int kernel, double sigma,
+                   int loss, int32_t n_steps, const double *mu, const int32_t *iters,
+                   double jitter, double *alpha, falkon_fit_info *info);
 
 const char *falkon_strerror(int code);
 /* Details of the last error on this thread (static storage, valid until the next call). */

@@ -22,6 +22,7 @@ KERNELS = {"gaussian": GAUSSIAN, "laplacian": LAPLACIAN}
 
 PATH_AUTO, PATH_SIMT, PATH_TENSOR = 0, 1, 2
 OPT_PATH, OPT_TC_MIN_D, OPT_TC_TERMS, OPT_KERNEL_TIMING, OPT_EXP_OFFLOAD = 1, 2, 3, 4, 5
+OPT_POTRF_OUTER, OPT_GEMM_WARPS = 6, 7
 TIMING_NAMES = ["prep", "pass_a", "pass_b", "reduce", "allreduce", "precond", "trsv", "vec"]
 
 ERRORS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ENONFINITE", 4: "ENOMEM", 5: "ECUDA",
@@ -32,7 +33,11 @@ EXPORTS = ["falkon_get_unique_id", "falkon_ctx_create", "falkon_ctx_destroy",
            "falkon_ctx_set_stream", "falkon_ctx_set_option", "falkon_ctx_timings",
            "falkon_ctx_launch_count", "falkon_knm_matvec", "falkon_kernel_vec",
            "falkon_kernel_tvec", "falkon_precond_work_elems", "falkon_precond_build", "falkon_precond_solve", "falkon_fit",
-           "falkon_predict", "falkon_strerror", "falkon_last_error", "falkon_version"]
+           "falkon_predict", "falkon_gsc_fit", "falkon_strerror", "falkon_last_error",
+           "falkon_version"]
+
+LOSS_LOGISTIC, LOSS_SQUARED = 0, 1
+LOSSES = {"logistic": LOSS_LOGISTIC, "squared": LOSS_SQUARED}
 
 
 class FalkonError(RuntimeError):
@@ -82,6 +87,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "falkon_precond_solve": (C, [P, P, P, P, P, I64, C, C, P]),
         "falkon_fit": (C, [P, P, P, I64, I64, P, I64, C, D, D, I32, D, P, P]),
         "falkon_predict": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
+        "falkon_gsc_fit": (C, [P, P, P, I64, I64, P, P, I64, C, D, C, I32, P, P, D, P, P]),
         "falkon_strerror": (ctypes.c_char_p, [C]),
         "falkon_last_error": (ctypes.c_char_p, []),
         "falkon_version": (ctypes.c_char_p, []),
@@ -119,6 +125,22 @@ def _ptr(a, dtype: str, name: str):
 
 def _kernel_id(kernel) -> int:
     return KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
+
+
+def newton_path(mu0: float, q: float, lam: float, t: int, t_final: int):
+    """Level schedule of Alg. 2 GSC-Falkon (reading g5):
+    mu_0, q mu_0, ... while >= lam (stop when mu_{k+1} < lam), then lam with t_final CG
+    iterations.  Returns (mus, iters) for Context.gsc_fit."""
+    if not (mu0 > 0 and 0 < q < 1 and lam > 0):
+        raise ValueError("need mu0 > 0, 0 < q < 1, lam > 0")
+    mus, its, mu = [], [], float(mu0)
+    while True:
+        mus.append(mu)
+        its.append(int(t))
+        mu *= q
+        if mu < lam:
+            break
+    return mus + [float(lam)], its + [int(t_final)]
 
 
 def get_unique_id() -> bytes:
@@ -251,6 +273,31 @@ class Context:
         info = FitInfo()
         code = _LIB.falkon_fit(self.h, px, py, n, d, pc, m, _kernel_id(kernel), float(sigma),
                                float(lam), int(iters), float(jitter), pa, ctypes.byref(info))
+        if code != 0:
+            e = FalkonError(code, (_LIB.falkon_last_error() or b"").decode())
+            e.info = info.as_dict()
+            raise e
+        return alpha, info.as_dict()
+
+    def gsc_fit(self, X, y, C, yC, kernel, sigma, loss, mus, iters, alpha, jitter: float = -1.0):
+        """GSC-Falkon / LogFalkon (Alg. 2): Newton steps at levels mus[k] with iters[k] CG
+        iterations each; loss "logistic" or "squared"."""
+        px, n, d, pc, m = self._xc(X, C)
+        py, _ = _ptr(y, "float32", "y")
+        pyc, myc = _ptr(yC, "float32", "yC")
+        if myc != m:
+            raise ValueError("yC must have m entries")
+        pa, _ = _ptr(alpha, "float64", "alpha")
+        k = len(mus)
+        if len(iters) != k:
+            raise ValueError("mus and iters differ in length")
+        mu_arr = (ctypes.c_double * max(k, 1))(*[float(x) for x in mus])
+        it_arr = (ctypes.c_int32 * max(k, 1))(*[int(x) for x in iters])
+        info = FitInfo()
+        lid = LOSSES[loss] if isinstance(loss, str) else int(loss)
+        code = _LIB.falkon_gsc_fit(self.h, px, py, n, d, pc, pyc, m, _kernel_id(kernel),
+                                   float(sigma), lid, k, mu_arr, it_arr, float(jitter), pa,
+                                   ctypes.byref(info))
         if code != 0:
             e = FalkonError(code, (_LIB.falkon_last_error() or b"").decode())
             e.info = info.as_dict()

@@ -153,6 +153,54 @@ static int dot(falkon_ctx *ctx, const double *a, const double *b, int64_t m, dou
   return FALKON_OK;
 }
 
+
+// ------------------------------------------------------------------ GSC losses (Alg. 2)
+// (l', l'') of Def. 1 / Example 1 in fp64; logistic in a stable form:
+// sigma(-s) = 1 / (1 + e^s) evaluated through e^{-|s|} (no overflow), s = y z.
+__device__ __forceinline__ void loss_d12(int loss, double z, double y, double &d1, double &d2) {
+  if (loss == FALKON_LOSS_LOGISTIC) {
+    const double s = y * z;
+    const double e = exp(-fabs(s));
+    const double sn = s >= 0.0 ? e / (1.0 + e) : 1.0 / (1.0 + e);  // sigma(-s)
+    d1 = -y * sn;
+    d2 = sn * (1.0 - sn);
+  } else {
+    d1 = z - y;
+    d2 = 1.0;
+  }
+}
+// rows: g (-> fp32 w, pass B input) and D (-> fp32 weights) at the predictions z (reading g1)
+__global__ void gsc_row_loss_kernel(const double *__restrict__ z, const float *__restrict__ y,
+                                    int64_t n, int64_t n_pad, int loss, float *__restrict__ g,
+                                    float *__restrict__ dw) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double d1 = 0.0, d2 = 0.0;
+    if (i < n) loss_d12(loss, z ? z[i] : 0.0, (double)y[i], d1, d2);
+    g[i] = (float)d1;
+    dw[i] = (float)d2;
+  }
+}
+// centres: D~_j = l''((Kmm alpha)_j, yC_j) with Kmm alpha = zt - delta alpha
+__global__ void gsc_center_weight_kernel(const double *__restrict__ zt,
+                                         const double *__restrict__ alpha, double delta,
+                                         const float *__restrict__ yC, int64_t m, int loss,
+                                         double *__restrict__ dm) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double d1, d2;
+    loss_d12(loss, zt[j] - delta * alpha[j], (double)yC[j], d1, d2);
+    dm[j] = d2;
+  }
+}
+// r = -(r + s zt): the preconditioned Newton residual at the warm start, -(Knm^T g + mu n K alpha)
+__global__ void gsc_rhs_kernel(double *__restrict__ r, const double *__restrict__ zt, double s,
+                               int64_t m) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    r[i] = -fma(s, zt[i], r[i]);
+}
+
 // ------------------------------------------------------------------ product pieces
 struct Fit {
   Prepared pp;
@@ -160,12 +208,76 @@ struct Fit {
   float *w32 = nullptr;   // n_pad
 };
 
-static int product(falkon_ctx *ctx, Fit &F, const double *v, double *u) {
+// w[i] *= dw[i] for the rows, 0 in the padding (GSC LinOp: Knm^T D Knm, Alg. 2 line 6)
+__global__ void scale_rows_kernel(float *__restrict__ w, const float *__restrict__ dw, int64_t n,
+                                  int64_t n_pad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad;
+       i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = i < n ? w[i] * dw[i] : 0.0f;
+}
+
+// u = sum_ranks Knm^T D Knm v  (D = I when dw == NULL: Alg. 1's product)
+static int product(falkon_ctx *ctx, Fit &F, const double *v, double *u,
+                   const float *dw = nullptr) {
   const int64_t m = F.pp.m;
   FK_TRY(f64_to_f32(ctx, v, F.v32, m, round_up<int64_t>(m, 128)));
   FK_TRY(pass_A(ctx, F.pp, F.v32, nullptr, F.w32));
+  if (dw) {
+    const int64_t n_pad = round_up<int64_t>(std::max<int64_t>(F.pp.n, 1), 128);
+    LaunchScope ls(ctx, FALKON_T_VEC);
+    scale_rows_kernel<<<vgrid(n_pad), VT, 0, ctx->stream>>>(F.w32, dw, F.pp.n, n_pad);
+  }
   FK_TRY(pass_B(ctx, F.pp, F.w32, u));
   return nccl_allreduce_f64(ctx, u, m);
+}
+
+// CG vectors and device scalars of one solve (Alg. 1 line 10)
+struct CgState {
+  double *x, *r, *p, *t1, *t2, *u, *sc, *dpart;
+};
+
+// Textbook CG from x = 0 on the preconditioned operator (reading c9), with r already set to
+// the right-hand side:  LinOp(p) = A^-T ( T^-T Knm^T D Knm T^-1 A^-1 p + lam_n A^-1 p )
+// (Eq. (9); Alg. 2 LinOp PAPER.md:979-985 with D = diag(dw), D = I if dw NULL).
+// Never synchronises with the host: breakdown flags live in sc.
+static int cg_run(falkon_ctx *ctx, Fit &F, const double *P, const double *dT, const double *dA,
+                  const double *pw, int64_t m, double lam_n, int iters, const float *dw,
+                  const CgState &S) {
+  FK_CUDA(cudaMemsetAsync(S.x, 0, sizeof(double) * m, ctx->stream));
+  FK_CUDA(cudaMemcpyAsync(S.p, S.r, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+  FK_TRY(dot(ctx, S.r, S.r, m, S.dpart, S.sc + S_RHO));
+  {
+    LaunchScope ls(ctx, FALKON_T_VEC);
+    cg_init_kernel<<<1, 1, 0, ctx->stream>>>(S.sc);
+  }
+  for (int it = 1; it <= iters; ++it) {
+    FK_CUDA(cudaMemcpyAsync(S.t1, S.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+    FK_TRY(trsv(ctx, P, dA, pw, m, 1, 0, S.t1));  // t1 = A^-1 p
+    FK_CUDA(cudaMemcpyAsync(S.t2, S.t1, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+    FK_TRY(trsv(ctx, P, dT, pw, m, 0, 0, S.t2));  // t2 = T^-1 t1
+    FK_TRY(product(ctx, F, S.t2, S.u, dw));       // u = Knm^T D Knm t2 (allreduced)
+    FK_TRY(trsv(ctx, P, dT, pw, m, 0, 1, S.u));   // u = T^-T u
+    {
+      LaunchScope ls(ctx, FALKON_T_VEC);
+      axpy_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(S.u, S.t1, lam_n, m);
+    }
+    FK_TRY(trsv(ctx, P, dA, pw, m, 1, 1, S.u));   // q = A^-T u
+    const double *qv = S.u;
+    FK_TRY(dot(ctx, S.p, qv, m, S.dpart, S.sc + S_GAMMA));
+    {
+      LaunchScope ls(ctx, FALKON_T_VEC);
+      cg_xr_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(S.x, S.r, S.p, qv, m, S.sc, it);
+    }
+    FK_TRY(dot(ctx, S.r, S.r, m, S.dpart, S.sc + S_RHO_NEW));
+    {
+      LaunchScope ls(ctx, FALKON_T_VEC);
+      cg_flags_kernel<<<1, 1, 0, ctx->stream>>>(S.sc, it);
+      cg_p_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(S.p, S.r, m, S.sc);
+      ctx->launches++;
+    }
+    FK_LAUNCH_CHECK();
+  }
+  return FALKON_OK;
 }
 
 static int alloc_fit_vectors(falkon_ctx *ctx, Fit &F) {
@@ -303,6 +415,14 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
     case FALKON_OPT_EXP_OFFLOAD:
       if (value < 0 || value > 3) return fail(FALKON_EINVAL, "exp offload mode must be 0..3");
       ctx->opt.exp_offload = (int)value;
+      return FALKON_OK;
+    case FALKON_OPT_GEMM_WARPS:
+      if (value != 8 && value != 16) return fail(FALKON_EINVAL, "gemm warps must be 8 or 16");
+      ctx->opt.gemm_warps = (int)value;
+      return FALKON_OK;
+    case FALKON_OPT_POTRF_OUTER:
+      if (value < 1 || value > 64) return fail(FALKON_EINVAL, "potrf outer block must be 1..64 x 128");
+      ctx->opt.potrf_outer = (int)value;
       return FALKON_OK;
     default:
       return fail(FALKON_EINVAL, "unknown option");
@@ -538,42 +658,9 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
     if ((rc = trsv(ctx, P, dA, pw, m, 1, 1, r))) break;  // A^-T
     cudaEventRecord(ev[2], ctx->stream);
     // (3) CG  (Alg. 1 line 10; reading c9)
-    BRK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * m, ctx->stream));
-    BRK_CUDA(cudaMemcpyAsync(p, r, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
-    if ((rc = dot(ctx, r, r, m, dpart, sc + S_RHO))) break;
-    {
-      LaunchScope ls(ctx, FALKON_T_VEC);
-      cg_init_kernel<<<1, 1, 0, ctx->stream>>>(sc);
-    }
-    const double lam_n = lambda * (double)n_global;
-    for (int it = 1; it <= iters && rc == FALKON_OK; ++it) {
-      // LinOp(p) = A^-T ( T^-T Knm^T Knm T^-1 A^-1 p + lambda n A^-1 p )   (Eq. (9))
-      BRK_CUDA(cudaMemcpyAsync(t1, p, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
-      if ((rc = trsv(ctx, P, dA, pw, m, 1, 0, t1))) break;  // t1 = A^-1 p
-      BRK_CUDA(cudaMemcpyAsync(t2, t1, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
-      if ((rc = trsv(ctx, P, dT, pw, m, 0, 0, t2))) break;  // t2 = T^-1 t1
-      if ((rc = product(ctx, F, t2, u))) break;          // u = Knm^T Knm t2 (allreduced)
-      if ((rc = trsv(ctx, P, dT, pw, m, 0, 1, u))) break;   // u = T^-T u
-      {
-        LaunchScope ls(ctx, FALKON_T_VEC);
-        axpy_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(u, t1, lam_n, m);
-      }
-      if ((rc = trsv(ctx, P, dA, pw, m, 1, 1, u))) break;   // q = A^-T u
-      double *qv = u;
-      if ((rc = dot(ctx, p, qv, m, dpart, sc + S_GAMMA))) break;
-      {
-        LaunchScope ls(ctx, FALKON_T_VEC);
-        cg_xr_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(x, r, p, qv, m, sc, it);
-      }
-      if ((rc = dot(ctx, r, r, m, dpart, sc + S_RHO_NEW))) break;
-      {
-        LaunchScope ls(ctx, FALKON_T_VEC);
-        cg_flags_kernel<<<1, 1, 0, ctx->stream>>>(sc, it);
-        cg_p_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(p, r, m, sc);
-        ctx->launches++;
-      }
-      BRK_CUDA(cudaGetLastError());
-    }
+    CgState S{x, r, p, t1, t2, u, sc, dpart};
+    if ((rc = cg_run(ctx, F, P, dT, dA, pw, m, lambda * (double)n_global, iters, nullptr, S)))
+      break;
     if (rc) break;
     cudaEventRecord(ev[3], ctx->stream);
     // (4) alpha = T^-1 A^-1 x   (Alg. 1 line 11)
@@ -613,6 +700,189 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
   if (loc.failed_iter >= 0)
     return fail(FALKON_ENONFINITE, "CG breakdown at iteration " + std::to_string(loc.failed_iter));
   return FALKON_OK;
+}
+
+
+// ------------------------------------------------------------------ GSC-Falkon (Alg. 2)
+int falkon_gsc_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local, int64_t d,
+                   const float *C, const float *yC, int64_t m, int kernel, double sigma,
+                   int loss, int32_t n_steps, const double *mu, const int32_t *iters,
+                   double jitter, double *alpha, falkon_fit_info *info) {
+  FK_TRY(check_common(ctx, n_local, d, m, kernel, sigma));
+  if ((!X && n_local > 0) || (!y && n_local > 0) || !C || !yC || !alpha || !mu || !iters)
+    return fail(FALKON_EINVAL, "NULL array");
+  if (loss != FALKON_LOSS_LOGISTIC && loss != FALKON_LOSS_SQUARED)
+    return fail(FALKON_EINVAL, "unknown loss " + std::to_string(loss));
+  if (n_steps < 1) return fail(FALKON_EINVAL, "n_steps < 1");
+  for (int k = 0; k < n_steps; ++k) {
+    if (!(mu[k] > 0.0) || !std::isfinite(mu[k])) return fail(FALKON_EINVAL, "mu[k] must be > 0");
+    if (iters[k] < 0) return fail(FALKON_EINVAL, "iters[k] < 0");
+  }
+  if (jitter < 0) jitter = 1e-8;
+  falkon_fit_info loc;
+  memset(&loc, 0, sizeof(loc));
+  loc.failed_factor = -1;
+  loc.failed_column = -1;
+  loc.failed_iter = -1;
+  loc.jitter_used = jitter;
+  auto t_start = std::chrono::steady_clock::now();
+  int64_t n_global = n_local;
+  if (ctx->nccl_comm) {
+    void *p;
+    FK_TRY(ws_get(ctx, WS_SCALARS, 64, &p));
+    FK_CUDA(cudaMemcpyAsync(p, &n_global, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    FK_TRY(nccl_allreduce_i64(ctx, (int64_t *)p, 1));
+    FK_CUDA(cudaMemcpyAsync(&n_global, p, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  void *cgv, *scal, *gv;
+  FK_TRY(ws_get(ctx, WS_CG, sizeof(double) * m * 8, &cgv));
+  FK_TRY(ws_get(ctx, WS_CG2, sizeof(double) * (S_NSLOTS + DOT_BLOCKS + 8), &scal));
+  FK_TRY(ws_get(ctx, WS_GSC, sizeof(double) * m * 4, &gv));
+  double *x = (double *)cgv, *r = x + m, *p = r + m, *t1 = p + m, *t2 = t1 + m, *u = t2 + m;
+  double *sc = (double *)scal, *dpart = sc + S_NSLOTS + 4;
+  double *acur = (double *)gv, *zt = acur + m, *tmp = zt + m, *dm = tmp + m;
+
+  double *P = nullptr, *dT = nullptr;
+  {
+    cudaError_t e = cudaMalloc(&P, sizeof(double) * (size_t)m * (size_t)m);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FALKON_ENOMEM, "preconditioner buffer of " + std::to_string(8.0 * m * m / 1e9) +
+                                     " GB: " + cudaGetErrorString(e));
+    }
+    e = cudaMalloc(&dT, sizeof(double) * (2 * (size_t)m + (size_t)precond_work_elems(m)));
+    if (e != cudaSuccess) {
+      cudaFree(P);
+      cudaGetLastError();
+      return fail(FALKON_ENOMEM, "diag vectors");
+    }
+  }
+  double *dA = dT + m, *pw = dT + 2 * m;
+  cudaEvent_t ev[4];
+  for (auto &e : ev) cudaEventCreate(&e);
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(P);
+    cudaFree(dT);
+    for (auto &e : ev) cudaEventDestroy(e);
+  };
+  int rc = FALKON_OK;
+  Fit F;
+  do {
+    const void *Xd, *yd, *Cd, *yCd;
+    if ((rc = stage_in(ctx, WS_STAGE_X, X, sizeof(float) * n_local * d, &Xd))) break;
+    if ((rc = stage_in(ctx, WS_STAGE_Y, y, sizeof(float) * n_local, &yd))) break;
+    if ((rc = stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd))) break;
+    if ((rc = stage_in(ctx, WS_STAGE_V, yC, sizeof(float) * m, &yCd))) break;
+    if ((rc = prepare_operands(ctx, (const float *)Xd, n_local, d, (const float *)Cd, m, kernel,
+                               sigma, &F.pp)))
+      break;
+    if ((rc = alloc_fit_vectors(ctx, F))) break;
+    const int64_t n_pad = round_up<int64_t>(std::max<int64_t>(n_local, 1), 128);
+    void *dwp, *zp;
+    if ((rc = ws_get(ctx, WS_DW, sizeof(float) * n_pad, &dwp))) break;
+    if ((rc = ws_get(ctx, WS_Z64, sizeof(double) * std::max<int64_t>(n_local, 1), &zp))) break;
+    float *dw = (float *)dwp;
+    double *z = (double *)zp;
+    // T = chol(Kmm + delta I) once: Kmm does not depend on the Newton iterate (Alg. 2 WP l.1-3)
+    BRK_CUDA(cudaEventRecord(ev[0], ctx->stream));
+    if ((rc = precond_build_T(ctx, (const float *)Cd, m, d, kernel, sigma, jitter, P, dT, pw, &loc)))
+      break;
+    BRK_CUDA(cudaEventRecord(ev[1], ctx->stream));
+    BRK_CUDA(cudaStreamSynchronize(ctx->stream));
+    {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[0], ev[1]);
+      loc.t_precond_s += ms * 1e-3;
+    }
+    BRK_CUDA(cudaMemsetAsync(acur, 0, sizeof(double) * m, ctx->stream));
+    for (int k = 0; k < n_steps && rc == FALKON_OK; ++k) {
+      const double muk = mu[k];
+      BRK_CUDA(cudaEventRecord(ev[0], ctx->stream));
+      // WeightedPreconditioner at the current alpha:
+      // zt = (Kmm + delta I) alpha = T^T T alpha;  D~ = l''(Kmm alpha, yC);  A = chol(T D~ T^T/m + mu I)
+      if (k == 0) {
+        BRK_CUDA(cudaMemsetAsync(zt, 0, sizeof(double) * m, ctx->stream));
+      } else if ((rc = trmv_TtT(ctx, P, dT, m, acur, tmp, zt))) {
+        break;
+      }
+      {
+        LaunchScope ls(ctx, FALKON_T_VEC);
+        gsc_center_weight_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(zt, acur, jitter,
+                                                                     (const float *)yCd, m, loss, dm);
+      }
+      BRK_CUDA(cudaGetLastError());
+      if ((rc = precond_build_A(ctx, m, muk, dm, P, dT, dA, pw, jitter, &loc))) break;
+      BRK_CUDA(cudaEventRecord(ev[1], ctx->stream));
+      // rows: z = Knm alpha, g = l'(z, y), D = l''(z, y)   (readings g1, g2)
+      {
+        const double *zz = nullptr;
+        if (k > 0 && n_local > 0) {
+          if ((rc = f64_to_f32(ctx, acur, F.v32, m, round_up<int64_t>(m, 128)))) break;
+          if ((rc = pass_A(ctx, F.pp, F.v32, z, nullptr))) break;
+          zz = z;
+        }
+        LaunchScope ls(ctx, FALKON_T_VEC);
+        gsc_row_loss_kernel<<<vgrid(n_pad), VT, 0, ctx->stream>>>(zz, (const float *)yd, n_local,
+                                                                   n_pad, loss, F.w32, dw);
+      }
+      BRK_CUDA(cudaGetLastError());
+      // residual at the warm start beta_0 = A T alpha (reading g4):
+      //   R - LinOp(beta_0) = -A^-T T^-T (Knm^T g + mu n (Kmm + delta I) alpha)
+      if ((rc = pass_B(ctx, F.pp, F.w32, r))) break;
+      if ((rc = nccl_allreduce_f64(ctx, r, m))) break;
+      {
+        LaunchScope ls(ctx, FALKON_T_VEC);
+        gsc_rhs_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(r, zt, muk * (double)n_global, m);
+      }
+      BRK_CUDA(cudaGetLastError());
+      if ((rc = trsv(ctx, P, dT, pw, m, 0, 1, r))) break;  // T^-T
+      if ((rc = trsv(ctx, P, dA, pw, m, 1, 1, r))) break;  // A^-T
+      BRK_CUDA(cudaEventRecord(ev[2], ctx->stream));
+      // CG on the correction (Alg. 2 line 10), LinOp with D on the rows
+      CgState S{x, r, p, t1, t2, u, sc, dpart};
+      if (iters[k] > 0) {
+        if ((rc = cg_run(ctx, F, P, dT, dA, pw, m, muk * (double)n_global, iters[k], dw, S))) break;
+        // alpha += T^-1 A^-1 x  (Alg. 2 line 11 applied to beta_0 + x)
+        BRK_CUDA(cudaMemcpyAsync(t1, x, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+        if ((rc = trsv(ctx, P, dA, pw, m, 1, 0, t1))) break;
+        if ((rc = trsv(ctx, P, dT, pw, m, 0, 0, t1))) break;
+        LaunchScope ls(ctx, FALKON_T_VEC);
+        axpy_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(acur, t1, 1.0, m);
+      }
+      BRK_CUDA(cudaGetLastError());
+      BRK_CUDA(cudaEventRecord(ev[3], ctx->stream));
+      double hs[S_NSLOTS] = {};
+      if (iters[k] > 0)
+        BRK_CUDA(cudaMemcpyAsync(hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+      BRK_CUDA(cudaStreamSynchronize(ctx->stream));
+      float a = 0, b = 0, c = 0;
+      cudaEventElapsedTime(&a, ev[0], ev[1]);
+      cudaEventElapsedTime(&b, ev[1], ev[2]);
+      cudaEventElapsedTime(&c, ev[2], ev[3]);
+      loc.t_precond_s += a * 1e-3;
+      loc.t_rhs_s += b * 1e-3;
+      loc.t_cg_s += c * 1e-3;
+      if (iters[k] > 0) {
+        loc.iters_run += (int32_t)hs[S_ITERS];
+        if (hs[S_FAIL] >= 0) {
+          loc.failed_iter = (int32_t)hs[S_FAIL];
+          rc = fail(FALKON_ENONFINITE, "CG breakdown at iteration " + std::to_string(loc.failed_iter) +
+                                           " of Newton step " + std::to_string(k));
+        }
+      }
+    }
+    if (rc) break;
+    BRK_CUDA(cudaMemcpyAsync(alpha, acur, sizeof(double) * m,
+                             is_device_ptr(alpha) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    BRK_CUDA(cudaStreamSynchronize(ctx->stream));
+  } while (0);
+  cleanup();
+  loc.t_total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  if (info) *info = loc;
+  return rc;
 }
 
 }  // extern "C"

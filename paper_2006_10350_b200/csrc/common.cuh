@@ -54,6 +54,10 @@ enum WsSlot {
   WS_TMAP,        // TMA descriptors (device copies)
   WS_PW,          // fp64 NB x NB inverse of the current diagonal block
   WS_CG2,         // fp64 CG scalars
+  WS_TRMV,        // fp64 partials of the transposed triangular mat-vec
+  WS_DW,          // fp32 n: per-row curvature weights D (GSC LinOp, Alg. 2)
+  WS_Z64,         // fp64 n: predictions z = Knm alpha on the rows (GSC)
+  WS_GSC,         // fp64 m vectors of the GSC outer loop
   WS_COUNT
 };
 
@@ -68,6 +72,9 @@ struct Options {
   int tc_terms = 3;
   int kernel_timing = 0;
   int exp_offload = 0;  // tensor path: share of exp2 evaluated on the FMA pipe (0..3)
+  int gemm_warps = 8;   // fp64 GEMM CTA: 8 warps (32 x 64 warp tiles) or 16 (32 x 32)
+  int potrf_outer = 8;  // outer POTRF block in units of NB = 128 (trailing-update depth;
+                        // measured m = 5e4: 2 -> 5.46 s, 4 -> 5.21 s, 8 -> 5.10 s)
 };
 
 }  // namespace falkon
@@ -153,6 +160,17 @@ int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int ker
                   double lambda, double jitter, double *P, double *diagT, double *diagA,
                   double *work, falkon_fit_info *info);
 int64_t precond_work_elems(int64_t m);
+// Split build for GSC-Falkon (Alg. 2): T once (Kmm does not change along the Newton path),
+// then A per step from M = T diag(dscale) T^T / m + lambda I (dscale NULL: D = I).
+int precond_build_T(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel,
+                    double sigma, double jitter, double *P, double *diagT, double *work,
+                    falkon_fit_info *info);
+int precond_build_A(falkon_ctx *ctx, int64_t m, double lambda, const double *dscale, double *P,
+                    double *diagT, double *diagA, double *work, double jitter,
+                    falkon_fit_info *info);
+// z = T^T (T x) = (Kmm + delta I) x from the factored buffer; tmp: m doubles
+int trmv_TtT(falkon_ctx *ctx, const double *P, const double *diagT, int64_t m, const double *x,
+             double *tmp, double *z);
 // x <- op(F)^-1 x, F = T (which 0) or A (which 1); work = the build's work buffer
 int trsv(falkon_ctx *ctx, const double *P, const double *diag, const double *work, int64_t m,
          int which, int trans, double *x);

@@ -35,7 +35,9 @@ constexpr int NB = 128;        // factorization block
 constexpr int GT = 128;        // GEMM CTA tile
 constexpr int GK = 16;         // GEMM k-chunk (32 with 3 stages measured 7% slower)
 constexpr int GSTAGES = 4;     // cp.async pipeline depth of the fp64 GEMM
-constexpr int GPAD = 8;        // smem row padding (doubles): conflict-free DMMA fragments
+constexpr int GPAD = 4;        // smem row padding (doubles): row stride = 8 banks (mod 32), so the
+                               // 4 k-rows x 4 doubles of a half-warp DMMA fragment load hit 32
+                               // distinct banks (GPAD = 8 measured 2-way conflicts in ncu)
 constexpr int TB = 64;         // TRSV block
 
 int64_t precond_work_elems(int64_t m);
@@ -159,12 +161,14 @@ __global__ void __launch_bounds__(512) potrf_diag_kernel(View S, int64_t k0, int
   extern __shared__ double sL[];  // nb x (nb+1)
   const int ld = nb + 1;
   const int tid = threadIdx.x, nt = blockDim.x;
+  // element order follows the view's storage (coalesced for both orientations)
   for (int e = tid; e < nb * nb; e += nt) {
-    const int r = e / nb, c = e % nb;
+    const int r = S.trans ? e % nb : e / nb, c = S.trans ? e / nb : e % nb;
     sL[r * ld + c] = (r >= c) ? vget(S, k0 + r, k0 + c) : 0.0;
   }
   __syncthreads();
-  // unblocked right-looking Cholesky
+  // unblocked right-looking Cholesky; the rank-1 update runs on a 16 x 32 thread grid
+  const int ty = tid >> 5, tx = tid & 31;
   for (int j = 0; j < nb; ++j) {
     if (tid == 0) {
       const double p = sL[j * ld + j];
@@ -176,37 +180,56 @@ __global__ void __launch_bounds__(512) potrf_diag_kernel(View S, int64_t k0, int
       }
     }
     __syncthreads();
-    const double ljj = sL[j * ld + j];
-    for (int i = j + 1 + tid; i < nb; i += nt) sL[i * ld + j] /= ljj;
+    const double rjj = 1.0 / sL[j * ld + j];
+    for (int i = j + 1 + tid; i < nb; i += nt) sL[i * ld + j] *= rjj;
     __syncthreads();
-    const int rem = nb - j - 1;
-    for (int e = tid; e < rem * rem; e += nt) {
-      const int i = j + 1 + e / rem, k = j + 1 + e % rem;
-      if (k <= i) sL[i * ld + k] -= sL[i * ld + j] * sL[k * ld + j];
+    for (int i = j + 1 + ty; i < nb; i += nt / 32) {
+      const double lij = sL[i * ld + j];
+      for (int k = j + 1 + tx; k <= i; k += 32) sL[i * ld + k] = fma(-lij, sL[k * ld + j], sL[i * ld + k]);
     }
     __syncthreads();
   }
   // write L back (lower + diag)
   for (int e = tid; e < nb * nb; e += nt) {
-    const int r = e / nb, c = e % nb;
+    const int r = S.trans ? e % nb : e / nb, c = S.trans ? e / nb : e % nb;
     if (r >= c) vset(S, k0 + r, k0 + c, sL[r * ld + c]);
   }
   __syncthreads();
-  // in-place inverse of lower-triangular L (LAPACK trti2 order: columns right to left)
-  __shared__ double xcol[NB];
-  for (int j = nb - 1; j >= 0; --j) {
-    if (tid == 0) sL[j * ld + j] = 1.0 / sL[j * ld + j];
-    for (int i = j + 1 + tid; i < nb; i += nt) xcol[i] = sL[i * ld + j];
-    __syncthreads();
-    const double ajj = -sL[j * ld + j];
-    // x <- Winv[j+1:, j+1:] * x  (Winv lower, already inverted), then scale by ajj
-    for (int i = j + 1 + tid; i < nb; i += nt) {
-      double s = 0.0;
-      for (int k = j + 1; k <= i; ++k) s = fma(sL[i * ld + k], xcol[k], s);
-      sL[i * ld + j] = s * ajj;
+  // W = L^-1 by column-parallel forward substitution, 4 lanes per column (nb <= 128, 512
+  // threads): W(c,c) = 1/L(c,c);  W(i,c) = -(sum_{c<=k<i} L(i,k) W(k,c)) / L(i,i).
+  // W(i,c), i > c, is kept transposed in the free upper triangle (sL[c][i]), its diagonal in
+  // wd[], and moved over L once complete.
+  __shared__ double wd[NB];
+  {
+    const int c = tid >> 2, sub = tid & 3;
+    const bool act = c < nb;
+    for (int i = 0; i < nb; ++i) {
+      double acc = 0.0;
+      if (act && i > c) {
+        int k = c + sub;
+        if (sub == 0) {
+          acc = sL[i * ld + c] * wd[c];
+          k += 4;
+        }
+        for (; k < i; k += 4) acc = fma(sL[i * ld + k], sL[c * ld + k], acc);
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (act && sub == 0 && i >= c) {
+        const double rii = 1.0 / sL[i * ld + i];
+        if (i == c) wd[c] = rii;
+        else sL[c * ld + i] = -acc * rii;
+      }
+      __syncwarp();
     }
-    __syncthreads();
   }
+  __syncthreads();
+  for (int e = tid; e < nb * nb; e += nt) {
+    const int r = e / nb, c = e % nb;
+    if (r > c) sL[r * ld + c] = sL[c * ld + r];
+    else if (r == c) sL[r * ld + r] = wd[r];
+  }
+  __syncthreads();
   for (int e = tid; e < nb * nb; e += nt) {
     const int r = e / nb, c = e % nb;
     W[(int64_t)r * NB + c] = (r >= c) ? sL[r * ld + c] : 0.0;
@@ -237,6 +260,7 @@ struct GemmArgs {
   int k_from_row;
   int tri_tiles;
   double alpha, beta;
+  const double *kscale;  // optional: B(j, k) is multiplied by kscale[k] (weighted LAUUM, Alg. 2)
 };
 
 // Asynchronous (cp.async, LDGSTS) staging of a GT x GK chunk of a view into shared memory:
@@ -266,11 +290,13 @@ __device__ __forceinline__ bool view_dense(const View &v, int64_t r0, int64_t nr
   return true;
 }
 // masked / diagonal-touching chunks (rare): kept out of line to keep the hot loop small
+template <int NTHR>
 __device__ __noinline__ void gemm_async_chunk_masked(const View v, double (*s)[GT + GPAD],
                                                      int64_t row0, int64_t rmax, int64_t k,
                                                      int64_t kmax) {
   const int tid = threadIdx.x;
-  constexpr int RP = 256 / GK;  // rows per pass (storage contiguous along k)
+  constexpr int RP = NTHR / GK;  // rows per pass (storage contiguous along k)
+  constexpr int KP = NTHR / GT;  // k-rows per pass (storage contiguous along rows)
   if (!v.trans) {
     const int kk = tid % GK, rr = tid / GK;
     for (int p = 0; p < GT / RP; ++p) {
@@ -280,23 +306,25 @@ __device__ __noinline__ void gemm_async_chunk_masked(const View v, double (*s)[G
       cp_async8z(&s[kk][rr + RP * p], src, ok);
     }
   } else {
-    const int rr = tid & 127, kk = tid >> 7;
-    for (int p = 0; p < GK / 2; ++p) {
-      const int64_t r = row0 + rr, kg = k + kk + 2 * p;
+    const int rr = tid % GT, kk = tid / GT;
+    for (int p = 0; p < GK / KP; ++p) {
+      const int64_t r = row0 + rr, kg = k + kk + KP * p;
       bool ok = r < rmax && kg < kmax;
       const double *src = ok ? vsrc(v, r, kg, ok) : v.base;
-      cp_async8z(&s[kk + 2 * p][rr], src, ok);
+      cp_async8z(&s[kk + KP * p][rr], src, ok);
     }
   }
 }
 
+template <int NTHR>
 __device__ __forceinline__ void gemm_async_chunk(const View &v, double (*s)[GT + GPAD],
                                                  int64_t row0, int64_t rmax, int64_t k,
                                                  int64_t kmax) {
   const int tid = threadIdx.x;
   if (view_dense(v, row0, GT, k, GK)) {
     // branch-free: out-of-range rows/columns are zero-filled from a clamped address
-    constexpr int RP = 256 / GK;
+    constexpr int RP = NTHR / GK;
+    constexpr int KP = NTHR / GT;
     if (!v.trans) {
       const int kk = tid % GK, rr = tid / GK;
       const int64_t kg = k + kk;
@@ -309,20 +337,20 @@ __device__ __forceinline__ void gemm_async_chunk(const View &v, double (*s)[GT +
         cp_async8z(&s[kk][rr + RP * p], v.base + (ok ? r : row0) * v.ld + kc, ok);
       }
     } else {
-      const int rr = tid & 127, kk = tid >> 7;
+      const int rr = tid % GT, kk = tid / GT;
       const int64_t r = row0 + rr;
       const bool rok = r < rmax;
       const int64_t rc = rok ? r : row0;
 #pragma unroll
-      for (int p = 0; p < GK / 2; ++p) {
-        const int64_t kg = k + kk + 2 * p;
+      for (int p = 0; p < GK / KP; ++p) {
+        const int64_t kg = k + kk + KP * p;
         const bool ok = rok && kg < kmax;
-        cp_async8z(&s[kk + 2 * p][rr], v.base + (ok ? kg : k) * v.ld + rc, ok);
+        cp_async8z(&s[kk + KP * p][rr], v.base + (ok ? kg : k) * v.ld + rc, ok);
       }
     }
     return;
   }
-  gemm_async_chunk_masked(v, s, row0, rmax, k, kmax);
+  gemm_async_chunk_masked<NTHR>(v, s, row0, rmax, k, kmax);
 }
 
 __device__ __noinline__ void gemm_epilogue(const GemmArgs a, const double *sC, int64_t i0,
@@ -365,10 +393,13 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// CTA tile 128 x 128, 8 warps (4 x 2), warp tile 32 x 64 = 4 x 8 DMMA tiles; per k4 step a
-// warp loads 12 fragments from shared memory for 32 MMAs.  k-chunks of GK are staged
-// global -> registers -> shared (double-buffered) through the views.
-__global__ void __launch_bounds__(256) gemm_f64_kernel(GemmArgs a) {
+// CTA tile 128 x 128, 4 x WN warps, warp tile 32 x (8 NT) = 4 x NT DMMA tiles (WN = 2, NT = 8:
+// 8 warps, 32 x 64, 12 fragments per 32 MMAs; WN = 4, NT = 4: 16 warps, 32 x 32, 8 fragments
+// per 16 MMAs, twice the warps to hide DMMA issue latency).  k-chunks of GK are staged
+// global -> shared with cp.async (GSTAGES deep) through the views.
+template <int WN, int NT>
+__global__ void __launch_bounds__(128 * WN) gemm_f64_kernel(GemmArgs a) {
+  constexpr int NTHR = 128 * WN;
   int64_t ti, tj;
   if (a.tri_tiles) {
     const int64_t t = blockIdx.x;
@@ -391,29 +422,30 @@ __global__ void __launch_bounds__(256) gemm_f64_kernel(GemmArgs a) {
       reinterpret_cast<double(*)[GK][GT + GPAD]>(gsm + GSTAGES * GK * (GT + GPAD));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wr = warp >> 1, wc = warp & 1;
+  const int wr = warp / WN, wc = warp % WN;
   const int g = lane >> 2, q = lane & 3;
-  double acc[4][8][2];
+  double acc[4][NT][2];
   // Tiles strictly inside C's triangle (the vast majority) accumulate on top of C itself:
   // acc starts at (beta/alpha) C, loaded here so the loads overlap the pipeline fill, and the
   // epilogue is a plain store of alpha * acc (no read-modify-write round trips).
   const bool cdense = view_dense(a.C, a.rc + i0, GT, a.cc + j0, GT) && i0 + GT <= a.M &&
                       j0 + GT <= a.N;
   const int64_t csr = a.C.trans ? 1 : a.C.ld, csc = a.C.trans ? a.C.ld : 1;
-  double *cfrag = a.C.base + (a.rc + i0 + wr * 32 + g) * csr + (a.cc + j0 + wc * 64 + 2 * q) * csc;
+  double *cfrag =
+      a.C.base + (a.rc + i0 + wr * 32 + g) * csr + (a.cc + j0 + wc * (8 * NT) + 2 * q) * csc;
   if (cdense && a.beta != 0.0) {
     const double sb = a.beta / a.alpha;
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int h = 0; h < 2; ++h) acc[mt][nt][h] = sb * cfrag[(mt * 8) * csr + (nt * 8 + h) * csc];
   } else {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   }
 
   const int64_t ra = a.ra + i0, rb = a.rb + j0;
@@ -423,36 +455,45 @@ __global__ void __launch_bounds__(256) gemm_f64_kernel(GemmArgs a) {
 #pragma unroll
   for (int c = 0; c < GSTAGES - 1; ++c) {
     if (c < nch) {
-      gemm_async_chunk(a.A, As[c], ra, ramax, kb + (int64_t)c * GK, ke);
-      gemm_async_chunk(a.B, Bs[c], rb, rbmax, kb + (int64_t)c * GK, ke);
+      gemm_async_chunk<NTHR>(a.A, As[c], ra, ramax, kb + (int64_t)c * GK, ke);
+      gemm_async_chunk<NTHR>(a.B, Bs[c], rb, rbmax, kb + (int64_t)c * GK, ke);
     }
     cp_async_commit();
   }
   for (int c = 0; c < nch; ++c) {
     cp_async_wait<GSTAGES - 2>();
     __syncthreads();
+    if (a.kscale) {  // T D T^T of Alg. 2: scale the staged B chunk by D(k)
+      const int st = c % GSTAGES;
+      const int64_t kc = kb + (int64_t)c * GK;
+      for (int e = tid; e < GK * GT; e += NTHR) {
+        const int kk = e / GT, j = e % GT;
+        if (kc + kk < ke) Bs[st][kk][j] *= a.kscale[kc + kk];
+      }
+      __syncthreads();
+    }
     {
       const int cn = c + GSTAGES - 1;
       if (cn < nch) {
-        gemm_async_chunk(a.A, As[cn % GSTAGES], ra, ramax, kb + (int64_t)cn * GK, ke);
-        gemm_async_chunk(a.B, Bs[cn % GSTAGES], rb, rbmax, kb + (int64_t)cn * GK, ke);
+        gemm_async_chunk<NTHR>(a.A, As[cn % GSTAGES], ra, ramax, kb + (int64_t)cn * GK, ke);
+        gemm_async_chunk<NTHR>(a.B, Bs[cn % GSTAGES], rb, rbmax, kb + (int64_t)cn * GK, ke);
       }
       cp_async_commit();
     }
     const int st = c % GSTAGES;
 #pragma unroll
     for (int ks = 0; ks < GK / 4; ++ks) {
-      double af[4], bf[8];
+      double af[4], bf[NT];
       const double *arow = &As[st][ks * 4 + q][wr * 32 + g];
-      const double *brow = &Bs[st][ks * 4 + q][wc * 64 + g];
+      const double *brow = &Bs[st][ks * 4 + q][wc * (8 * NT) + g];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) af[mt] = arow[mt * 8];
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt) bf[nt] = brow[nt * 8];
+      for (int nt = 0; nt < NT; ++nt) bf[nt] = brow[nt * 8];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 8; ++nt) dmma_8x8x4(acc[mt][nt], af[mt], bf[nt]);
+        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], af[mt], bf[nt]);
     }
   }
   cp_async_wait<0>();
@@ -463,7 +504,7 @@ __global__ void __launch_bounds__(256) gemm_f64_kernel(GemmArgs a) {
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int h = 0; h < 2; ++h)
           cfrag[(mt * 8) * csr + (nt * 8 + h) * csc] = a.alpha * acc[mt][nt][h];
@@ -475,28 +516,33 @@ __global__ void __launch_bounds__(256) gemm_f64_kernel(GemmArgs a) {
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int h = 0; h < 2; ++h)
-        sC[(wr * 32 + mt * 8 + g) * CLD + wc * 64 + nt * 8 + 2 * q + h] = acc[mt][nt][h];
+        sC[(wr * 32 + mt * 8 + g) * CLD + wc * (8 * NT) + nt * 8 + 2 * q + h] = acc[mt][nt][h];
   __syncthreads();
   gemm_epilogue(a, sC, i0, j0);
 }
 
-static int gemm(falkon_ctx *ctx, const GemmArgs &a) {
-  if (a.M <= 0 || a.N <= 0) return FALKON_OK;
+template <int WN, int NT>
+static int gemm_launch(falkon_ctx *ctx, const GemmArgs &a) {
   const size_t smem = sizeof(double) * 2 * GSTAGES * GK * (GT + GPAD);
-  FK_CUDA(cudaFuncSetAttribute(gemm_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
+  FK_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<WN, NT>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t tm = cdiv<int64_t>(a.M, GT), tn = cdiv<int64_t>(a.N, GT);
   LaunchScope ls(ctx, FALKON_T_PRECOND);
   if (a.tri_tiles) {
-    gemm_f64_kernel<<<(unsigned)(tm * (tm + 1) / 2), 256, smem, ctx->stream>>>(a);
+    gemm_f64_kernel<WN, NT><<<(unsigned)(tm * (tm + 1) / 2), 128 * WN, smem, ctx->stream>>>(a);
   } else {
-    gemm_f64_kernel<<<dim3((unsigned)tn, (unsigned)tm), 256, smem, ctx->stream>>>(a);
+    gemm_f64_kernel<WN, NT><<<dim3((unsigned)tn, (unsigned)tm), 128 * WN, smem, ctx->stream>>>(a);
   }
   FK_LAUNCH_CHECK();
   return FALKON_OK;
+}
+
+static int gemm(falkon_ctx *ctx, const GemmArgs &a) {
+  if (a.M <= 0 || a.N <= 0) return FALKON_OK;
+  return ctx->opt.gemm_warps == 16 ? gemm_launch<4, 4>(ctx, a) : gemm_launch<2, 8>(ctx, a);
 }
 
 // ------------------------------------------------------------------ blocked Cholesky
@@ -508,9 +554,10 @@ static int potrf(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, double *Dinv,
   View W{Wbuf, NB, 0, 0, nullptr};
   // Two-level right-looking blocking: inner NB = 128 steps (diagonal factor + inverse, panel
   // solve as a GEMM with W = L_kk^-1, update of the rest of the NBO-wide outer panel only),
-  // then one trailing update of the remaining matrix with K = NBO = 256 (halves the passes
+  // then one trailing update of the remaining matrix with K = NBO (FALKON_OPT_POTRF_OUTER x 128;
+  // fewer passes
   // over the trailing matrix and doubles the GEMM depth per tile).
-  constexpr int NBO = 2 * NB;
+  const int NBO = NB * ctx->opt.potrf_outer;
   for (int64_t K0 = 0; K0 < m; K0 += NBO) {
     const int64_t K1 = std::min<int64_t>(K0 + NBO, m);
     for (int64_t k0 = K0; k0 < K1; k0 += NB) {
@@ -586,19 +633,39 @@ __global__ void add_diag_kernel(double *dvec, int64_t m, double scale, double ad
   if (i < m) dvec[i] = dvec[i] * scale + add;
 }
 
-int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel, double sigma,
-                  double lambda, double jitter, double *P, double *diagT, double *diagA,
-                  double *work, falkon_fit_info *info) {
-  double *dinvT = work, *dinvA = work ? work + precond_work_elems(m) / 2 : nullptr;
-  void *flags, *wb;
-  FK_TRY(ws_get(ctx, WS_FLAGS, 64, &flags));
+// Reads the two pivot-failure words written by potrf (first failing column or ~0) and
+// turns a failure into ENOTPD naming the factor and column.
+static int check_pivots(falkon_ctx *ctx, const unsigned long long *failf, int f0, int f1,
+                        double jitter, falkon_fit_info *info) {
+  unsigned long long hf[2];
+  FK_CUDA(cudaMemcpyAsync(hf, failf, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
+  FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (info) {
+    info->failed_factor = -1;
+    info->failed_column = -1;
+    info->jitter_used = jitter;
+  }
+  for (int f = f0; f <= f1; ++f) {
+    if (hf[f] != ~0ULL) {
+      if (info) {
+        info->failed_factor = f;
+        info->failed_column = (int64_t)hf[f];
+      }
+      return fail(FALKON_ENOTPD, std::string("Cholesky of ") + (f ? "A" : "T") +
+                                     " failed at column " + std::to_string(hf[f]));
+    }
+  }
+  return FALKON_OK;
+}
+
+// Steps (b)-(c): Kmm + delta I into the upper triangle, factored in place into T.
+// `check`: synchronise and report a pivot failure (else the caller checks later).
+static int build_T(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel,
+                   double sigma, double jitter, double *P, double *diagT, double *dinvT,
+                   unsigned long long *failf) {
+  void *wb;
   FK_TRY(ws_get(ctx, WS_PW, sizeof(double) * NB * NB, &wb));
-  unsigned long long *failf = (unsigned long long *)flags;
-  FK_CUDA(cudaMemsetAsync(failf, 0xff, 16, ctx->stream));
   View L1{P, m, 1, 1, diagT};  // L1 = T^T, stored in the upper triangle
-  View L2{P, m, 0, 1, diagA};  // L2 = A^T, stored in the lower triangle
-  View Tv{P, m, 0, 2, diagT};  // T itself (upper view of the same storage)
-  // (b) Kmm + delta I
   {
     const int64_t tt = cdiv<int64_t>(m, 64);
     LaunchScope ls(ctx, FALKON_T_PRECOND);
@@ -606,9 +673,18 @@ int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int ker
         C, m, d, kernel, 1.0 / (2.0 * sigma * sigma), 1.0 / sigma, jitter, L1);
   }
   FK_LAUNCH_CHECK();
-  // (c) T
-  FK_TRY(potrf(ctx, L1, m, (double *)wb, dinvT, failf));
-  // (d) M = T T^T / m + lambda I  -> lower triangle + diagA:  M(i,j) = sum_{k>=i} T(i,k) T(j,k)
+  return potrf(ctx, L1, m, (double *)wb, dinvT, failf);
+}
+
+// Steps (d)-(e): M = T D T^T / m + lambda I into the lower triangle (+ diagA), factored in
+// place into A^T.  D = diag(dscale) (Alg. 2 line 5) or I (dscale == NULL,
+// Alg. 1 line 16).  M(i,j) = sum_{k>=i} T(i,k) D(k) T(j,k).
+static int build_A(falkon_ctx *ctx, int64_t m, double lambda, const double *dscale, double *P,
+                   double *diagT, double *diagA, double *dinvA, unsigned long long *failf) {
+  void *wb;
+  FK_TRY(ws_get(ctx, WS_PW, sizeof(double) * NB * NB, &wb));
+  View L2{P, m, 0, 1, diagA};  // L2 = A^T, stored in the lower triangle
+  View Tv{P, m, 0, 2, diagT};  // T itself (upper view of the same storage)
   {
     GemmArgs g{};
     g.A = Tv;
@@ -622,32 +698,122 @@ int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int ker
     g.tri_tiles = 1;
     g.alpha = 1.0 / (double)m;
     g.beta = 0.0;
+    g.kscale = dscale;
     FK_TRY(gemm(ctx, g));
     LaunchScope ls(ctx, FALKON_T_PRECOND);
     add_diag_kernel<<<(unsigned)cdiv<int64_t>(m, 256), 256, 0, ctx->stream>>>(diagA, m, 1.0,
                                                                                 lambda);
   }
   FK_LAUNCH_CHECK();
-  // (e) A^T
-  FK_TRY(potrf(ctx, L2, m, (double *)wb, dinvA, failf + 1));
-  unsigned long long hf[2];
-  FK_CUDA(cudaMemcpyAsync(hf, failf, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
-  FK_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (info) {
-    info->failed_factor = -1;
-    info->failed_column = -1;
-    info->jitter_used = jitter;
+  return potrf(ctx, L2, m, (double *)wb, dinvA, failf);
+}
+
+int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel, double sigma,
+                  double lambda, double jitter, double *P, double *diagT, double *diagA,
+                  double *work, falkon_fit_info *info) {
+  double *dinvT = work, *dinvA = work ? work + precond_work_elems(m) / 2 : nullptr;
+  void *flags;
+  FK_TRY(ws_get(ctx, WS_FLAGS, 64, &flags));
+  unsigned long long *failf = (unsigned long long *)flags;
+  FK_CUDA(cudaMemsetAsync(failf, 0xff, 16, ctx->stream));
+  FK_TRY(build_T(ctx, C, m, d, kernel, sigma, jitter, P, diagT, dinvT, failf));
+  FK_TRY(build_A(ctx, m, lambda, nullptr, P, diagT, diagA, dinvA, failf + 1));
+  return check_pivots(ctx, failf, 0, 1, jitter, info);
+}
+
+int precond_build_T(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel,
+                    double sigma, double jitter, double *P, double *diagT, double *work,
+                    falkon_fit_info *info) {
+  void *flags;
+  FK_TRY(ws_get(ctx, WS_FLAGS, 64, &flags));
+  unsigned long long *failf = (unsigned long long *)flags;
+  FK_CUDA(cudaMemsetAsync(failf, 0xff, 16, ctx->stream));
+  FK_TRY(build_T(ctx, C, m, d, kernel, sigma, jitter, P, diagT, work, failf));
+  return check_pivots(ctx, failf, 0, 0, jitter, info);
+}
+
+int precond_build_A(falkon_ctx *ctx, int64_t m, double lambda, const double *dscale, double *P,
+                    double *diagT, double *diagA, double *work, double jitter,
+                    falkon_fit_info *info) {
+  void *flags;
+  FK_TRY(ws_get(ctx, WS_FLAGS, 64, &flags));
+  unsigned long long *failf = (unsigned long long *)flags;
+  FK_CUDA(cudaMemsetAsync(failf, 0xff, 16, ctx->stream));
+  FK_TRY(build_A(ctx, m, lambda, dscale, P, diagT, diagA, work + precond_work_elems(m) / 2,
+                 failf + 1));
+  return check_pivots(ctx, failf, 1, 1, jitter, info);
+}
+
+// ------------------------------------------------------------------ triangular mat-vecs
+// y = T x and z = T^T y for the upper factor T (strict upper triangle row-major in P, diagonal
+// in diagT): the fp64 predictions on the Nystrom points of Alg. 2 are
+// (Kmm + delta I) alpha = T^T (T alpha) once Kmm has been factored in place.  HBM-bound
+// streams of the triangle; fixed-order reductions (bitwise-reproducible on every rank).
+constexpr int TRMV_SEG = 32;  // row segments of the transposed product
+
+// y_r = diagT_r x_r + sum_{c > r} P[r m + c] x_c : one warp per row, coalesced, shuffle tree
+__global__ void __launch_bounds__(256) trmv_upper_kernel(const double *__restrict__ P,
+                                                         const double *__restrict__ diagT,
+                                                         int64_t m, const double *__restrict__ x,
+                                                         double *__restrict__ y) {
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= m) return;
+  const double *row = P + r * m;
+  double a0 = 0.0, a1 = 0.0;
+  int64_t c = r + 1 + lane;
+  for (; c + 32 < m; c += 64) {
+    a0 = fma(row[c], x[c], a0);
+    a1 = fma(row[c + 32], x[c + 32], a1);
   }
-  for (int f = 0; f < 2; ++f) {
-    if (hf[f] != ~0ULL) {
-      if (info) {
-        info->failed_factor = f;
-        info->failed_column = (int64_t)hf[f];
-      }
-      return fail(FALKON_ENOTPD, std::string("Cholesky of ") + (f ? "A" : "T") +
-                                     " failed at column " + std::to_string(hf[f]));
-    }
+  if (c < m) a0 = fma(row[c], x[c], a0);
+  double a = a0 + a1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if (lane == 0) y[r] = fma(diagT[r], x[r], a);
+}
+
+// part[s][c] = sum_{r in segment s, r < c} P[r m + c] y_r : thread per column, coalesced rows
+__global__ void __launch_bounds__(256) trmv_upper_t_part_kernel(const double *__restrict__ P,
+                                                                int64_t m,
+                                                                const double *__restrict__ y,
+                                                                double *__restrict__ part) {
+  const int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int s = blockIdx.y;
+  if (c >= m) return;
+  const int64_t seg = cdiv<int64_t>(m, TRMV_SEG);
+  const int64_t r0 = s * seg, r1 = lmin(lmin((int64_t)(s + 1) * seg, c), m);
+  double a0 = 0.0, a1 = 0.0;
+  int64_t r = r0;
+  for (; r + 1 < r1; r += 2) {
+    a0 = fma(P[r * m + c], y[r], a0);
+    a1 = fma(P[(r + 1) * m + c], y[r + 1], a1);
   }
+  if (r < r1) a0 = fma(P[r * m + c], y[r], a0);
+  part[(int64_t)s * m + c] = a0 + a1;
+}
+__global__ void trmv_upper_t_final_kernel(const double *__restrict__ diagT, int64_t m,
+                                          const double *__restrict__ y,
+                                          const double *__restrict__ part, double *__restrict__ z) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  double a = diagT[c] * y[c];
+  for (int s = 0; s < TRMV_SEG; ++s) a += part[(int64_t)s * m + c];
+  z[c] = a;
+}
+
+int trmv_TtT(falkon_ctx *ctx, const double *P, const double *diagT, int64_t m, const double *x,
+             double *tmp, double *z) {
+  void *pp;
+  FK_TRY(ws_get(ctx, WS_TRMV, sizeof(double) * TRMV_SEG * m, &pp));
+  LaunchScope ls(ctx, FALKON_T_PRECOND);
+  trmv_upper_kernel<<<(unsigned)cdiv<int64_t>(m, 8), 256, 0, ctx->stream>>>(P, diagT, m, x, tmp);
+  trmv_upper_t_part_kernel<<<dim3((unsigned)cdiv<int64_t>(m, 256), TRMV_SEG), 256, 0,
+                             ctx->stream>>>(P, m, tmp, (double *)pp);
+  trmv_upper_t_final_kernel<<<(unsigned)cdiv<int64_t>(m, 256), 256, 0, ctx->stream>>>(
+      diagT, m, tmp, (const double *)pp, z);
+  ctx->launches += 2;
+  FK_LAUNCH_CHECK();
   return FALKON_OK;
 }
 

@@ -21,11 +21,13 @@ def rate(fn, flops, reps=10):
     return flops / (best * 1e-3) / 1e12, best
 
 
-for N in (4096, 8192):
+for N in ((4096, 8192) if os.environ.get("PROBE_LIB", "1") == "1" else ()):
     a = torch.randn(N, N, dtype=torch.float64, device=dev)
     b = torch.randn(N, N, dtype=torch.float64, device=dev)
     out[f"cublas_dgemm_{N}_tflops"] = rate(lambda: a @ b, 2.0 * N ** 3)[0]
 N = 8192
+if os.environ.get("PROBE_LIB", "1") != "1":
+    N = 64
 a8 = torch.randint(-127, 127, (N, N), dtype=torch.int8, device=dev)
 b8 = torch.randint(-127, 127, (N, N), dtype=torch.int8, device=dev).t().contiguous().t()
 try:
@@ -36,7 +38,12 @@ a16 = torch.randn(N, N, dtype=torch.float16, device=dev)
 out["fp16_mm_8192_tflops"] = rate(lambda: a16 @ a16, 2.0 * N ** 3)[0]
 
 ctx = binding.Context(0)
-for m in [int(x) for x in os.environ.get("PROBE_M", "20000,50000").split(",")]:
+import itertools
+for warps, outer in itertools.product([int(x) for x in os.environ.get("PROBE_WARPS", "8").split(",")],
+                                      [int(x) for x in os.environ.get("PROBE_OUTER", "8").split(",")]):
+  ctx.set_option(binding.OPT_POTRF_OUTER, outer)
+  ctx.set_option(binding.OPT_GEMM_WARPS, warps)
+  for m in [int(x) for x in os.environ.get("PROBE_M", "20000,50000").split(",")]:
     cfg = synth.CONFIGS["msd"]
     C = torch.randn(m, cfg.d, dtype=torch.float32, device=dev)
     P = torch.empty(m * m, dtype=torch.float64, device=dev)
@@ -49,8 +56,8 @@ for m in [int(x) for x in os.environ.get("PROBE_M", "20000,50000").split(",")]:
     ctx.precond_build(C, 0, cfg.sigma, cfg.lam, 1e-8, P, dT, dA, W)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    out[f"precond_m{m}_s"] = dt
-    out[f"precond_m{m}_tflops_m3"] = m ** 3 / dt / 1e12
+    out[f"precond_w{warps}_o{outer}_m{m}_s"] = dt
+    out[f"precond_w{warps}_o{outer}_m{m}_tflops_m3"] = m ** 3 / dt / 1e12
     del P, W
     torch.cuda.empty_cache()
 print(json.dumps(out), flush=True)

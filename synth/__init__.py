@@ -64,6 +64,42 @@ CONFIGS = {
 }
 
 
+@dataclasses.dataclass(frozen=True)
+class GscConfig:
+    """LogFalkon (Alg. 2) workloads: Table 3 LogFalkon column for HIGGS
+    (m = 1e5, sigma = 5, lambda = 1e-9, 9 Newton steps) and a tiny case for the CPU oracle.
+    The level path is explicit (reading g5): geometric from mus[0] to lambda."""
+    name: str
+    base: str          # Config supplying n, d, seed and the +-1 labels
+    m: int
+    sigma: float
+    mus: tuple
+    iters: tuple
+
+
+def _geom(hi: float, lo: float, k: int) -> tuple:
+    return tuple(float(hi * (lo / hi) ** (i / (k - 1))) for i in range(k))
+
+
+GSC_CONFIGS = {
+    "tiny_log": GscConfig("tiny_log", "tiny", 100, 1.0, _geom(1e-2, 1e-6, 5), (5, 5, 5, 5, 10)),
+    "higgs_log": GscConfig("higgs_log", "higgs", 100_000, 5.0, _geom(1e-3, 1e-9, 9),
+                           (5,) * 8 + (10,)),
+}
+
+
+def make_gsc_problem(name: str, n: int | None = None, m: int | None = None):
+    """(gcfg, X, y, C, yC): +-1 labels (cls task of the base config), C = m rows of X and
+    yC = their labels (the y_m of Alg. 2)."""
+    g = GSC_CONFIGS[name]
+    base = CONFIGS[g.base]
+    nn = base.n if n is None else n
+    mm = g.m if m is None else m
+    X = gen_X(base.seed, 0, nn, base.d)
+    y = gen_y(base.seed, X, 0, "cls")
+    idx = center_indices(base.seed, nn, mm)
+    return g, X, y, X[idx].copy(), y[idx].copy()
+
 def _splitmix64(z: np.ndarray) -> np.ndarray:
     z = (z + _GOLD) & _M64
     z = ((z ^ (z >> np.uint64(30))) * _C1) & _M64
@@ -109,6 +145,17 @@ def gen_X(cfg_or_seed, row0: int = 0, nrows: int | None = None, d: int | None = 
 def gen_y(seed: int, X: np.ndarray, row0: int, task: str = "reg") -> np.ndarray:
     """Targets for rows [row0, row0+len(X)) (fp32)."""
     noise = _normals(seed, STREAM_NOISE, np.arange(row0, row0 + X.shape[0], dtype=np.int64))
+    k = min(3, X.shape[1])
+    y = np.sin(X[:, :k].astype(np.float64).sum(axis=1)) + 0.3 * noise
+    if task == "cls":
+        y = np.where(y >= 0.0, 1.0, -1.0)
+    return y.astype(np.float32)
+
+
+def gen_y_rows(seed: int, X: np.ndarray, rows: np.ndarray, task: str = "reg") -> np.ndarray:
+    """Targets of the generator rows `rows` (any subset, e.g. the centres' y_m) given those
+    rows' X; equals gen_y on a contiguous range."""
+    noise = _normals(seed, STREAM_NOISE, np.asarray(rows, dtype=np.int64))
     k = min(3, X.shape[1])
     y = np.sin(X[:, :k].astype(np.float64).sum(axis=1)) + 0.3 * noise
     if task == "cls":

@@ -186,3 +186,16 @@ def test_path_decreases_objective_and_newton_path_schedule():
     objs = [gsc.objective(X, y, C, a, gsc.LOGISTIC, G, s, lam) for a in path]
     assert objs[-1] <= min(objs[:-1]) + 1e-12
     assert objs[0] < gsc.objective(X, y, C, np.zeros(len(C)), gsc.LOGISTIC, G, s, lam)
+
+
+def test_center_labels_are_the_rows_labels():
+    """synth.gen_y_rows on the centre indices equals the labels of those rows (y_m of Alg. 2,
+    PAPER.md:964: the Nystrom points keep their own labels)."""
+    import synth
+    X = synth.gen_X(3, 0, 1000, 28)
+    y = synth.gen_y(3, X, 0, "cls")
+    idx = synth.center_indices(3, 1000, 50)
+    assert np.array_equal(synth.gen_y_rows(3, X[idx], idx, "cls"), y[idx])
+    g, Xg, yg, C, yC = synth.make_gsc_problem("tiny_log")
+    idx = synth.center_indices(0, 2000, 100)
+    assert np.array_equal(C, Xg[idx]) and np.array_equal(yC, yg[idx])
