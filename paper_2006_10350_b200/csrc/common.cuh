@@ -58,6 +58,7 @@ enum WsSlot {
   WS_DW,          // fp32 n: per-row curvature weights D (GSC LinOp, Alg. 2)
   WS_Z64,         // fp64 n: predictions z = Knm alpha on the rows (GSC)
   WS_GSC,         // fp64 m vectors of the GSC outer loop
+  WS_TRSV,        // fp64 m: sentinel-initialised output of the triangular solve
   WS_COUNT
 };
 

@@ -818,13 +818,14 @@ int trmv_TtT(falkon_ctx *ctx, const double *P, const double *diagT, int64_t m, c
 }
 
 // ------------------------------------------------------------------ sync-free blocked TRSV
-// Solves L z = r (forward) or L^T z = r (backward) in place for the lower-triangular view L,
-// with Dinv = the inverses of L's 64 x 64 diagonal blocks (written by the factorization).
+// Solves L z = r (forward) or L^T z = r (backward) for the lower-triangular view L, with
+// Dinv = the inverses of L's 64 x 64 diagonal blocks (written by the factorization).
 // CTA with ticket b owns row block I (forward: I = b, backward: I = nb-1-b): it streams its
-// off-diagonal 64 x 64 tiles from HBM into shared memory with cp.async one tile ahead of the
-// dependency front, multiplies each by z_J as soon as flags[J] == gen, then finishes its
-// block with the 64 x 64 inverse (a parallel mat-vec, no sequential substitution), so the
-// serial chain per block is a few L2 round trips and the solve streams at HBM rate.
+// off-diagonal 64 x 64 tiles from HBM into shared memory with cp.async ahead of the
+// dependency front, multiplies each by z_J as soon as z_J is final (sentinel-tagged output,
+// see trsv_kernel), then finishes its block with the 64 x 64 inverse (a parallel mat-vec, no
+// sequential substitution), so the serial chain per block is ~one L2 round trip plus a few
+// shared-memory mat-vecs, and the solve streams the triangle at HBM rate behind it.
 constexpr int TS_LD = TB + 2;  // smem row stride (doubles), 16 B aligned rows
 
 
@@ -849,30 +850,34 @@ __device__ __forceinline__ void tile_async(double *dst, const double *src, int64
   }
 }
 
-constexpr int TRSV_ZR = 16;  // z blocks fetched per L2 round trip (ring of ready z_J)
+constexpr int TRSV_ZR = 16;  // z blocks fetched per L2 round trip
+
+// Readiness of the solution travels with the data: the output vector zo is pre-filled with a
+// NaN sentinel (all bits set) and every element is written exactly once, so a consumer that
+// reads a non-sentinel value holds the final value -- one L2 round trip from the producer's
+// store to the consumer, no fence / counter / second fetch on the dependency chain.
+constexpr unsigned long long TRSV_SENT = ~0ULL;
+__device__ __forceinline__ bool is_sent(double v) {
+  return (unsigned long long)__double_as_longlong(v) == TRSV_SENT;
+}
 
 __global__ void __launch_bounds__(256) trsv_kernel(View L, int64_t m, int forward,
-                                                   double *__restrict__ z,
-                                                   const double *__restrict__ Dinv,
-                                                   unsigned int *__restrict__ counter,
-                                                   unsigned int *__restrict__ done) {
-  // Blocks finish strictly in dependency order, so one monotone counter `done` (number of
-  // finished blocks, in solve order) tells every CTA which z_J are final.  Tiles of L do not
-  // depend on z, so they are prefetched (cp.async, 2 deep) regardless of the front; the
-  // final z_J are fetched in batches of up to TRSV_ZR blocks per L2 round trip, and the
-  // counter is polled only when a CTA reaches the dependency front.
+                                                   const double *__restrict__ rhs,
+                                                   double *zo, const double *__restrict__ Dinv,
+                                                   unsigned int *__restrict__ counter) {
+  // CTAs take row blocks in solve order (ticket); tiles of L do not depend on z, so they are
+  // prefetched (cp.async, 2 deep) regardless of the front; final z_J are fetched in batches of
+  // up to TRSV_ZR blocks per L2 round trip; at the front the CTA spins on the sentinel.
   extern __shared__ __align__(16) double tsm[];
   double *sT0 = tsm, *sT1 = tsm + TB * TS_LD;
   double *sD = tsm + 2 * TB * TS_LD;
   double *zr = sD + TB * TS_LD;   // [TRSV_ZR * TB]
   double *sx = zr + TRSV_ZR * TB;  // [TB]
-  __shared__ unsigned int s_ticket, s_known;
+  __shared__ unsigned int s_ticket;
+  __shared__ int s_ready;
   const int tid = threadIdx.x;
   const int64_t nblk = cdiv<int64_t>(m, TB);
-  if (tid == 0) {
-    s_ticket = atomicAdd(counter, 1u);
-    s_known = 0;
-  }
+  if (tid == 0) s_ticket = atomicAdd(counter, 1u);
   __syncthreads();
   const int64_t b = s_ticket;  // this block's rank in solve order
   const int64_t I = forward ? b : nblk - 1 - b;
@@ -904,25 +909,35 @@ __global__ void __launch_bounds__(256) trsv_kernel(View L, int64_t m, int forwar
   for (int64_t s = 0; s < nJ; ++s) {
     if (s + 1 < nJ) issue(s + 1);
     if (s >= zhi) {
-      if (s >= (int64_t)s_known) {  // at the dependency front: poll the counter
-        if (tid == 0) {
-          volatile unsigned int *d = done;
-          unsigned int v;
-          while ((v = *d) <= (unsigned int)s) {
-          }
-          __threadfence();
-          s_known = v;
-        }
-        __syncthreads();
+      // batch-fetch blocks [s, s + TRSV_ZR); the ready prefix ends at the first sentinel
+      const int64_t want = lmin(nJ, s + TRSV_ZR);
+      if (tid == 0) s_ready = (int)(want - s);
+      __syncthreads();
+      for (int e = tid; e < (want - s) * TB; e += blockDim.x) {
+        const int64_t st = s + e / TB;
+        const int64_t jg = j0of(st) + e % TB;
+        const double v = jg < m ? __ldcg(zo + jg) : 0.0;
+        zr[e] = v;
+        if (is_sent(v)) atomicMin(&s_ready, (int)(e / TB));
       }
+      __syncthreads();
       zlo = s;
-      zhi = lmin((int64_t)s_known, s + TRSV_ZR);
-      for (int e = tid; e < (zhi - zlo) * TB; e += blockDim.x) {
-        const int64_t st = zlo + e / TB;
-        const int jj = e % TB;
-        const int64_t jg = j0of(st) + jj;
-        zr[e] = jg < m ? __ldcg(z + jg) : 0.0;
+      zhi = s + s_ready;
+      if (zhi == s) {  // at the dependency front: spin on block s itself
+        if (tid < TB) {
+          const int64_t jg = j0of(s) + tid;
+          double v = 0.0;
+          if (jg < m) {
+            const volatile double *pz = zo + jg;
+            do {
+              v = *pz;
+            } while (is_sent(v));
+          }
+          zr[tid] = v;
+        }
+        zhi = s + 1;
       }
+      __syncthreads();
     }
     if (s + 1 < nJ) cp_async_wait<1>();
     else cp_async_wait<0>();
@@ -954,8 +969,8 @@ __global__ void __launch_bounds__(256) trsv_kernel(View L, int64_t m, int forwar
   part[qq * TB + ri] = acc;
   __syncthreads();
   if (tid < TB)
-    sx[tid] = (tid < nI) ? z[i0 + tid] - (part[tid] + part[TB + tid] + part[2 * TB + tid] +
-                                         part[3 * TB + tid])
+    sx[tid] = (tid < nI) ? rhs[i0 + tid] - (part[tid] + part[TB + tid] + part[2 * TB + tid] +
+                                           part[3 * TB + tid])
                          : 0.0;
   __syncthreads();
   // z_I = D x (forward, D = Dinv_I) or D^T x (backward): parallel, no substitution
@@ -971,10 +986,11 @@ __global__ void __launch_bounds__(256) trsv_kernel(View L, int64_t m, int forwar
     part[q4 * TB + r] = v;
   }
   __syncthreads();
-  if (tid < nI) z[i0 + tid] = part[tid] + part[TB + tid] + part[2 * TB + tid] + part[3 * TB + tid];
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) atomicMax(done, (unsigned int)(b + 1));
+  if (tid < nI) {
+    double v = part[tid] + part[TB + tid] + part[2 * TB + tid] + part[3 * TB + tid];
+    if (is_sent(v)) v = __longlong_as_double(0x7ff8000000000000LL);  // keep the sentinel unique
+    __stcg(zo + i0 + tid, v);
+  }
 }
 
 int64_t precond_work_elems(int64_t m) { return 2 * cdiv<int64_t>(m, TB) * (int64_t)(TB * TB); }
@@ -987,16 +1003,21 @@ int trsv(falkon_ctx *ctx, const double *P, const double *diag, const double *wor
   const double *dinv = work + (which == 0 ? 0 : precond_work_elems(m) / 2);
   const int forward = trans ? 1 : 0;
   const int64_t nblk = cdiv<int64_t>(m, TB);
-  void *fl;
+  void *fl, *zb;
   FK_TRY(ws_get(ctx, WS_FLAGS, 64 + sizeof(unsigned int) * (nblk + 64), &fl));
-  unsigned int *counter = (unsigned int *)((char *)fl + 32);  // [0] ticket, [1] done
+  FK_TRY(ws_get(ctx, WS_TRSV, sizeof(double) * m, &zb));
+  unsigned int *counter = (unsigned int *)((char *)fl + 32);
   const size_t smem = sizeof(double) * (3 * TB * TS_LD + (TRSV_ZR + 1) * TB);
   FK_CUDA(cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  FK_CUDA(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned int), ctx->stream));
-  LaunchScope ls(ctx, FALKON_T_TRSV);
-  trsv_kernel<<<(unsigned)nblk, 256, smem, ctx->stream>>>(L, m, forward, x, dinv, counter,
-                                                          counter + 1);
+  FK_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), ctx->stream));
+  FK_CUDA(cudaMemsetAsync(zb, 0xff, sizeof(double) * m, ctx->stream));  // sentinel
+  {
+    LaunchScope ls(ctx, FALKON_T_TRSV);
+    trsv_kernel<<<(unsigned)nblk, 256, smem, ctx->stream>>>(L, m, forward, x, (double *)zb, dinv,
+                                                            counter);
+  }
   FK_LAUNCH_CHECK();
+  FK_CUDA(cudaMemcpyAsync(x, zb, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
   return FALKON_OK;
 }
 
