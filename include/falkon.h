@@ -72,7 +72,8 @@ enum {
                                    2 = 1/4, 3 = 1/2 of the entries (rest on MUFU) */
   FALKON_OPT_POTRF_OUTER = 6,   /* blocked Cholesky: depth of the trailing fp64 GEMM updates in
                                    units of 128 columns (1..64, default 8) */
-  FALKON_OPT_GEMM_WARPS = 7     /* fp64 DMMA GEMM CTA: 8 (32 x 64 warp tiles) or 16 (32 x 32) */
+  FALKON_OPT_GEMM_WARPS = 7     /* fp64 DMMA GEMM CTA: 8 (128 x 128 tile, 8 warps), 16 (16 warps)
+                                   or 2 (128 x 64 tiles, 2 CTAs of 8 warps per SM) */
 };
 
 /* Per-launch-class accumulated device times in ms (falkon_ctx_timings). */

@@ -417,7 +417,8 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
       ctx->opt.exp_offload = (int)value;
       return FALKON_OK;
     case FALKON_OPT_GEMM_WARPS:
-      if (value != 8 && value != 16) return fail(FALKON_EINVAL, "gemm warps must be 8 or 16");
+      if (value != 8 && value != 16 && value != 2)
+        return fail(FALKON_EINVAL, "gemm variant must be 8, 16 (warps, 1 CTA/SM) or 2 (2 CTAs/SM)");
       ctx->opt.gemm_warps = (int)value;
       return FALKON_OK;
     case FALKON_OPT_POTRF_OUTER:

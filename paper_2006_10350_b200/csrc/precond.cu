@@ -290,23 +290,23 @@ __device__ __forceinline__ bool view_dense(const View &v, int64_t r0, int64_t nr
   return true;
 }
 // masked / diagonal-touching chunks (rare): kept out of line to keep the hot loop small
-template <int NTHR>
-__device__ __noinline__ void gemm_async_chunk_masked(const View v, double (*s)[GT + GPAD],
+template <int NTHR, int ROWS>
+__device__ __noinline__ void gemm_async_chunk_masked(const View v, double (*s)[ROWS + GPAD],
                                                      int64_t row0, int64_t rmax, int64_t k,
                                                      int64_t kmax) {
   const int tid = threadIdx.x;
   constexpr int RP = NTHR / GK;  // rows per pass (storage contiguous along k)
-  constexpr int KP = NTHR / GT;  // k-rows per pass (storage contiguous along rows)
+  constexpr int KP = NTHR / ROWS;  // k-rows per pass (storage contiguous along rows)
   if (!v.trans) {
     const int kk = tid % GK, rr = tid / GK;
-    for (int p = 0; p < GT / RP; ++p) {
+    for (int p = 0; p < ROWS / RP; ++p) {
       const int64_t r = row0 + rr + RP * p, kg = k + kk;
       bool ok = r < rmax && kg < kmax;
       const double *src = ok ? vsrc(v, r, kg, ok) : v.base;
       cp_async8z(&s[kk][rr + RP * p], src, ok);
     }
   } else {
-    const int rr = tid % GT, kk = tid / GT;
+    const int rr = tid % ROWS, kk = tid / ROWS;
     for (int p = 0; p < GK / KP; ++p) {
       const int64_t r = row0 + rr, kg = k + kk + KP * p;
       bool ok = r < rmax && kg < kmax;
@@ -316,28 +316,28 @@ __device__ __noinline__ void gemm_async_chunk_masked(const View v, double (*s)[G
   }
 }
 
-template <int NTHR>
-__device__ __forceinline__ void gemm_async_chunk(const View &v, double (*s)[GT + GPAD],
+template <int NTHR, int ROWS>
+__device__ __forceinline__ void gemm_async_chunk(const View &v, double (*s)[ROWS + GPAD],
                                                  int64_t row0, int64_t rmax, int64_t k,
                                                  int64_t kmax) {
   const int tid = threadIdx.x;
-  if (view_dense(v, row0, GT, k, GK)) {
+  if (view_dense(v, row0, ROWS, k, GK)) {
     // branch-free: out-of-range rows/columns are zero-filled from a clamped address
     constexpr int RP = NTHR / GK;
-    constexpr int KP = NTHR / GT;
+    constexpr int KP = NTHR / ROWS;
     if (!v.trans) {
       const int kk = tid % GK, rr = tid / GK;
       const int64_t kg = k + kk;
       const bool kok = kg < kmax;
       const int64_t kc = kok ? kg : k;
 #pragma unroll
-      for (int p = 0; p < GT / RP; ++p) {
+      for (int p = 0; p < ROWS / RP; ++p) {
         const int64_t r = row0 + rr + RP * p;
         const bool ok = kok && r < rmax;
         cp_async8z(&s[kk][rr + RP * p], v.base + (ok ? r : row0) * v.ld + kc, ok);
       }
     } else {
-      const int rr = tid % GT, kk = tid / GT;
+      const int rr = tid % ROWS, kk = tid / ROWS;
       const int64_t r = row0 + rr;
       const bool rok = r < rmax;
       const int64_t rc = rok ? r : row0;
@@ -350,33 +350,34 @@ __device__ __forceinline__ void gemm_async_chunk(const View &v, double (*s)[GT +
     }
     return;
   }
-  gemm_async_chunk_masked<NTHR>(v, s, row0, rmax, k, kmax);
+  gemm_async_chunk_masked<NTHR, ROWS>(v, s, row0, rmax, k, kmax);
 }
 
+template <int TN>
 __device__ __noinline__ void gemm_epilogue(const GemmArgs a, const double *sC, int64_t i0,
                                            int64_t j0) {
-  constexpr int CLD = GT + 1;
+  constexpr int CLD = TN + 1;
   constexpr int BATCH = 8;  // independent reads in flight per thread
-  for (int e0 = threadIdx.x; e0 < GT * GT; e0 += BATCH * blockDim.x) {
+  for (int e0 = threadIdx.x; e0 < GT * TN; e0 += BATCH * blockDim.x) {
     double cv[BATCH];
 #pragma unroll
     for (int u = 0; u < BATCH; ++u) {
       const int e = e0 + u * blockDim.x;
-      const int li_t = a.C.trans ? (e % GT) : (e / GT);
-      const int lj_t = a.C.trans ? (e / GT) : (e % GT);
+      const int li_t = a.C.trans ? (e % GT) : (e / TN);
+      const int lj_t = a.C.trans ? (e / GT) : (e % TN);
       const int64_t li = i0 + li_t, lj = j0 + lj_t;
       cv[u] = 0.0;
-      if (e < GT * GT && li < a.M && lj < a.N && a.beta != 0.0)
+      if (e < GT * TN && li < a.M && lj < a.N && a.beta != 0.0)
         cv[u] = vget(a.C, a.rc + li, a.cc + lj);
     }
 #pragma unroll
     for (int u = 0; u < BATCH; ++u) {
       // storage order: consecutive threads walk the contiguous dimension of C's storage
       const int e = e0 + u * blockDim.x;
-      const int li_t = a.C.trans ? (e % GT) : (e / GT);
-      const int lj_t = a.C.trans ? (e / GT) : (e % GT);
+      const int li_t = a.C.trans ? (e % GT) : (e / TN);
+      const int lj_t = a.C.trans ? (e / GT) : (e % TN);
       const int64_t li = i0 + li_t, lj = j0 + lj_t;
-      if (e >= GT * GT || li >= a.M || lj >= a.N) continue;
+      if (e >= GT * TN || li >= a.M || lj >= a.N) continue;
       const int64_t r = a.rc + li, c = a.cc + lj;
       if (a.C.tri == 1 && r < c) continue;
       if (a.C.tri == 2 && c < r) continue;
@@ -393,33 +394,40 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// CTA tile 128 x 128, 4 x WN warps, warp tile 32 x (8 NT) = 4 x NT DMMA tiles (WN = 2, NT = 8:
-// 8 warps, 32 x 64, 12 fragments per 32 MMAs; WN = 4, NT = 4: 16 warps, 32 x 32, 8 fragments
-// per 16 MMAs, twice the warps to hide DMMA issue latency).  k-chunks of GK are staged
-// global -> shared with cp.async (GSTAGES deep) through the views.
+// CTA tile 128 x TN (TN = 8 NT WN), 4 x WN warps, warp tile 32 x (8 NT) = 4 x NT DMMA tiles:
+//   <2, 8>: 8 warps, 128 x 128, 32 x 64 warp tiles (12 fragments per 32 MMAs), 1 CTA / SM;
+//   <4, 4>: 16 warps, 128 x 128, 32 x 32 warp tiles, 1 CTA / SM;
+//   <2, 4>: 8 warps, 128 x 64, 32 x 32 warp tiles, 2 CTAs / SM (<= 128 registers): the two
+//           CTAs' barriers, prologues and epilogues interleave, so the DMMA pipe (one DMMA per
+//           16 cycles per warp, SASS stall count 15) keeps >= 2 issuing warps per SMSP.
+// k-chunks of GK are staged global -> shared with cp.async (GSTAGES deep) through the views.
 template <int WN, int NT>
-__global__ void __launch_bounds__(128 * WN) gemm_f64_kernel(GemmArgs a) {
+__global__ void __launch_bounds__(128 * WN, (WN == 2 && NT == 4) ? 2 : 1)
+    gemm_f64_kernel(GemmArgs a) {
   constexpr int NTHR = 128 * WN;
+  constexpr int TN = 8 * NT * WN;
+  constexpr int R = GT / TN;  // column tiles per 128-row tile width
   int64_t ti, tj;
   if (a.tri_tiles) {
+    // row tile ti holds R (ti + 1) column tiles of the lower region
     const int64_t t = blockIdx.x;
-    ti = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-    while (ti * (ti + 1) / 2 > t) --ti;
-    tj = t - ti * (ti + 1) / 2;
+    ti = (int64_t)((sqrt(8.0 * (double)t / R + 1.0) - 1.0) * 0.5);
+    while (R * (ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    while (R * ti * (ti + 1) / 2 > t) --ti;
+    tj = t - R * ti * (ti + 1) / 2;
   } else {
     ti = blockIdx.y;
     tj = blockIdx.x;
   }
-  const int64_t i0 = ti * GT, j0 = tj * GT;
+  const int64_t i0 = ti * GT, j0 = tj * TN;
   if (i0 >= a.M || j0 >= a.N) return;
   const int64_t kb = a.k_from_row ? lmax(a.k0, a.ra + i0) : a.k0;
   const int64_t ke = a.k1;
 
   extern __shared__ __align__(16) double gsm[];
   double(*As)[GK][GT + GPAD] = reinterpret_cast<double(*)[GK][GT + GPAD]>(gsm);
-  double(*Bs)[GK][GT + GPAD] =
-      reinterpret_cast<double(*)[GK][GT + GPAD]>(gsm + GSTAGES * GK * (GT + GPAD));
+  double(*Bs)[GK][TN + GPAD] =
+      reinterpret_cast<double(*)[GK][TN + GPAD]>(gsm + GSTAGES * GK * (GT + GPAD));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wr = warp / WN, wc = warp % WN;
@@ -428,8 +436,8 @@ __global__ void __launch_bounds__(128 * WN) gemm_f64_kernel(GemmArgs a) {
   // Tiles strictly inside C's triangle (the vast majority) accumulate on top of C itself:
   // acc starts at (beta/alpha) C, loaded here so the loads overlap the pipeline fill, and the
   // epilogue is a plain store of alpha * acc (no read-modify-write round trips).
-  const bool cdense = view_dense(a.C, a.rc + i0, GT, a.cc + j0, GT) && i0 + GT <= a.M &&
-                      j0 + GT <= a.N;
+  const bool cdense = view_dense(a.C, a.rc + i0, GT, a.cc + j0, TN) && i0 + GT <= a.M &&
+                      j0 + TN <= a.N;
   const int64_t csr = a.C.trans ? 1 : a.C.ld, csc = a.C.trans ? a.C.ld : 1;
   double *cfrag =
       a.C.base + (a.rc + i0 + wr * 32 + g) * csr + (a.cc + j0 + wc * (8 * NT) + 2 * q) * csc;
@@ -455,8 +463,8 @@ __global__ void __launch_bounds__(128 * WN) gemm_f64_kernel(GemmArgs a) {
 #pragma unroll
   for (int c = 0; c < GSTAGES - 1; ++c) {
     if (c < nch) {
-      gemm_async_chunk<NTHR>(a.A, As[c], ra, ramax, kb + (int64_t)c * GK, ke);
-      gemm_async_chunk<NTHR>(a.B, Bs[c], rb, rbmax, kb + (int64_t)c * GK, ke);
+      gemm_async_chunk<NTHR, GT>(a.A, As[c], ra, ramax, kb + (int64_t)c * GK, ke);
+      gemm_async_chunk<NTHR, TN>(a.B, Bs[c], rb, rbmax, kb + (int64_t)c * GK, ke);
     }
     cp_async_commit();
   }
@@ -466,8 +474,8 @@ __global__ void __launch_bounds__(128 * WN) gemm_f64_kernel(GemmArgs a) {
     if (a.kscale) {  // T D T^T of Alg. 2: scale the staged B chunk by D(k)
       const int st = c % GSTAGES;
       const int64_t kc = kb + (int64_t)c * GK;
-      for (int e = tid; e < GK * GT; e += NTHR) {
-        const int kk = e / GT, j = e % GT;
+      for (int e = tid; e < GK * TN; e += NTHR) {
+        const int kk = e / TN, j = e % TN;
         if (kc + kk < ke) Bs[st][kk][j] *= a.kscale[kc + kk];
       }
       __syncthreads();
@@ -475,8 +483,8 @@ __global__ void __launch_bounds__(128 * WN) gemm_f64_kernel(GemmArgs a) {
     {
       const int cn = c + GSTAGES - 1;
       if (cn < nch) {
-        gemm_async_chunk<NTHR>(a.A, As[cn % GSTAGES], ra, ramax, kb + (int64_t)cn * GK, ke);
-        gemm_async_chunk<NTHR>(a.B, Bs[cn % GSTAGES], rb, rbmax, kb + (int64_t)cn * GK, ke);
+        gemm_async_chunk<NTHR, GT>(a.A, As[cn % GSTAGES], ra, ramax, kb + (int64_t)cn * GK, ke);
+        gemm_async_chunk<NTHR, TN>(a.B, Bs[cn % GSTAGES], rb, rbmax, kb + (int64_t)cn * GK, ke);
       }
       cp_async_commit();
     }
@@ -511,8 +519,8 @@ __global__ void __launch_bounds__(128 * WN) gemm_f64_kernel(GemmArgs a) {
     return;
   }
   __syncthreads();
-  double *sC = gsm;  // [GT][GT + 1]
-  constexpr int CLD = GT + 1;
+  double *sC = gsm;  // [GT][TN + 1]
+  constexpr int CLD = TN + 1;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -521,18 +529,19 @@ __global__ void __launch_bounds__(128 * WN) gemm_f64_kernel(GemmArgs a) {
       for (int h = 0; h < 2; ++h)
         sC[(wr * 32 + mt * 8 + g) * CLD + wc * (8 * NT) + nt * 8 + 2 * q + h] = acc[mt][nt][h];
   __syncthreads();
-  gemm_epilogue(a, sC, i0, j0);
+  gemm_epilogue<TN>(a, sC, i0, j0);
 }
 
 template <int WN, int NT>
 static int gemm_launch(falkon_ctx *ctx, const GemmArgs &a) {
-  const size_t smem = sizeof(double) * 2 * GSTAGES * GK * (GT + GPAD);
+  constexpr int TN = 8 * NT * WN, R = GT / TN;
+  const size_t smem = sizeof(double) * GSTAGES * GK * (GT + TN + 2 * GPAD);
   FK_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<WN, NT>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t tm = cdiv<int64_t>(a.M, GT), tn = cdiv<int64_t>(a.N, GT);
+  const int64_t tm = cdiv<int64_t>(a.M, GT), tn = cdiv<int64_t>(a.N, TN);
   LaunchScope ls(ctx, FALKON_T_PRECOND);
   if (a.tri_tiles) {
-    gemm_f64_kernel<WN, NT><<<(unsigned)(tm * (tm + 1) / 2), 128 * WN, smem, ctx->stream>>>(a);
+    gemm_f64_kernel<WN, NT><<<(unsigned)(R * tm * (tm + 1) / 2), 128 * WN, smem, ctx->stream>>>(a);
   } else {
     gemm_f64_kernel<WN, NT><<<dim3((unsigned)tn, (unsigned)tm), 128 * WN, smem, ctx->stream>>>(a);
   }
@@ -542,7 +551,11 @@ static int gemm_launch(falkon_ctx *ctx, const GemmArgs &a) {
 
 static int gemm(falkon_ctx *ctx, const GemmArgs &a) {
   if (a.M <= 0 || a.N <= 0) return FALKON_OK;
-  return ctx->opt.gemm_warps == 16 ? gemm_launch<4, 4>(ctx, a) : gemm_launch<2, 8>(ctx, a);
+  switch (ctx->opt.gemm_warps) {
+    case 16: return gemm_launch<4, 4>(ctx, a);
+    case 2: return gemm_launch<2, 4>(ctx, a);  // 2 CTAs of 8 warps per SM
+    default: return gemm_launch<2, 8>(ctx, a);
+  }
 }
 
 // ------------------------------------------------------------------ blocked Cholesky

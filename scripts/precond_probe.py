@@ -39,13 +39,15 @@ out["fp16_mm_8192_tflops"] = rate(lambda: a16 @ a16, 2.0 * N ** 3)[0]
 
 ctx = binding.Context(0)
 import itertools
+REF = {}
 for warps, outer in itertools.product([int(x) for x in os.environ.get("PROBE_WARPS", "8").split(",")],
                                       [int(x) for x in os.environ.get("PROBE_OUTER", "8").split(",")]):
   ctx.set_option(binding.OPT_POTRF_OUTER, outer)
   ctx.set_option(binding.OPT_GEMM_WARPS, warps)
   for m in [int(x) for x in os.environ.get("PROBE_M", "20000,50000").split(",")]:
     cfg = synth.CONFIGS["msd"]
-    C = torch.randn(m, cfg.d, dtype=torch.float32, device=dev)
+    C = torch.randn(m, cfg.d, dtype=torch.float32, device=dev,
+                    generator=torch.Generator(device=dev).manual_seed(m))
     P = torch.empty(m * m, dtype=torch.float64, device=dev)
     dT = torch.empty(m, dtype=torch.float64, device=dev)
     dA = torch.empty(m, dtype=torch.float64, device=dev)
@@ -57,6 +59,13 @@ for warps, outer in itertools.product([int(x) for x in os.environ.get("PROBE_WAR
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     out[f"precond_w{warps}_o{outer}_m{m}_s"] = dt
+    key = ("ref", m)
+    if key not in REF:
+        REF[key] = (P.clone(), dT.clone(), dA.clone())
+    else:
+        Pr, dTr, dAr = REF[key]
+        out[f"precond_w{warps}_o{outer}_m{m}_maxdiff"] = max(
+            float((P - Pr).abs().max()), float((dT - dTr).abs().max()), float((dA - dAr).abs().max()))
     out[f"precond_w{warps}_o{outer}_m{m}_tflops_m3"] = m ** 3 / dt / 1e12
     del P, W
     torch.cuda.empty_cache()
