@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--gsc-config", default=None, choices=[None] + list(synth.GSC_CONFIGS),
                     help="also time one GSC-Falkon / LogFalkon fit (Alg. 2) on this workload")
     ap.add_argument("--gsc-n", type=int, default=None, help="override the GSC workload's n")
+    ap.add_argument("--multi-k", type=int, default=0,
+                    help="also time the k-output product Knm^T (Knm V), V in R^{m x k} (NEXT-3)")
     ap.add_argument("--quick", action="store_true",
                     help="timed product steps only (no e2e, cpu_baseline, fit): for ncu runs")
     return ap.parse_args()
@@ -437,6 +439,29 @@ def main():
         except Exception as ex:  # report, do not hide
             fit = {"error": str(ex)}
 
+    multi = None
+    if args.multi_k > 0:
+        k = args.multi_k
+        V = torch.from_numpy(np.random.default_rng(7).standard_normal((m, k))).cuda()
+        U = torch.zeros((m, k), dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            ctx.knm_matmat(X, C, V, kernel, sigma, U)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(2, min(args.steps, 5))
+        e0.record(stream)
+        for _ in range(reps):
+            ctx.knm_matmat(X, C, V, kernel, sigma, U)
+        e1.record(stream)
+        barrier()
+        ms_k = e0.elapsed_time(e1) / reps
+        if world > 1:
+            t = torch.tensor([ms_k], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_k = float(t.item())
+        multi = {"k": k, "ms_per_product": ms_k, "value": n_global * m * k / (ms_k * 1e-3),
+                 "unit": "n*m*k/s", "vs_k_single_products": k * ms_step / ms_k}
+
     gsc_fit = None
     if args.gsc_config and not args.quick:
         gsc_fit = run_gsc(args, ctx, world, rank, barrier)
@@ -463,7 +488,7 @@ def main():
                               "%.0f MB < 2x L2)" if flush else "inputs larger than L2 (packed X "
                               "%.0f MB)") % (packed / 1e6)},
             "clocks": clk, "gpu_launches": int(launches), "roofline": roof, "e2e": e2e,
-            "cpu_baseline": cpu, "fit": fit, "gsc_fit": gsc_fit,
+            "cpu_baseline": cpu, "fit": fit, "gsc_fit": gsc_fit, "multi_output": multi,
             "kernel_ms": {k: v[0] for k, v in kt.items()},
         }
         print(json.dumps(out), flush=True)

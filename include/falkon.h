@@ -188,6 +188,31 @@ int falkon_predict(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d,
                    const float *C, int64_t m, int kernel, double sigma,
                    const double *alpha, double *f);
 
+/* ---- multi-output (k outputs, e.g. TIMIT's 144 classes) -- */
+
+/* U = sum over ranks of Knm_r^T (Knm_r V) for k vectors at once.  V, U: m x k fp64 ROW-MAJOR
+   (replicated; U allreduced).  On the tensor path the vectors go through the fused kernel in
+   blocks of 8 or 16 (one cross term + exp per entry for the whole block);
+   on the SIMT path (Laplacian, d <= 8) each column is its own pass.  k >= 1. */
+int falkon_knm_matmat(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d,
+                      const float *C, int64_t m, int kernel, double sigma,
+                      const double *V, int64_t k, double *U);
+
+/* F = k(X, C) alpha for k coefficient columns (Eq. (4)); alpha m x k, F n_local x k fp64,
+   row-major; no collective. */
+int falkon_predict_multi(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d,
+                         const float *C, int64_t m, int kernel, double sigma,
+                         const double *alpha, int64_t k, double *F);
+
+/* Multi-output Falkon: Alg. 1 for the k columns of Y (n_local x k fp32 row-major) at once.
+   The k CGs are independent (per-column step sizes and breakdown rules, reading c9) and share
+   the preconditioner and every kernel product.  alpha: m x k fp64 row-major (replicated).
+   info->iters_run is the mean over columns; other fields as falkon_fit. */
+int falkon_fit_multi(falkon_ctx *ctx, const float *X, const float *Y, int64_t n_local, int64_t d,
+                     const float *C, int64_t m, int64_t k, int kernel, double sigma,
+                     double lambda, int32_t iters, double jitter, double *alpha,
+                     falkon_fit_info *info);
+
 /* ---- GSC-Falkon / LogFalkon (Appendix B, Alg. 2) ------------------- */
 
 /* Losses of falkon_gsc_fit (Def. 1 / Example 1). */

@@ -33,7 +33,8 @@ EXPORTS = ["falkon_get_unique_id", "falkon_ctx_create", "falkon_ctx_destroy",
            "falkon_ctx_set_stream", "falkon_ctx_set_option", "falkon_ctx_timings",
            "falkon_ctx_launch_count", "falkon_knm_matvec", "falkon_kernel_vec",
            "falkon_kernel_tvec", "falkon_precond_work_elems", "falkon_precond_build", "falkon_precond_solve", "falkon_fit",
-           "falkon_predict", "falkon_gsc_fit", "falkon_strerror", "falkon_last_error",
+           "falkon_predict", "falkon_gsc_fit", "falkon_knm_matmat", "falkon_predict_multi",
+           "falkon_fit_multi", "falkon_strerror", "falkon_last_error",
            "falkon_version"]
 
 LOSS_LOGISTIC, LOSS_SQUARED = 0, 1
@@ -88,6 +89,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "falkon_fit": (C, [P, P, P, I64, I64, P, I64, C, D, D, I32, D, P, P]),
         "falkon_predict": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
         "falkon_gsc_fit": (C, [P, P, P, I64, I64, P, P, I64, C, D, C, I32, P, P, D, P, P]),
+        "falkon_knm_matmat": (C, [P, P, I64, I64, P, I64, C, D, P, I64, P]),
+        "falkon_predict_multi": (C, [P, P, I64, I64, P, I64, C, D, P, I64, P]),
+        "falkon_fit_multi": (C, [P, P, P, I64, I64, P, I64, I64, C, D, D, I32, D, P, P]),
         "falkon_strerror": (ctypes.c_char_p, [C]),
         "falkon_last_error": (ctypes.c_char_p, []),
         "falkon_version": (ctypes.c_char_p, []),
@@ -298,6 +302,51 @@ class Context:
         code = _LIB.falkon_gsc_fit(self.h, px, py, n, d, pc, pyc, m, _kernel_id(kernel),
                                    float(sigma), lid, k, mu_arr, it_arr, float(jitter), pa,
                                    ctypes.byref(info))
+        if code != 0:
+            e = FalkonError(code, (_LIB.falkon_last_error() or b"").decode())
+            e.info = info.as_dict()
+            raise e
+        return alpha, info.as_dict()
+
+    @staticmethod
+    def _mat(a, dtype, name, rows):
+        p, numel = _ptr(a, dtype, name)
+        k = numel // max(rows, 1) if rows else 0
+        if rows and k * rows != numel:
+            raise ValueError(f"{name}: size {numel} is not a multiple of {rows} rows")
+        return p, k
+
+    def knm_matmat(self, X, C, V, kernel, sigma, out):
+        """U = sum_ranks Knm^T (Knm V); V, out: m x k fp64 row-major."""
+        px, n, d, pc, m = self._xc(X, C)
+        pv, k = self._mat(V, "float64", "V", m)
+        pu, ku = self._mat(out, "float64", "out", m)
+        if k != ku or k < 1:
+            raise ValueError("V and out must both be m x k")
+        _check(_LIB.falkon_knm_matmat(self.h, px, n, d, pc, m, _kernel_id(kernel), float(sigma),
+                                      pv, k, pu))
+        return out
+
+    def predict_multi(self, X, C, alpha, kernel, sigma, out):
+        """F = k(X, C) alpha; alpha m x k, out n x k (fp64 row-major)."""
+        px, n, d, pc, m = self._xc(X, C)
+        pa, k = self._mat(alpha, "float64", "alpha", m)
+        pf, _ = _ptr(out, "float64", "out")
+        _check(_LIB.falkon_predict_multi(self.h, px, n, d, pc, m, _kernel_id(kernel), float(sigma),
+                                         pa, k, pf))
+        return out
+
+    def fit_multi(self, X, Y, C, kernel, sigma, lam, iters, alpha, jitter: float = -1.0):
+        """Multi-output Falkon; Y: n x k fp32 row-major, alpha: m x k fp64 row-major."""
+        px, n, d, pc, m = self._xc(X, C)
+        py, k = self._mat(Y, "float32", "Y", n)
+        pa, ka = self._mat(alpha, "float64", "alpha", m)
+        if n and k != ka:
+            raise ValueError("Y and alpha column counts differ")
+        info = FitInfo()
+        code = _LIB.falkon_fit_multi(self.h, px, py, n, d, pc, m, ka, _kernel_id(kernel),
+                                     float(sigma), float(lam), int(iters), float(jitter), pa,
+                                     ctypes.byref(info))
         if code != 0:
             e = FalkonError(code, (_LIB.falkon_last_error() or b"").decode())
             e.info = info.as_dict()

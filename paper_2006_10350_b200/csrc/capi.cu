@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <vector>
 
 #include "common.cuh"
 
@@ -276,6 +277,82 @@ static int cg_run(falkon_ctx *ctx, Fit &F, const double *P, const double *dT, co
       ctx->launches++;
     }
     FK_LAUNCH_CHECK();
+  }
+  return FALKON_OK;
+}
+
+
+// ------------------------------------------------------------------ multi-output blocks (NEXT-3)
+// pack columns [c0, c0 + kcols) of a strided matrix (element (i, c) at src[i rs + c cs]) into a
+// zero-padded fp32 block [rows_pad][kvb]; unpack the fp64 block [rows][kvb] back.
+template <typename S>
+__global__ void pack_block_kernel(const S *__restrict__ src, int64_t rs, int64_t cs, int64_t rows,
+                                  int64_t c0, int kcols, int kvb, float *__restrict__ dst,
+                                  int64_t rows_pad) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows_pad * kvb) return;
+  const int64_t i = e / kvb;
+  const int j = (int)(e % kvb);
+  dst[e] = (i < rows && j < kcols) ? (float)src[i * rs + (c0 + j) * cs] : 0.f;
+}
+__global__ void unpack_block_kernel(const double *__restrict__ src, int64_t rows, int kvb,
+                                    int kcols, int64_t c0, double *__restrict__ dst, int64_t rs,
+                                    int64_t cs) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * kcols) return;
+  const int64_t i = e / kcols;
+  const int j = (int)(e % kcols);
+  dst[i * rs + (c0 + j) * cs] = src[i * kvb + j];
+}
+
+// column block width of a multi-vector pass: the tensor epilogue is compiled for 8 / 16 vectors
+// (padded with zero columns); the SIMT path loops over exactly the columns given
+static int block_kv(const Prepared &pp, int64_t left) {
+  if (left == 1) return 1;
+  if (pp.path == FALKON_PATH_TENSOR) return left > 8 ? 16 : 8;
+  return (int)std::min<int64_t>(left, 16);
+}
+
+template <typename S>
+static int pack_block(falkon_ctx *ctx, const S *src, int64_t rs, int64_t cs, int64_t rows,
+                      int64_t c0, int kcols, int kvb, float *dst, int64_t rows_pad) {
+  const int64_t tot = rows_pad * kvb;
+  if (tot <= 0) return FALKON_OK;
+  LaunchScope ls(ctx, FALKON_T_PREP);
+  pack_block_kernel<S><<<(unsigned)cdiv<int64_t>(tot, 256), 256, 0, ctx->stream>>>(
+      src, rs, cs, rows, c0, kcols, kvb, dst, rows_pad);
+  FK_LAUNCH_CHECK();
+  return FALKON_OK;
+}
+static int unpack_block(falkon_ctx *ctx, const double *src, int64_t rows, int kvb, int kcols,
+                        int64_t c0, double *dst, int64_t rs, int64_t cs) {
+  const int64_t tot = rows * kcols;
+  if (tot <= 0) return FALKON_OK;
+  LaunchScope ls(ctx, FALKON_T_PREP);
+  unpack_block_kernel<<<(unsigned)cdiv<int64_t>(tot, 256), 256, 0, ctx->stream>>>(
+      src, rows, kvb, kcols, c0, dst, rs, cs);
+  FK_LAUNCH_CHECK();
+  return FALKON_OK;
+}
+
+// U = Knm^T (Knm V) for k vectors on this rank (no collective): V element (j, c) at
+// V[j vrs + c vcs], U element (j, c) written at U[j urs + c ucs].
+static int product_multi(falkon_ctx *ctx, Fit &F, const double *V, int64_t vrs, int64_t vcs,
+                         int64_t k, double *U, int64_t urs, int64_t ucs) {
+  const int64_t m = F.pp.m, n = F.pp.n;
+  const int64_t m_pad = round_up<int64_t>(m, 256), n_pad = round_up<int64_t>(std::max<int64_t>(n, 1), 256);
+  void *v32, *w32, *u64;
+  FK_TRY(ws_get(ctx, WS_MV32, sizeof(float) * m_pad * 16, &v32));
+  FK_TRY(ws_get(ctx, WS_MW32, sizeof(float) * n_pad * 16, &w32));
+  FK_TRY(ws_get(ctx, WS_MU64, sizeof(double) * m * 16, &u64));
+  for (int64_t c0 = 0; c0 < k; ) {
+    const int kvb = block_kv(F.pp, k - c0);
+    const int kc = (int)std::min<int64_t>(kvb, k - c0);
+    FK_TRY(pack_block<double>(ctx, V, vrs, vcs, m, c0, kc, kvb, (float *)v32, m_pad));
+    FK_TRY(pass_A_multi(ctx, F.pp, (const float *)v32, kvb, nullptr, (float *)w32));
+    FK_TRY(pass_B_multi(ctx, F.pp, (const float *)w32, kvb, (double *)u64));
+    FK_TRY(unpack_block(ctx, (const double *)u64, m, kvb, kc, c0, U, urs, ucs));
+    c0 += kc;
   }
   return FALKON_OK;
 }
@@ -883,6 +960,264 @@ int falkon_gsc_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_lo
   cleanup();
   loc.t_total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   if (info) *info = loc;
+  return rc;
+}
+
+
+// ------------------------------------------------------------------ multi-output (NEXT-3)
+int falkon_knm_matmat(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d, const float *C,
+                      int64_t m, int kernel, double sigma, const double *V, int64_t k, double *U) {
+  FK_TRY(check_common(ctx, n_local, d, m, kernel, sigma));
+  if ((!X && n_local > 0) || !C || !V || !U) return fail(FALKON_EINVAL, "NULL array");
+  if (k < 1) return fail(FALKON_EINVAL, "k < 1");
+  Fit F;
+  FK_TRY(matvec_common(ctx, X, n_local, d, C, m, kernel, sigma, F));
+  const void *Vd;
+  FK_TRY(stage_in(ctx, WS_STAGE_V, V, sizeof(double) * m * k, &Vd));
+  const bool host_out = !is_device_ptr(U);
+  double *Ud = U;
+  if (host_out) {
+    void *w;
+    FK_TRY(ws_get(ctx, WS_STAGE_OUT, sizeof(double) * m * k, &w));
+    Ud = (double *)w;
+  }
+  FK_TRY(product_multi(ctx, F, (const double *)Vd, k, 1, k, Ud, k, 1));
+  FK_TRY(nccl_allreduce_f64(ctx, Ud, m * k));
+  if (host_out) {
+    FK_CUDA(cudaMemcpyAsync(U, Ud, sizeof(double) * m * k, cudaMemcpyDeviceToHost, ctx->stream));
+    FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return FALKON_OK;
+}
+
+int falkon_predict_multi(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d,
+                         const float *C, int64_t m, int kernel, double sigma, const double *alpha,
+                         int64_t k, double *Fo) {
+  FK_TRY(check_common(ctx, n_local, d, m, kernel, sigma));
+  if ((!X && n_local > 0) || !C || !alpha || (!Fo && n_local > 0)) return fail(FALKON_EINVAL, "NULL array");
+  if (k < 1) return fail(FALKON_EINVAL, "k < 1");
+  if (n_local == 0) return FALKON_OK;
+  Fit F;
+  FK_TRY(matvec_common(ctx, X, n_local, d, C, m, kernel, sigma, F));
+  const void *Ad;
+  FK_TRY(stage_in(ctx, WS_STAGE_V, alpha, sizeof(double) * m * k, &Ad));
+  const bool host_out = !is_device_ptr(Fo);
+  double *Fd = Fo;
+  if (host_out) {
+    void *w;
+    FK_TRY(ws_get(ctx, WS_STAGE_OUT, sizeof(double) * n_local * k, &w));
+    Fd = (double *)w;
+  }
+  const int64_t m_pad = round_up<int64_t>(m, 256);
+  void *v32, *f64b;
+  FK_TRY(ws_get(ctx, WS_MV32, sizeof(float) * m_pad * 16, &v32));
+  FK_TRY(ws_get(ctx, WS_Z64, sizeof(double) * n_local * 16, &f64b));
+  for (int64_t c0 = 0; c0 < k;) {
+    const int kvb = block_kv(F.pp, k - c0);
+    const int kc = (int)std::min<int64_t>(kvb, k - c0);
+    FK_TRY(pack_block<double>(ctx, (const double *)Ad, k, 1, m, c0, kc, kvb, (float *)v32, m_pad));
+    FK_TRY(pass_A_multi(ctx, F.pp, (const float *)v32, kvb, (double *)f64b, nullptr));
+    FK_TRY(unpack_block(ctx, (const double *)f64b, n_local, kvb, kc, c0, Fd, k, 1));
+    c0 += kc;
+  }
+  if (host_out) {
+    FK_CUDA(cudaMemcpyAsync(Fo, Fd, sizeof(double) * n_local * k, cudaMemcpyDeviceToHost, ctx->stream));
+    FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return FALKON_OK;
+}
+
+// Multi-output Falkon: Alg. 1 for k right-hand sides at once (the k CGs are independent; they
+// share the preconditioner and every kernel product).  CG state is column-major [k][m].
+int falkon_fit_multi(falkon_ctx *ctx, const float *X, const float *Y, int64_t n_local, int64_t d,
+                     const float *C, int64_t m, int64_t k, int kernel, double sigma, double lambda,
+                     int32_t iters, double jitter, double *alpha, falkon_fit_info *info) {
+  FK_TRY(check_common(ctx, n_local, d, m, kernel, sigma));
+  if ((!X && n_local > 0) || (!Y && n_local > 0) || !C || !alpha) return fail(FALKON_EINVAL, "NULL array");
+  if (k < 1) return fail(FALKON_EINVAL, "k < 1");
+  if (!(lambda >= 0.0) || !std::isfinite(lambda)) return fail(FALKON_EINVAL, "lambda must be >= 0");
+  if (iters < 0) return fail(FALKON_EINVAL, "iters < 0");
+  if (jitter < 0) jitter = 1e-8;
+  falkon_fit_info loc;
+  memset(&loc, 0, sizeof(loc));
+  loc.failed_factor = -1;
+  loc.failed_column = -1;
+  loc.failed_iter = -1;
+  loc.jitter_used = jitter;
+  auto t_start = std::chrono::steady_clock::now();
+  int64_t n_global = n_local;
+  if (ctx->nccl_comm) {
+    void *p;
+    FK_TRY(ws_get(ctx, WS_SCALARS, 64, &p));
+    FK_CUDA(cudaMemcpyAsync(p, &n_global, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    FK_TRY(nccl_allreduce_i64(ctx, (int64_t *)p, 1));
+    FK_CUDA(cudaMemcpyAsync(&n_global, p, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  const bool host_out = !is_device_ptr(alpha);
+  void *st, *scal;
+  FK_TRY(ws_get(ctx, WS_MULTI, sizeof(double) * m * k * 7, &st));
+  const size_t nsl = S_NSLOTS + DOT_BLOCKS + 8;
+  FK_TRY(ws_get(ctx, WS_CG2, sizeof(double) * nsl * k, &scal));
+  double *x = (double *)st, *r = x + m * k, *p = r + m * k, *t1 = p + m * k, *t2 = t1 + m * k,
+         *u = t2 + m * k, *ares = u + m * k;
+  double *P = nullptr, *dT = nullptr;
+  if (iters > 0) {
+    cudaError_t e = cudaMalloc(&P, sizeof(double) * (size_t)m * (size_t)m);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FALKON_ENOMEM, "preconditioner buffer of " + std::to_string(8.0 * m * m / 1e9) + " GB");
+    }
+    e = cudaMalloc(&dT, sizeof(double) * (2 * (size_t)m + (size_t)precond_work_elems(m)));
+    if (e != cudaSuccess) {
+      cudaFree(P);
+      cudaGetLastError();
+      return fail(FALKON_ENOMEM, "diag vectors");
+    }
+  }
+  double *dA = dT ? dT + m : nullptr, *pw = dT ? dT + 2 * m : nullptr;
+  cudaEvent_t ev[4];
+  for (auto &e : ev) cudaEventCreate(&e);
+  int rc = FALKON_OK;
+  Fit F;
+  do {
+    if (iters == 0) {
+      BRK_CUDA(cudaMemsetAsync(ares, 0, sizeof(double) * m * k, ctx->stream));
+      break;
+    }
+    const void *Xd, *Yd, *Cd;
+    if ((rc = stage_in(ctx, WS_STAGE_X, X, sizeof(float) * n_local * d, &Xd))) break;
+    if ((rc = stage_in(ctx, WS_STAGE_Y, Y, sizeof(float) * n_local * k, &Yd))) break;
+    if ((rc = stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd))) break;
+    BRK_CUDA(cudaEventRecord(ev[0], ctx->stream));
+    if ((rc = precond_build(ctx, (const float *)Cd, m, d, kernel, sigma, lambda, jitter, P, dT, dA,
+                            pw, &loc)))
+      break;
+    BRK_CUDA(cudaEventRecord(ev[1], ctx->stream));
+    if ((rc = prepare_operands(ctx, (const float *)Xd, n_local, d, (const float *)Cd, m, kernel,
+                               sigma, &F.pp)))
+      break;
+    // RHS  R = A^-T T^-T Knm^T Y  (Alg. 1 line 9, k columns)
+    {
+      const int64_t n_pad = round_up<int64_t>(std::max<int64_t>(n_local, 1), 256);
+      void *w32, *u64;
+      if ((rc = ws_get(ctx, WS_MW32, sizeof(float) * n_pad * 16, &w32))) break;
+      if ((rc = ws_get(ctx, WS_MU64, sizeof(double) * m * 16, &u64))) break;
+      for (int64_t c0 = 0; c0 < k && rc == FALKON_OK;) {
+        const int kvb = block_kv(F.pp, k - c0);
+        const int kc = (int)std::min<int64_t>(kvb, k - c0);
+        if ((rc = pack_block<float>(ctx, (const float *)Yd, k, 1, n_local, c0, kc, kvb,
+                                    (float *)w32, n_pad)))
+          break;
+        if ((rc = pass_B_multi(ctx, F.pp, (const float *)w32, kvb, (double *)u64))) break;
+        rc = unpack_block(ctx, (const double *)u64, m, kvb, kc, c0, r, 1, m);
+        c0 += kc;
+      }
+      if (rc) break;
+    }
+    if ((rc = nccl_allreduce_f64(ctx, r, m * k))) break;
+    for (int64_t c = 0; c < k && rc == FALKON_OK; ++c) {
+      if ((rc = trsv(ctx, P, dT, pw, m, 0, 1, r + c * m))) break;
+      rc = trsv(ctx, P, dA, pw, m, 1, 1, r + c * m);
+    }
+    if (rc) break;
+    BRK_CUDA(cudaEventRecord(ev[2], ctx->stream));
+    // k independent CGs (reading c9 per column) sharing each block product
+    BRK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * m * k, ctx->stream));
+    BRK_CUDA(cudaMemcpyAsync(p, r, sizeof(double) * m * k, cudaMemcpyDeviceToDevice, ctx->stream));
+    double *scb = (double *)scal;
+    for (int64_t c = 0; c < k && rc == FALKON_OK; ++c) {
+      double *sc = scb + c * nsl;
+      if ((rc = dot(ctx, r + c * m, r + c * m, m, sc + S_NSLOTS + 4, sc + S_RHO))) break;
+      LaunchScope ls(ctx, FALKON_T_VEC);
+      cg_init_kernel<<<1, 1, 0, ctx->stream>>>(sc);
+    }
+    const double lam_n = lambda * (double)n_global;
+    for (int it = 1; it <= iters && rc == FALKON_OK; ++it) {
+      BRK_CUDA(cudaMemcpyAsync(t1, p, sizeof(double) * m * k, cudaMemcpyDeviceToDevice, ctx->stream));
+      for (int64_t c = 0; c < k && rc == FALKON_OK; ++c)
+        rc = trsv(ctx, P, dA, pw, m, 1, 0, t1 + c * m);  // t1 = A^-1 p
+      if (rc) break;
+      BRK_CUDA(cudaMemcpyAsync(t2, t1, sizeof(double) * m * k, cudaMemcpyDeviceToDevice, ctx->stream));
+      for (int64_t c = 0; c < k && rc == FALKON_OK; ++c)
+        rc = trsv(ctx, P, dT, pw, m, 0, 0, t2 + c * m);  // t2 = T^-1 t1
+      if (rc) break;
+      if ((rc = product_multi(ctx, F, t2, 1, m, k, u, 1, m))) break;  // u = Knm^T Knm t2
+      if ((rc = nccl_allreduce_f64(ctx, u, m * k))) break;
+      for (int64_t c = 0; c < k && rc == FALKON_OK; ++c) {
+        double *uc = u + c * m, *sc = scb + c * nsl;
+        if ((rc = trsv(ctx, P, dT, pw, m, 0, 1, uc))) break;
+        {
+          LaunchScope ls(ctx, FALKON_T_VEC);
+          axpy_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(uc, t1 + c * m, lam_n, m);
+        }
+        if ((rc = trsv(ctx, P, dA, pw, m, 1, 1, uc))) break;
+        if ((rc = dot(ctx, p + c * m, uc, m, sc + S_NSLOTS + 4, sc + S_GAMMA))) break;
+        {
+          LaunchScope ls(ctx, FALKON_T_VEC);
+          cg_xr_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(x + c * m, r + c * m, p + c * m, uc, m, sc, it);
+        }
+        if ((rc = dot(ctx, r + c * m, r + c * m, m, sc + S_NSLOTS + 4, sc + S_RHO_NEW))) break;
+        LaunchScope ls(ctx, FALKON_T_VEC);
+        cg_flags_kernel<<<1, 1, 0, ctx->stream>>>(sc, it);
+        cg_p_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(p + c * m, r + c * m, m, sc);
+        ctx->launches++;
+      }
+      BRK_CUDA(cudaGetLastError());
+    }
+    if (rc) break;
+    BRK_CUDA(cudaEventRecord(ev[3], ctx->stream));
+    // alpha_c = T^-1 A^-1 x_c  (Alg. 1 line 11)
+    BRK_CUDA(cudaMemcpyAsync(ares, x, sizeof(double) * m * k, cudaMemcpyDeviceToDevice, ctx->stream));
+    for (int64_t c = 0; c < k && rc == FALKON_OK; ++c) {
+      if ((rc = trsv(ctx, P, dA, pw, m, 1, 0, ares + c * m))) break;
+      rc = trsv(ctx, P, dT, pw, m, 0, 0, ares + c * m);
+    }
+  } while (0);
+  if (rc == FALKON_OK) {
+    // column-major [k][m] -> caller's row-major m x k
+    double *outd = alpha;
+    void *stg = nullptr;
+    if (host_out) {
+      rc = ws_get(ctx, WS_STAGE_OUT, sizeof(double) * m * k, &stg);
+      outd = (double *)stg;
+    }
+    if (rc == FALKON_OK) {
+      LaunchScope ls(ctx, FALKON_T_VEC);
+      unpack_block_kernel<<<(unsigned)cdiv<int64_t>(m * k, 256), 256, 0, ctx->stream>>>(
+          ares, k, (int)m, (int)m, 0, outd, 1, k);  // src [k][m] as rows=k, cols=m
+    }
+    if (rc == FALKON_OK && host_out)
+      cudaMemcpyAsync(alpha, outd, sizeof(double) * m * k, cudaMemcpyDeviceToHost, ctx->stream);
+  }
+  double hsum = 0;
+  int32_t fail_it = -1;
+  if (rc == FALKON_OK && iters > 0) {
+    std::vector<double> hs(nsl * k);
+    cudaMemcpyAsync(hs.data(), scal, sizeof(double) * nsl * k, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    for (int64_t c = 0; c < k; ++c) {
+      hsum += hs[c * nsl + S_ITERS];
+      if (hs[c * nsl + S_FAIL] >= 0 && fail_it < 0) fail_it = (int32_t)hs[c * nsl + S_FAIL];
+    }
+    float a = 0, b = 0, cc = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&cc, ev[2], ev[3]);
+    loc.t_precond_s = a * 1e-3;
+    loc.t_rhs_s = b * 1e-3;
+    loc.t_cg_s = cc * 1e-3;
+    loc.iters_run = (int32_t)(hsum / (double)k);  // mean over columns
+    loc.failed_iter = fail_it;
+  }
+  cudaStreamSynchronize(ctx->stream);
+  if (P) cudaFree(P);
+  if (dT) cudaFree(dT);
+  for (auto &e : ev) cudaEventDestroy(e);
+  loc.t_total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  if (info) *info = loc;
+  if (rc == FALKON_OK && fail_it >= 0)
+    return fail(FALKON_ENONFINITE, "CG breakdown at iteration " + std::to_string(fail_it));
   return rc;
 }
 

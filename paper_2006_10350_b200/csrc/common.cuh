@@ -59,6 +59,12 @@ enum WsSlot {
   WS_Z64,         // fp64 n: predictions z = Knm alpha on the rows (GSC)
   WS_GSC,         // fp64 m vectors of the GSC outer loop
   WS_TRSV,        // fp64 m: sentinel-initialised output of the triangular solve
+  WS_MCOL,        // fp32 column scratch of the SIMT multi-vector passes
+  WS_MCOL64,      // fp64 + fp32 column outputs of the SIMT multi-vector passes
+  WS_MV32,        // fp32 [m_pad][kv] packed vector block (multi-output)
+  WS_MW32,        // fp32 [n_pad][kv] pass-A output block (multi-output)
+  WS_MU64,        // fp64 [m][kv] pass-B output block (multi-output)
+  WS_MULTI,       // fp64 multi-output fit state
   WS_COUNT
 };
 
@@ -148,14 +154,20 @@ int pass_A(falkon_ctx *ctx, const Prepared &pp, const float *z, double *w64, flo
 // u = Knm^T w (pass B) on this rank (no collective).  w: fp32 n (padded).  u: fp64 m.
 int pass_B(falkon_ctx *ctx, const Prepared &pp, const float *w, double *u);
 int f64_to_f32(falkon_ctx *ctx, const double *src, float *dst, int64_t n, int64_t n_pad);
+// multi-vector passes: z [q][kv] fp32 (q = m for pass A, n_pad rows for pass B), outputs
+// [p][kv] (fp64 and/or fp32); kv = 1, 8 or 16
+int pass_A_multi(falkon_ctx *ctx, const Prepared &pp, const float *z, int kv, double *w64,
+                 float *w32);
+int pass_B_multi(falkon_ctx *ctx, const Prepared &pp, const float *w, int kv, double *u);
 int f32_to_f32_pad(falkon_ctx *ctx, const float *src, float *dst, int64_t n, int64_t n_pad);
 
 // tensor path (kvp_tc.cu)
 bool tc_supported(const falkon_ctx *ctx, int kernel, int64_t d);
 int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const float *C, int64_t m,
                double sigma, const double *mu, Prepared *pp);
+// kv > 1 (8 or 16): z is [q][kv] fp32 and the outputs [p][kv] (multi-vector product)
 int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, double *out64,
-            float *out32);
+            float *out32, int kv = 1);
 
 // ------------------------------------------------------------------ preconditioner (precond.cu)
 int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel, double sigma,

@@ -751,4 +751,76 @@ int pass_B(falkon_ctx *ctx, const Prepared &pp, const float *w, double *u) {
                     (const float *)pp.Xp, pp.xa, w, pp.n, FALKON_T_PASS_B, u, nullptr);
 }
 
+// ------------------------------------------------------------------ multi-vector passes
+// Z in R^{q x kv} (k outputs, e.g. TIMIT's classes).  Tensor path: one fused
+// pass with a kv-wide epilogue (tc_pass, kv = 8 or 16).  SIMT path (Laplacian, d <= 8): the
+// single-vector kernel per column (the exp is recomputed per column).
+__global__ void col_gather_f32_kernel(const float *__restrict__ src, int64_t rows, int kv, int c,
+                                      float *__restrict__ dst, int64_t rows_pad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows) dst[i] = src[i * kv + c];
+  else if (i < rows_pad) dst[i] = 0.f;
+}
+template <typename T>
+__global__ void col_scatter_kernel(const T *__restrict__ src, int64_t rows, int kv, int c,
+                                   T *__restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows) dst[i * kv + c] = src[i];
+}
+
+static int simt_multi(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, int kv,
+                      double *o64, float *o32) {
+  const int64_t np = passA ? pp.n : pp.m, nq = passA ? pp.m : pp.n;
+  const int64_t nq_pad = round_up<int64_t>(std::max<int64_t>(nq, 1), 128);
+  const int64_t np_pad = round_up<int64_t>(std::max<int64_t>(np, 1), 128);
+  void *zc, *oc;
+  FK_TRY(ws_get(ctx, WS_MCOL, sizeof(float) * nq_pad, &zc));
+  FK_TRY(ws_get(ctx, WS_MCOL64, sizeof(double) * np_pad + sizeof(float) * np_pad, &oc));
+  double *c64 = (double *)oc;
+  float *c32 = (float *)(c64 + np_pad);
+  for (int c = 0; c < kv; ++c) {
+    {
+      LaunchScope ls(ctx, FALKON_T_PREP);
+      col_gather_f32_kernel<<<(unsigned)cdiv<int64_t>(nq_pad, 256), 256, 0, ctx->stream>>>(
+          z, nq, kv, c, (float *)zc, nq_pad);
+    }
+    FK_LAUNCH_CHECK();
+    if (passA)
+      FK_TRY(kvp_launch(ctx, pp.kernel, pp.d, pp.dq, (const float *)pp.Xp, pp.xa, pp.n,
+                        (const float *)pp.Cp, pp.cb, (const float *)zc, pp.m, FALKON_T_PASS_A,
+                        o64 ? c64 : nullptr, o32 ? c32 : nullptr));
+    else
+      FK_TRY(kvp_launch(ctx, pp.kernel, pp.d, pp.dq, (const float *)pp.Cp, pp.cb, pp.m,
+                        (const float *)pp.Xp, pp.xa, (const float *)zc, pp.n, FALKON_T_PASS_B,
+                        c64, nullptr));
+    LaunchScope ls(ctx, FALKON_T_PREP);
+    if (o64)
+      col_scatter_kernel<double><<<(unsigned)cdiv<int64_t>(np, 256), 256, 0, ctx->stream>>>(
+          c64, np, kv, c, o64);
+    if (o32)
+      col_scatter_kernel<float><<<(unsigned)cdiv<int64_t>(np, 256), 256, 0, ctx->stream>>>(
+          c32, np, kv, c, o32);
+    FK_LAUNCH_CHECK();
+  }
+  return FALKON_OK;
+}
+
+int pass_A_multi(falkon_ctx *ctx, const Prepared &pp, const float *z, int kv, double *w64,
+                 float *w32) {
+  if (pp.n <= 0) return FALKON_OK;
+  if (kv == 1) return pass_A(ctx, pp, z, w64, w32);
+  if (pp.path == FALKON_PATH_TENSOR) return tc_pass(ctx, pp, true, z, w64, w32, kv);
+  return simt_multi(ctx, pp, true, z, kv, w64, w32);
+}
+
+int pass_B_multi(falkon_ctx *ctx, const Prepared &pp, const float *w, int kv, double *u) {
+  if (pp.n <= 0) {
+    FK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * pp.m * kv, ctx->stream));
+    return FALKON_OK;
+  }
+  if (kv == 1) return pass_B(ctx, pp, w, u);
+  if (pp.path == FALKON_PATH_TENSOR) return tc_pass(ctx, pp, false, w, u, nullptr, kv);
+  return simt_multi(ctx, pp, false, w, kv, u, nullptr);
+}
+
 }  // namespace falkon

@@ -250,6 +250,28 @@ __device__ __forceinline__ void tc_epi_chunk(const uint32_t (&r)[32], const floa
   }
 }
 
+// Multi-vector epilogue (Kv for V in R^{q x KV}): 32 accumulator columns,
+// k = exp2(min(t, 0)) once per entry, then acc[c] += k * z[j][c] for the KV vectors (z is
+// [q][KV] fp32).  MASK: columns j >= lim are skipped (their z rows may be past the buffer).
+template <bool MASK, int KV>
+__device__ __forceinline__ void tc_epi_chunk_kv(const uint32_t (&r)[32], const float *__restrict__ z,
+                                                int lim, float (&acc)[KV]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    if (MASK && j >= lim) break;
+    const float k = ex2_approx(fminf(__uint_as_float(r[j]), 0.f));
+    const float4 *zp = reinterpret_cast<const float4 *>(z + j * KV);
+#pragma unroll
+    for (int g = 0; g < KV / 4; ++g) {
+      const float4 zz = __ldg(zp + g);
+      acc[4 * g + 0] = fmaf(k, zz.x, acc[4 * g + 0]);
+      acc[4 * g + 1] = fmaf(k, zz.y, acc[4 * g + 1]);
+      acc[4 * g + 2] = fmaf(k, zz.z, acc[4 * g + 2]);
+      acc[4 * g + 3] = fmaf(k, zz.w, acc[4 * g + 3]);
+    }
+  }
+}
+
 __device__ __forceinline__ void tc_mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
                                               uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -267,7 +289,7 @@ __device__ __forceinline__ void tc_cp_128x256b(uint32_t tmem_dst, uint64_t sdesc
 // STREAM: large d (2*d16 > 384): the P tile cannot stay resident, so each pipeline stage
 // carries the matching 64-wide K box of BOTH segments of P and Q ([h|l] layout with
 // 64-aligned segments): 16 + 16 + 32 + 32 KB, three MMAs per 16-wide chunk.
-template <int MODE, int NT, bool TS, bool STREAM = false, int EPIW = TC_EPI_WARPS>
+template <int MODE, int NT, bool TS, bool STREAM = false, int EPIW = TC_EPI_WARPS, int KV = 1>
 __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     tc_kvp_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                   TcArgs a) {
@@ -429,7 +451,67 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       if (elect_one()) tc_commit(&tfull[acc]);
       __syncwarp();
     }
-  } else if (warp >= 4) {
+  } else if (KV > 1 && warp >= 4) {
+    // multi-vector epilogue: thread = P row, KV fp32 chains per tile -> KV fp64 sums
+    const int ew = warp - 4;
+    const int lg = ew & 3;
+    const int half = ew >> 2;
+    const int row = lg * 32 + lane;
+    const int64_t p = p0 + row;
+    const int col0 = half * HALF;
+    double acc64[KV];
+#pragma unroll
+    for (int c = 0; c < KV; ++c) acc64[c] = 0.0;
+    uint32_t rr[2][32];
+    for (int t = 0; t < ntiles; ++t) {
+      const int accb = t & 1;
+      mbar_wait(&tfull[accb], (t >> 1) & 1);
+      tc_fence_after();
+      const int64_t q0 = qlo + (int64_t)t * NT;
+      const int cnt = (int)lmin(NT, qhi - q0) - col0;
+      const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(accb * NT + col0);
+      const float *zt = a.z + (q0 + col0) * KV;
+      float acc[KV];
+#pragma unroll
+      for (int c = 0; c < KV; ++c) acc[c] = 0.f;
+      if (cnt >= HALF) {
+        tmem_ld32(tb, rr[0]);
+        tmem_wait_ld_regs(rr[0]);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          if (c + 1 < NCH) tmem_ld32(tb + (uint32_t)((c + 1) * 32), rr[(c + 1) & 1]);
+          tc_epi_chunk_kv<false, KV>(rr[c & 1], zt + c * 32 * KV, 32, acc);
+          if (c + 1 < NCH) tmem_wait_ld_regs(rr[(c + 1) & 1]);
+        }
+      } else {
+        for (int c = 0; c * 32 < cnt; ++c) {
+          tmem_ld32(tb + (uint32_t)(c * 32), rr[0]);
+          tmem_wait_ld_regs(rr[0]);
+          tc_epi_chunk_kv<true, KV>(rr[0], zt + c * 32 * KV, cnt - c * 32, acc);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[accb]);
+#pragma unroll
+      for (int c = 0; c < KV; ++c) acc64[c] += (double)acc[c];
+    }
+    // combine the column groups of each row in a fixed order (deterministic)
+    if (half > 0) {
+#pragma unroll
+      for (int c = 0; c < KV; ++c) red[((half - 1) * TC_M + row) * KV + c] = acc64[c];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * EPIW) : "memory");
+    if (half == 0 && p < a.np) {
+#pragma unroll
+      for (int c = 0; c < KV; ++c) {
+        double tot = acc64[c];
+        for (int g2 = 1; g2 < GRP; ++g2) tot += red[((g2 - 1) * TC_M + row) * KV + c];
+        if (a.out64) a.out64[((int64_t)blockIdx.y * a.np + p) * KV + c] = tot;
+        if (a.out32) a.out32[p * KV + c] = (float)tot;
+      }
+    }
+  } else if (KV == 1 && warp >= 4) {
     const int ew = warp - 4;
     const int lg = ew & 3;        // TMEM lane group: warp % 4 == lg
     const int half = ew >> 2;     // column group of the accumulator
@@ -566,18 +648,19 @@ int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const floa
   return FALKON_OK;
 }
 
-static size_t tc_smem_bytes(int nbox, int stages, int nt) {
-  return 1024 + (size_t)nbox * TC_A_BOX + (size_t)stages * nt * TC_BK * 2 + 256 + 3 * 8 * TC_M;
+static size_t tc_smem_bytes(int nbox, int stages, int nt, int kv = 1) {
+  return 1024 + (size_t)nbox * TC_A_BOX + (size_t)stages * nt * TC_BK * 2 + 256 +
+         (size_t)8 * TC_M * std::max(3, kv);
 }
-static int tc_stages(int nbox, int nt) {
+static int tc_stages(int nbox, int nt, int kv = 1) {
   int s = 8;
-  while (s > 2 && tc_smem_bytes(nbox, s, nt) > (size_t)TC_SMEM_MAX) --s;
+  while (s > 2 && tc_smem_bytes(nbox, s, nt, kv) > (size_t)TC_SMEM_MAX) --s;
   return s;
 }
 
 
 int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, double *out64,
-            float *out32) {
+            float *out32, int kv) {
   const CUtensorMap *maps = reinterpret_cast<const CUtensorMap *>(pp.tmaps);
   const int d16 = pp.dq;
   const bool stream = tc_stream(pp.d);
@@ -585,11 +668,12 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   const int nbox = stream ? d16 / TC_BK : (int)cdiv<int64_t>(2 * d16, TC_BK);
   const int64_t np = passA ? pp.n : pp.m, nq = passA ? pp.m : pp.n;
   if (np <= 0) return FALKON_OK;
-  const bool ts = !stream && tc_use_ts(d16);
+  const bool ts = kv == 1 && !stream && tc_use_ts(d16);
   const int nt = ts ? TC_N_TS : TC_N;
-  const int stages = stream ? 2 : tc_stages(nbox, nt);
-  const size_t smem = stream ? 1024 + (size_t)2 * 2 * (TC_A_BOX + TC_B_BOX) + 256 + 3 * 8 * TC_M
-                             : tc_smem_bytes(nbox, stages, nt);
+  const int stages = stream ? 2 : tc_stages(nbox, nt, kv);
+  const size_t smem = stream ? 1024 + (size_t)2 * 2 * (TC_A_BOX + TC_B_BOX) + 256 +
+                                   (size_t)8 * TC_M * std::max(3, kv)
+                             : tc_smem_bytes(nbox, stages, nt, kv);
   int mode = ctx->opt.exp_offload;
   if (const char *e = getenv("FALKON_TC_MODE")) mode = atoi(e);  // diagnostics (8-11)
   typedef void (*kfn)(const CUtensorMap, const CUtensorMap, TcArgs);
@@ -615,6 +699,12 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   }
 #undef FK_TC
   if (stream) fn = mode == 11 ? tc_kvp_kernel<11, TC_N, false, true> : tc_kvp_kernel<0, TC_N, false, true>;
+  if (kv > 1) {  // multi-vector epilogue (8 epilogue warps: KV fp32 + KV fp64 sums per thread)
+    epiw = 8;
+    if (kv == 8) fn = stream ? tc_kvp_kernel<0, TC_N, false, true, 8, 8> : tc_kvp_kernel<0, TC_N, false, false, 8, 8>;
+    else if (kv == 16) fn = stream ? tc_kvp_kernel<0, TC_N, false, true, 8, 16> : tc_kvp_kernel<0, TC_N, false, false, 8, 16>;
+    else return fail(FALKON_EINVAL, "tc_pass: kv must be 1, 8 or 16");
+  }
   const int threads = 128 + 32 * epiw;
   FK_CUDA(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                TC_SMEM_MAX));
@@ -639,7 +729,7 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   double *part = out64;
   if (splits > 1 || !out64) {
     void *pw;
-    FK_TRY(ws_get(ctx, WS_PART, sizeof(double) * splits * np, &pw));
+    FK_TRY(ws_get(ctx, WS_PART, sizeof(double) * splits * np * kv, &pw));
     part = (double *)pw;
   }
   TcArgs args;
@@ -658,7 +748,8 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
         passA ? maps[0] : maps[2], passA ? maps[1] : maps[3], args);
   }
   FK_LAUNCH_CHECK();
-  if (splits > 1 || (!out64 && !out32)) FK_TRY(reduce_partials(ctx, part, splits, np, out64, out32));
+  if (splits > 1 || (!out64 && !out32))
+    FK_TRY(reduce_partials(ctx, part, splits, np * kv, out64, out32));
   return FALKON_OK;
 }
 
