@@ -172,6 +172,12 @@ int falkon_precond_solve(falkon_ctx *ctx, const double *P, const double *diagT,
                          const double *diagA, const double *work, int64_t m, int which,
                          int trans, double *x);
 
+/* Multi-column form of falkon_precond_solve: column c of x starts at x + c * ldx (ldx >= m),
+   c < k.  One pass over the triangle per 16 columns (multi-output fits). */
+int falkon_precond_solve_multi(falkon_ctx *ctx, const double *P, const double *diagT,
+                               const double *diagA, const double *work, int64_t m, int which,
+                               int trans, double *x, int64_t ldx, int64_t k);
+
 /* ---- Falkon ---------------------------------------------------------------------------- */
 
 /* alpha = Falkon(X, y, C, kernel, sigma, lambda, iters)  (Alg. 1).

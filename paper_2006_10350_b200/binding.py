@@ -32,7 +32,7 @@ ERRORS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ENONFINITE", 4: "ENOMEM", 5: "E
 EXPORTS = ["falkon_get_unique_id", "falkon_ctx_create", "falkon_ctx_destroy",
            "falkon_ctx_set_stream", "falkon_ctx_set_option", "falkon_ctx_timings",
            "falkon_ctx_launch_count", "falkon_knm_matvec", "falkon_kernel_vec",
-           "falkon_kernel_tvec", "falkon_precond_work_elems", "falkon_precond_build", "falkon_precond_solve", "falkon_fit",
+           "falkon_kernel_tvec", "falkon_precond_work_elems", "falkon_precond_build", "falkon_precond_solve", "falkon_precond_solve_multi", "falkon_fit",
            "falkon_predict", "falkon_gsc_fit", "falkon_knm_matmat", "falkon_predict_multi",
            "falkon_fit_multi", "falkon_strerror", "falkon_last_error",
            "falkon_version"]
@@ -86,6 +86,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "falkon_precond_work_elems": (I64, [I64]),
         "falkon_precond_build": (C, [P, P, I64, I64, C, D, D, D, P, P, P, P, P]),
         "falkon_precond_solve": (C, [P, P, P, P, P, I64, C, C, P]),
+        "falkon_precond_solve_multi": (C, [P, P, P, P, P, I64, C, C, P, I64, I64]),
         "falkon_fit": (C, [P, P, P, I64, I64, P, I64, C, D, D, I32, D, P, P]),
         "falkon_predict": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
         "falkon_gsc_fit": (C, [P, P, P, I64, I64, P, P, I64, C, D, C, I32, P, P, D, P, P]),
@@ -269,6 +270,17 @@ class Context:
                                          _ptr(work, "float64", "work")[0], m, int(which),
                                          int(bool(trans)), _ptr(x, "float64", "x")[0]))
         return x
+
+    def precond_solve_multi(self, P, diagT, diagA, work, which: int, trans: bool, X):
+        """In-place solve of every row of X (k x m, each row one right-hand side)."""
+        k, m = X.shape
+        _check(_LIB.falkon_precond_solve_multi(self.h, _ptr(P, "float64", "P")[0],
+                                               _ptr(diagT, "float64", "diagT")[0],
+                                               _ptr(diagA, "float64", "diagA")[0],
+                                               _ptr(work, "float64", "work")[0], m, int(which),
+                                               int(bool(trans)), _ptr(X, "float64", "X")[0],
+                                               m, k))
+        return X
 
     def fit(self, X, y, C, kernel, sigma, lam, iters, alpha, jitter: float = -1.0):
         px, n, d, pc, m = self._xc(X, C)

@@ -639,6 +639,16 @@ int falkon_precond_solve(falkon_ctx *ctx, const double *P, const double *diagT, 
   return trsv(ctx, P, which == 0 ? diagT : diagA, work, m, which, trans, x);
 }
 
+int falkon_precond_solve_multi(falkon_ctx *ctx, const double *P, const double *diagT,
+                               const double *diagA, const double *work, int64_t m, int which,
+                               int trans, double *x, int64_t ldx, int64_t k) {
+  if (!ctx || !P || !diagT || !diagA || !work || !x || m < 1 || k < 1 || ldx < m ||
+      (which != 0 && which != 1))
+    return fail(FALKON_EINVAL, "bad arguments");
+  FK_CUDA(cudaSetDevice(ctx->device));
+  return trsv_multi(ctx, P, which == 0 ? diagT : diagA, work, m, which, trans, x, ldx, k);
+}
+
 // ------------------------------------------------------------------ Falkon fit
 int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local, int64_t d,
                const float *C, int64_t m, int kernel, double sigma, double lambda, int32_t iters,
@@ -1116,11 +1126,8 @@ int falkon_fit_multi(falkon_ctx *ctx, const float *X, const float *Y, int64_t n_
       if (rc) break;
     }
     if ((rc = nccl_allreduce_f64(ctx, r, m * k))) break;
-    for (int64_t c = 0; c < k && rc == FALKON_OK; ++c) {
-      if ((rc = trsv(ctx, P, dT, pw, m, 0, 1, r + c * m))) break;
-      rc = trsv(ctx, P, dA, pw, m, 1, 1, r + c * m);
-    }
-    if (rc) break;
+    if ((rc = trsv_multi(ctx, P, dT, pw, m, 0, 1, r, m, k))) break;
+    if ((rc = trsv_multi(ctx, P, dA, pw, m, 1, 1, r, m, k))) break;
     BRK_CUDA(cudaEventRecord(ev[2], ctx->stream));
     // k independent CGs (reading c9 per column) sharing each block product
     BRK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * m * k, ctx->stream));
@@ -1135,23 +1142,19 @@ int falkon_fit_multi(falkon_ctx *ctx, const float *X, const float *Y, int64_t n_
     const double lam_n = lambda * (double)n_global;
     for (int it = 1; it <= iters && rc == FALKON_OK; ++it) {
       BRK_CUDA(cudaMemcpyAsync(t1, p, sizeof(double) * m * k, cudaMemcpyDeviceToDevice, ctx->stream));
-      for (int64_t c = 0; c < k && rc == FALKON_OK; ++c)
-        rc = trsv(ctx, P, dA, pw, m, 1, 0, t1 + c * m);  // t1 = A^-1 p
-      if (rc) break;
+      if ((rc = trsv_multi(ctx, P, dA, pw, m, 1, 0, t1, m, k))) break;  // t1 = A^-1 p
       BRK_CUDA(cudaMemcpyAsync(t2, t1, sizeof(double) * m * k, cudaMemcpyDeviceToDevice, ctx->stream));
-      for (int64_t c = 0; c < k && rc == FALKON_OK; ++c)
-        rc = trsv(ctx, P, dT, pw, m, 0, 0, t2 + c * m);  // t2 = T^-1 t1
-      if (rc) break;
+      if ((rc = trsv_multi(ctx, P, dT, pw, m, 0, 0, t2, m, k))) break;  // t2 = T^-1 t1
       if ((rc = product_multi(ctx, F, t2, 1, m, k, u, 1, m))) break;  // u = Knm^T Knm t2
       if ((rc = nccl_allreduce_f64(ctx, u, m * k))) break;
+      if ((rc = trsv_multi(ctx, P, dT, pw, m, 0, 1, u, m, k))) break;  // u = T^-T u
+      {
+        LaunchScope ls(ctx, FALKON_T_VEC);
+        axpy_kernel<<<vgrid(m * k), VT, 0, ctx->stream>>>(u, t1, lam_n, m * k);
+      }
+      if ((rc = trsv_multi(ctx, P, dA, pw, m, 1, 1, u, m, k))) break;  // q = A^-T u
       for (int64_t c = 0; c < k && rc == FALKON_OK; ++c) {
         double *uc = u + c * m, *sc = scb + c * nsl;
-        if ((rc = trsv(ctx, P, dT, pw, m, 0, 1, uc))) break;
-        {
-          LaunchScope ls(ctx, FALKON_T_VEC);
-          axpy_kernel<<<vgrid(m), VT, 0, ctx->stream>>>(uc, t1 + c * m, lam_n, m);
-        }
-        if ((rc = trsv(ctx, P, dA, pw, m, 1, 1, uc))) break;
         if ((rc = dot(ctx, p + c * m, uc, m, sc + S_NSLOTS + 4, sc + S_GAMMA))) break;
         {
           LaunchScope ls(ctx, FALKON_T_VEC);
@@ -1169,10 +1172,8 @@ int falkon_fit_multi(falkon_ctx *ctx, const float *X, const float *Y, int64_t n_
     BRK_CUDA(cudaEventRecord(ev[3], ctx->stream));
     // alpha_c = T^-1 A^-1 x_c  (Alg. 1 line 11)
     BRK_CUDA(cudaMemcpyAsync(ares, x, sizeof(double) * m * k, cudaMemcpyDeviceToDevice, ctx->stream));
-    for (int64_t c = 0; c < k && rc == FALKON_OK; ++c) {
-      if ((rc = trsv(ctx, P, dA, pw, m, 1, 0, ares + c * m))) break;
-      rc = trsv(ctx, P, dT, pw, m, 0, 0, ares + c * m);
-    }
+    if ((rc = trsv_multi(ctx, P, dA, pw, m, 1, 0, ares, m, k))) break;
+    rc = trsv_multi(ctx, P, dT, pw, m, 0, 0, ares, m, k);
   } while (0);
   if (rc == FALKON_OK) {
     // column-major [k][m] -> caller's row-major m x k

@@ -185,6 +185,9 @@ int precond_build_A(falkon_ctx *ctx, int64_t m, double lambda, const double *dsc
 // z = T^T (T x) = (Kmm + delta I) x from the factored buffer; tmp: m doubles
 int trmv_TtT(falkon_ctx *ctx, const double *P, const double *diagT, int64_t m, const double *x,
              double *tmp, double *z);
+// multi-column solve: columns x + c ldx, c < kcols (one pass over the triangle per 16 columns)
+int trsv_multi(falkon_ctx *ctx, const double *P, const double *diag, const double *work, int64_t m,
+               int which, int trans, double *x, int64_t ldx, int64_t kcols);
 // x <- op(F)^-1 x, F = T (which 0) or A (which 1); work = the build's work buffer
 int trsv(falkon_ctx *ctx, const double *P, const double *diag, const double *work, int64_t m,
          int which, int trans, double *x);

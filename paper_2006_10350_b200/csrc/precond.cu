@@ -1006,6 +1006,173 @@ __global__ void __launch_bounds__(256) trsv_kernel(View L, int64_t m, int forwar
   }
 }
 
+// Multi-column variant (multi-output fits): solves KC right-hand sides
+// (columns at stride ldx) in one pass over the triangle.  Same schedule and sentinel protocol as
+// trsv_kernel; each tile is multiplied into KC accumulators per thread.
+constexpr int TRSV_KC = 16;
+constexpr int TRSV_ZRM = 4;  // z blocks per batch fetch (x KC columns)
+
+template <int KC>
+__global__ void __launch_bounds__(256) trsv_multi_kernel(View L, int64_t m, int forward,
+                                                         const double *__restrict__ rhs,
+                                                         int64_t ldx, int kc, double *zo,
+                                                         const double *__restrict__ Dinv,
+                                                         unsigned int *__restrict__ counter) {
+  extern __shared__ __align__(16) double tsm[];
+  double *sT0 = tsm, *sT1 = tsm + TB * TS_LD;
+  double *sD = tsm + 2 * TB * TS_LD;
+  double *zr = sD + TB * TS_LD;          // [TRSV_ZRM][KC][TB]
+  double *sx = zr + TRSV_ZRM * KC * TB;  // [KC][TB]
+  __shared__ unsigned int s_ticket;
+  __shared__ int s_ready;
+  const int tid = threadIdx.x;
+  const int64_t nblk = cdiv<int64_t>(m, TB);
+  if (tid == 0) s_ticket = atomicAdd(counter, 1u);
+  __syncthreads();
+  const int64_t b = s_ticket;
+  const int64_t I = forward ? b : nblk - 1 - b;
+  const int64_t i0 = I * TB;
+  const int nI = (int)lmin(TB, m - i0);
+  const bool rowmaj = (forward != 0) == (L.trans == 0);
+  const int64_t nJ = b;
+  auto j0of = [&](int64_t s) { return (forward ? s : nblk - 1 - s) * TB; };
+  auto issue = [&](int64_t s) {
+    const int64_t j0 = j0of(s);
+    const int nJc = (int)lmin(TB, m - j0);
+    tile_async((s & 1) ? sT1 : sT0, rowmaj ? L.base + i0 * L.ld + j0 : L.base + j0 * L.ld + i0,
+               L.ld, rowmaj ? nI : nJc, rowmaj ? nJc : nI);
+    cp_async_commit();
+  };
+  {
+    const double *dsrc = Dinv + I * (int64_t)(TB * TB);
+    for (int e = tid; e < TB * (TB / 2); e += blockDim.x) {
+      const int r = e / (TB / 2), c2 = (e % (TB / 2)) * 2;
+      cp_async16(sD + r * TS_LD + c2, dsrc + r * TB + c2);
+    }
+    cp_async_commit();
+  }
+  if (nJ > 0) issue(0);
+  const int ri = rowmaj ? (tid >> 2) : (tid & 63);
+  const int qq = rowmaj ? (tid & 3) : (tid >> 6);
+  double acc[KC];
+#pragma unroll
+  for (int c = 0; c < KC; ++c) acc[c] = 0.0;
+  int64_t zlo = 0, zhi = 0;
+  for (int64_t s = 0; s < nJ; ++s) {
+    if (s + 1 < nJ) issue(s + 1);
+    if (s >= zhi) {
+      const int64_t want = lmin(nJ, s + TRSV_ZRM);
+      if (tid == 0) s_ready = (int)(want - s);
+      __syncthreads();
+      for (int e = tid; e < (want - s) * KC * TB; e += blockDim.x) {
+        const int blk = e / (KC * TB), c = (e / TB) % KC, jj = e % TB;
+        const int64_t jg = j0of(s + blk) + jj;
+        double v = 0.0;
+        if (jg < m && c < kc) {
+          v = __ldcg(zo + c * m + jg);
+          if (is_sent(v)) atomicMin(&s_ready, blk);
+        }
+        zr[e] = v;
+      }
+      __syncthreads();
+      zlo = s;
+      zhi = s + s_ready;
+      if (zhi == s) {  // dependency front: spin on block s (all columns)
+        for (int e = tid; e < KC * TB; e += blockDim.x) {
+          const int c = e / TB, jj = e % TB;
+          const int64_t jg = j0of(s) + jj;
+          double v = 0.0;
+          if (jg < m && c < kc) {
+            const volatile double *pz = zo + c * m + jg;
+            do {
+              v = *pz;
+            } while (is_sent(v));
+          }
+          zr[e] = v;
+        }
+        zhi = s + 1;
+      }
+      __syncthreads();
+    }
+    if (s + 1 < nJ) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
+    const double *T = (s & 1) ? sT1 : sT0;
+    const double *zz = zr + (s - zlo) * KC * TB;
+    const int nJc = (int)lmin(TB, m - j0of(s));
+    if (ri < nI) {
+#pragma unroll 4
+      for (int k = 0; k < TB / 4; ++k) {
+        const int jj = rowmaj ? qq + 4 * k : qq * (TB / 4) + k;
+        if (jj < nJc) {
+          const double t = rowmaj ? T[ri * TS_LD + jj] : T[jj * TS_LD + ri];
+#pragma unroll
+          for (int c = 0; c < KC; ++c) acc[c] = fma(t, zz[c * TB + jj], acc[c]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // x = r_I - acc per column (4 partial sums per row, fixed order), then z_I = D x
+  double *part = sT0;  // [4][KC][TB] fits in two tile buffers for KC <= 16 ... use sT0..sD
+#pragma unroll
+  for (int c = 0; c < KC; ++c) part[(qq * KC + c) * TB + ri] = acc[c];
+  __syncthreads();
+  for (int e = tid; e < KC * TB; e += blockDim.x) {
+    const int c = e / TB, r = e % TB;
+    double v = 0.0;
+    if (r < nI && c < kc)
+      v = rhs[c * ldx + i0 + r] - (part[(0 * KC + c) * TB + r] + part[(1 * KC + c) * TB + r] +
+                                   part[(2 * KC + c) * TB + r] + part[(3 * KC + c) * TB + r]);
+    sx[e] = v;
+  }
+  __syncthreads();
+  for (int e = tid; e < KC * TB; e += blockDim.x) {
+    const int c = e / TB, r = e % TB;
+    if (r >= nI || c >= kc) continue;
+    double v = 0.0;
+    for (int k = 0; k < TB; ++k) v = fma(forward ? sD[r * TS_LD + k] : sD[k * TS_LD + r], sx[c * TB + k], v);
+    if (is_sent(v)) v = __longlong_as_double(0x7ff8000000000000LL);
+    __stcg(zo + c * m + i0 + r, v);
+  }
+}
+
+// x[:, c] <- op(F)^-1 x[:, c] for the kcols columns of x (column c at x + c ldx)
+int trsv_multi(falkon_ctx *ctx, const double *P, const double *diag, const double *work, int64_t m,
+               int which, int trans, double *x, int64_t ldx, int64_t kcols) {
+  if (kcols == 1) return trsv(ctx, P, diag, work, m, which, trans, x);
+  View L{const_cast<double *>(P), m, which == 0 ? 1 : 0, 1, const_cast<double *>(diag)};
+  const double *dinv = work + (which == 0 ? 0 : precond_work_elems(m) / 2);
+  const int forward = trans ? 1 : 0;
+  const int64_t nblk = cdiv<int64_t>(m, TB);
+  void *fl, *zb;
+  FK_TRY(ws_get(ctx, WS_FLAGS, 64 + sizeof(unsigned int) * (nblk + 64), &fl));
+  FK_TRY(ws_get(ctx, WS_TRSV, sizeof(double) * m * TRSV_KC, &zb));
+  unsigned int *counter = (unsigned int *)((char *)fl + 32);
+  const size_t smem =
+      sizeof(double) * (3 * TB * TS_LD + (size_t)(TRSV_ZRM + 1) * TRSV_KC * TB);
+  static_assert(4 * TRSV_KC * TB <= 3 * TB * TS_LD + TRSV_ZRM * TRSV_KC * TB,
+                "partials fit in the tile + ring buffers");
+  FK_CUDA(cudaFuncSetAttribute(trsv_multi_kernel<TRSV_KC>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int64_t c0 = 0; c0 < kcols; c0 += TRSV_KC) {
+    const int kc = (int)std::min<int64_t>(TRSV_KC, kcols - c0);
+    FK_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), ctx->stream));
+    FK_CUDA(cudaMemsetAsync(zb, 0xff, sizeof(double) * m * kc, ctx->stream));
+    {
+      LaunchScope ls(ctx, FALKON_T_TRSV);
+      trsv_multi_kernel<TRSV_KC><<<(unsigned)nblk, 256, smem, ctx->stream>>>(
+          L, m, forward, x + c0 * ldx, ldx, kc, (double *)zb, dinv, counter);
+    }
+    FK_LAUNCH_CHECK();
+    FK_CUDA(cudaMemcpy2DAsync(x + c0 * ldx, sizeof(double) * ldx, zb, sizeof(double) * m,
+                              sizeof(double) * m, kc, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  return FALKON_OK;
+}
+
 int64_t precond_work_elems(int64_t m) { return 2 * cdiv<int64_t>(m, TB) * (int64_t)(TB * TB); }
 
 int trsv(falkon_ctx *ctx, const double *P, const double *diag, const double *work, int64_t m,

@@ -151,3 +151,19 @@ def test_fit_many_iterations_equals_eq5(ctx):
     direct = np.linalg.solve(Knm.T @ Knm + lam * n * Kmm, Knm.T @ y.astype(np.float64))
     alpha, _ = _fit_gpu(ctx, X, y, C, G, sigma, lam, 3 * m, jitter=delta)
     assert rel_l2(alpha, direct) <= 1e-3
+
+
+@pytest.mark.parametrize("m,k", [(300, 5), (1000, 16), (2085, 21)])
+def test_triangular_solves_multi_column(ctx, m, k):
+    """Multi-column solve (multi-output fits): every column equals SciPy's solve."""
+    from paper_2006_10350_b200 import binding  # noqa: F401
+    C = synth.gen_X(m + 1, 0, m, 9)
+    T, A, (P, dT, dA, W), _ = _build(ctx, C, G, 1.0, 1e-6, 1e-8)
+    rng = np.random.default_rng(m + k)
+    for which, F in ((0, T), (1, A)):
+        for trans in (False, True):
+            B = rng.standard_normal((k, m))  # column-major [k][m]
+            Xd = dev(B.copy())
+            ctx.precond_solve_multi(P, dT, dA, W, which, trans, Xd)
+            ref = sla.solve_triangular(F, B.T, lower=False, trans="T" if trans else "N")
+            assert rel_l2(host(Xd).T, ref) <= 1e-10
