@@ -255,19 +255,18 @@ __device__ __forceinline__ void tc_epi_chunk(const uint32_t (&r)[32], const floa
 // [q][KV] fp32).  MASK: columns j >= lim are skipped (their z rows may be past the buffer).
 template <bool MASK, int KV>
 __device__ __forceinline__ void tc_epi_chunk_kv(const uint32_t (&r)[32], const float *__restrict__ z,
-                                                int lim, float (&acc)[KV]) {
+                                                int lim, float2 (&acc)[KV > 1 ? KV / 2 : 1]) {
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     if (MASK && j >= lim) break;
     const float k = ex2_approx(fminf(__uint_as_float(r[j]), 0.f));
+    const float2 kk = make_float2(k, k);
     const float4 *zp = reinterpret_cast<const float4 *>(z + j * KV);
 #pragma unroll
-    for (int g = 0; g < KV / 4; ++g) {
-      const float4 zz = __ldg(zp + g);
-      acc[4 * g + 0] = fmaf(k, zz.x, acc[4 * g + 0]);
-      acc[4 * g + 1] = fmaf(k, zz.y, acc[4 * g + 1]);
-      acc[4 * g + 2] = fmaf(k, zz.z, acc[4 * g + 2]);
-      acc[4 * g + 3] = fmaf(k, zz.w, acc[4 * g + 3]);
+    for (int g = 0; g < KV / 4; ++g) {  // z in shared memory: LDS.128 broadcast per warp
+      const float4 zz = zp[g];  // smem (resident kernel) or global (streaming)
+      acc[2 * g] = __ffma2_rn(kk, make_float2(zz.x, zz.y), acc[2 * g]);
+      acc[2 * g + 1] = __ffma2_rn(kk, make_float2(zz.z, zz.w), acc[2 * g + 1]);
     }
   }
 }
@@ -452,28 +451,40 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       __syncwarp();
     }
   } else if (KV > 1 && warp >= 4) {
-    // multi-vector epilogue: thread = P row, KV fp32 chains per tile -> KV fp64 sums
+    // multi-vector epilogue: thread = P row; the Q tile's z block ([NT][KV] fp32) is staged in
+    // shared memory (double-buffered, one named barrier per tile), KV/2 packed FFMA2 chains per
+    // tile in fp32, then KV fp64 sums
     const int ew = warp - 4;
     const int lg = ew & 3;
     const int half = ew >> 2;
     const int row = lg * 32 + lane;
+    const int etid = ew * 32 + lane;  // 0 .. 32 * EPIW - 1
     const int64_t p = p0 + row;
     const int col0 = half * HALF;
+    float *zsm = reinterpret_cast<float *>(red + (size_t)TC_M * (KV > 3 ? KV : 3));  // [2][NT][KV]
     double acc64[KV];
 #pragma unroll
     for (int c = 0; c < KV; ++c) acc64[c] = 0.0;
     uint32_t rr[2][32];
     for (int t = 0; t < ntiles; ++t) {
+      const int64_t q0 = qlo + (int64_t)t * NT;
+      if (!STREAM) {  // streaming kernel: no shared memory left, z is read through L1
+        float4 *dst = reinterpret_cast<float4 *>(zsm + (t & 1) * NT * KV);
+        const float4 *src = reinterpret_cast<const float4 *>(a.z + q0 * KV);
+        const int64_t lim4 = (lmin(NT, a.nq - q0) * KV) / 4;
+        for (int e = etid; e < NT * KV / 4; e += 32 * EPIW)
+          dst[e] = e < lim4 ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * EPIW) : "memory");
+      }
       const int accb = t & 1;
       mbar_wait(&tfull[accb], (t >> 1) & 1);
       tc_fence_after();
-      const int64_t q0 = qlo + (int64_t)t * NT;
       const int cnt = (int)lmin(NT, qhi - q0) - col0;
       const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(accb * NT + col0);
-      const float *zt = a.z + (q0 + col0) * KV;
-      float acc[KV];
+      const float *zt = STREAM ? a.z + (q0 + col0) * KV : zsm + (t & 1) * NT * KV + col0 * KV;
+      float2 acc[KV > 1 ? KV / 2 : 1];
 #pragma unroll
-      for (int c = 0; c < KV; ++c) acc[c] = 0.f;
+      for (int c = 0; c < KV / 2; ++c) acc[c] = make_float2(0.f, 0.f);
       if (cnt >= HALF) {
         tmem_ld32(tb, rr[0]);
         tmem_wait_ld_regs(rr[0]);
@@ -494,7 +505,10 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[accb]);
 #pragma unroll
-      for (int c = 0; c < KV; ++c) acc64[c] += (double)acc[c];
+      for (int c = 0; c < KV / 2; ++c) {
+        acc64[2 * c] += (double)acc[c].x;
+        acc64[2 * c + 1] += (double)acc[c].y;
+      }
     }
     // combine the column groups of each row in a fixed order (deterministic)
     if (half > 0) {
@@ -648,9 +662,13 @@ int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const floa
   return FALKON_OK;
 }
 
+// tail: fp64 row partials [TC_M][max(3, kv)] and (kv > 1) the z staging buffers [2][nt][kv] fp32
+static size_t tc_tail_bytes(int nt, int kv, bool stream = false) {
+  return (size_t)8 * TC_M * std::max(3, kv) + (kv > 1 && !stream ? (size_t)2 * nt * kv * 4 : 0);
+}
 static size_t tc_smem_bytes(int nbox, int stages, int nt, int kv = 1) {
   return 1024 + (size_t)nbox * TC_A_BOX + (size_t)stages * nt * TC_BK * 2 + 256 +
-         (size_t)8 * TC_M * std::max(3, kv);
+         tc_tail_bytes(nt, kv);
 }
 static int tc_stages(int nbox, int nt, int kv = 1) {
   int s = 8;
@@ -672,8 +690,9 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   const int nt = ts ? TC_N_TS : TC_N;
   const int stages = stream ? 2 : tc_stages(nbox, nt, kv);
   const size_t smem = stream ? 1024 + (size_t)2 * 2 * (TC_A_BOX + TC_B_BOX) + 256 +
-                                   (size_t)8 * TC_M * std::max(3, kv)
+                                   tc_tail_bytes(nt, kv, true)
                              : tc_smem_bytes(nbox, stages, nt, kv);
+  if (smem > (size_t)TC_SMEM_MAX) return fail(FALKON_EUNSUPPORTED, "tc_pass: shared memory");
   int mode = ctx->opt.exp_offload;
   if (const char *e = getenv("FALKON_TC_MODE")) mode = atoi(e);  // diagnostics (8-11)
   typedef void (*kfn)(const CUtensorMap, const CUtensorMap, TcArgs);

@@ -1,0 +1,57 @@
+"""The bench.py contract on CPU (-m "not gpu"): the reference arm (the CPU oracle, tier
+framing) prints ONE JSON line with the driver's keys, rank > 0 prints nothing, and the roofline
+helper's algorithmic work matches SURVEY.md §8(d)'s per-entry figures."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(args, env=None):
+    e = dict(os.environ)
+    e.update(env or {})
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True,
+                       text=True, timeout=300, env=e, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return [ln for ln in r.stdout.splitlines() if ln.strip()]
+
+
+def test_reference_arm_json_line():
+    lines = _run(["--impl", "reference", "--config", "tiny", "--steps", "2", "--warmup", "1",
+                  "--oracle-seconds", "0.5"])
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["steps"] == 2 and d["warmup"] == 1
+    assert d["value"] > 0 and d["unit"] == "n*m/s" and d["config"]["workload"] == "tiny"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["cpu_baseline"]["cores"] >= 1
+
+
+def test_reference_arm_nonzero_rank_is_silent():
+    lines = _run(["--impl", "reference", "--config", "tiny", "--steps", "1", "--warmup", "1",
+                  "--oracle-seconds", "0.2"], env={"RANK": "1", "WORLD_SIZE": "2"})
+    assert lines == []
+
+
+def test_roofline_algorithmic_work():
+    """tensor path: achieved TFLOP/s = 2 d n m / t; SIMT: evals / t against min(FP32, MUFU)."""
+    sys.path.insert(0, ROOT)
+    import argparse
+    import bench
+    import synth
+    args = argparse.Namespace(path="auto")
+    cfg = synth.CONFIGS["msd"]
+    kt = {"pass_a": (10.0, 1), "pass_b": (9.0, 1)}
+    r = bench.roofline(args, cfg, kt, 20.0, cfg.n, cfg.m, 148)
+    assert r["bound"] == "tensor" and r["kernel"] == "pass_a"
+    assert abs(r["achieved"] - 2 * cfg.d * cfg.n * cfg.m / 10e-3 / 1e12) < 1e-9
+    cfg = synth.CONFIGS["tiny"]
+    r = bench.roofline(args, cfg, kt, 20.0, cfg.n, cfg.m, 148)
+    assert r["bound"] == "alu" and r["unit"] == "G kernel-evals/s"
+    assert abs(r["achieved"] - cfg.n * cfg.m / 10e-3 / 1e9) < 1e-9
