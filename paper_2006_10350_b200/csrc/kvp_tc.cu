@@ -308,7 +308,10 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   uint64_t *full = bars, *empty = bars + TC_MAX_STAGES, *tfull = bars + 2 * TC_MAX_STAGES,
            *tempty = tfull + 2, *afull = tempty + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(afull + 1);
-  double *red = reinterpret_cast<double *>(tmem_slot + 4);  // [TC_M] fp64 half-row partials
+  // [TC_M] fp64 half-row partials, 16-B aligned: the kv epilogue's z staging buffer that
+  // follows is accessed as float4 (bars + slot end at byte 184 of the 256-byte region)
+  double *red = reinterpret_cast<double *>(
+      (reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)blockIdx.x * TC_M;
