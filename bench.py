@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--gsc-config", default=None, choices=[None] + list(synth.GSC_CONFIGS),
                     help="also time one GSC-Falkon / LogFalkon fit (Alg. 2) on this workload")
     ap.add_argument("--gsc-n", type=int, default=None, help="override the GSC workload's n")
+    ap.add_argument("--single-eval", type=int, default=None, choices=[0, 1, 2],
+                    help="products: 0 two passes, 1 single evaluation (k strip), 2 auto")
+    ap.add_argument("--tc-cluster", type=int, default=None, choices=[1, 2],
+                    help="tensor path: 1 CTA or 2-CTA clusters multicasting the Q boxes")
     ap.add_argument("--multi-k", type=int, default=0,
                     help="also time the k-output product Knm^T (Knm V), V in R^{m x k} (NEXT-3)")
     ap.add_argument("--quick", action="store_true",
@@ -162,6 +166,24 @@ def kt_path_tensor(args, d):
     return args.path == "tensor" or d > 8
 
 
+# The paper's whole-fit times on the real datasets (context, not the target).
+PAPER_FIT = {
+    "msd": "Table 2/4 (PAPER.md:598-601, 846-853): MSD fit 62 s (2x Titan Xp) / 81 s (1x)",
+    "timit": "Table 2/4 (PAPER.md:598-601, 846-853): TIMIT fit 288 s (2x Titan Xp) / 416 s (1x)",
+    "higgs": "Table 2/4 (PAPER.md:566-569, 846-853): HIGGS fit 443 s (2x Titan Xp) / 715 s (1x)",
+    "taxi": "Table 2/4 (PAPER.md:566-569, 846-853): TAXI fit 3628 s (2x Titan Xp) / 7215 s (1x)",
+}
+
+
+def single_eval_active(args, d) -> bool:
+    """Mirror of tc_single_eval() in csrc/kvp_tc.cu: single evaluation (k strip) on the tensor
+    path when forced, or by default when the padded segment exceeds 192 (d > 190)."""
+    if not kt_path_tensor(args, d):
+        return False
+    se = 2 if args.single_eval is None else args.single_eval
+    return se == 1 or (se == 2 and -(-(d + 2) // 16) * 16 > 192)
+
+
 def roofline(args, cfg, kt, ms_total, n_local, m, sms):
     """Roofline of the dominant kernel (the pass with the larger device time in the timed
     region; both passes evaluate every Knm entry once).  Algorithmic work per launch and
@@ -179,7 +201,9 @@ def roofline(args, cfg, kt, ms_total, n_local, m, sms):
     peaks, peak_src = measured_peaks()
     dom = max(("pass_a", "pass_b"), key=lambda k: kt[k][0])
     dom_ms = kt[dom][0] / max(1, kt[dom][1])
-    evals = n_local * m
+    # entries per launch of the dominant class: a single-evaluation product launches pass A
+    # once per row strip, so the rate is taken over all launches of the timed region
+    evals = n_local * m * args.steps * dom_ms / max(kt[dom][0], 1e-9)
     d = cfg.d
     f_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     traffic = None
@@ -202,6 +226,14 @@ def roofline(args, cfg, kt, ms_total, n_local, m, sms):
         extra = {"issued_frac": issued_tf / float(peaks["bf16_tflops"]),
                  "evals_per_s": ach_eval, "tensor_evals_peak": tc_eval_peak,
                  "mufu_evals_peak": mufu_eval_peak}
+        if single_eval_active(args, d) and kt["pass_b"][1]:
+            # second contraction = streaming GEMV over the stored k strip: HBM-bound, 4 B/entry
+            gb_s = 4.0 * n_local * m * args.steps / (kt["pass_b"][0] * 1e-3) / 1e9
+            extra["single_eval"] = True
+            extra["strip_gemv"] = {"bound": "hbm", "achieved": gb_s,
+                                   "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
+                                   "frac": gb_s / float(peaks["hbm_gbs"]),
+                                   "ms_per_product": kt["pass_b"][0] / args.steps}
         if tc_eval_peak <= mufu_eval_peak:
             ach_tf = 2.0 * d * ach_eval / 1e12
             return {"bound": "tensor", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
@@ -321,6 +353,10 @@ def main():
     ctx.set_option(binding.OPT_PATH, {"auto": 0, "simt": 1, "tensor": 2}[args.path])
     if args.exp_offload is not None:
         ctx.set_option(binding.OPT_EXP_OFFLOAD, args.exp_offload)
+    if args.single_eval is not None:
+        ctx.set_option(binding.OPT_SINGLE_EVAL, args.single_eval)
+    if args.tc_cluster is not None:
+        ctx.set_option(binding.OPT_TC_CLUSTER, args.tc_cluster)
 
     n_global = args.n or cfg.n
     m = args.m or cfg.m
@@ -435,7 +471,7 @@ def main():
             fit = {"seconds": wall, "iters": iters, "t_precond_s": info["t_precond_s"],
                    "t_rhs_s": info["t_rhs_s"], "t_cg_s": info["t_cg_s"],
                    "iters_run": info["iters_run"],
-                   "paper_context": "Table 2/4: MSD fit 62 s (2x Titan Xp) / 81 s (1x)"}
+                   "paper_context": PAPER_FIT.get(cfg.name)}
         except Exception as ex:  # report, do not hide
             fit = {"error": str(ex)}
 

@@ -72,8 +72,19 @@ enum {
                                    2 = 1/4, 3 = 1/2 of the entries (rest on MUFU) */
   FALKON_OPT_POTRF_OUTER = 6,   /* blocked Cholesky: depth of the trailing fp64 GEMM updates in
                                    units of 128 columns (1..64, default 8) */
-  FALKON_OPT_GEMM_WARPS = 7     /* fp64 DMMA GEMM CTA: 8 (128 x 128 tile, 8 warps), 16 (16 warps)
+  FALKON_OPT_GEMM_WARPS = 7,    /* fp64 DMMA GEMM CTA: 8 (128 x 128 tile, 8 warps), 16 (16 warps)
                                    or 2 (128 x 64 tiles, 2 CTAs of 8 warps per SM) */
+  FALKON_OPT_SINGLE_EVAL = 8,   /* single-vector products on the tensor path: 0 = two passes (the
+                                   cross term and exp evaluated twice), 1 = single evaluation:
+                                   pass A also stores k(x_i, c_j) for a strip of rows in HBM and
+                                   u += strip^T w reads them back, 2 = auto
+                                   (default: single evaluation when d > 190, where the fp16x3
+                                   cross term costs more than the 8 B/entry strip round trip) */
+  FALKON_OPT_STRIP_BYTES = 9,   /* single evaluation: device bytes of the k strip (default 16 GiB,
+                                   minimum 64 MiB; rows per strip = bytes / (4 m)) */
+  FALKON_OPT_TC_CLUSTER = 10    /* tensor path: 1 = one CTA per P tile; 2 = clusters of two CTAs on
+                                   consecutive P tiles, each loading half of every streamed Q box
+                                   and multicasting it to both (halves the L2 -> SM traffic) */
 };
 
 /* Per-launch-class accumulated device times in ms (falkon_ctx_timings). */

@@ -222,6 +222,10 @@ static int product(falkon_ctx *ctx, Fit &F, const double *v, double *u,
                    const float *dw = nullptr) {
   const int64_t m = F.pp.m;
   FK_TRY(f64_to_f32(ctx, v, F.v32, m, round_up<int64_t>(m, 128)));
+  if (!dw && F.pp.n > 0 && tc_single_eval(ctx, F.pp)) {  // NEXT-4: one evaluation per entry
+    FK_TRY(tc_product_single_eval(ctx, F.pp, F.v32, F.w32, u));
+    return nccl_allreduce_f64(ctx, u, m);
+  }
   FK_TRY(pass_A(ctx, F.pp, F.v32, nullptr, F.w32));
   if (dw) {
     const int64_t n_pad = round_up<int64_t>(std::max<int64_t>(F.pp.n, 1), 128);
@@ -501,6 +505,18 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
     case FALKON_OPT_POTRF_OUTER:
       if (value < 1 || value > 64) return fail(FALKON_EINVAL, "potrf outer block must be 1..64 x 128");
       ctx->opt.potrf_outer = (int)value;
+      return FALKON_OK;
+    case FALKON_OPT_SINGLE_EVAL:
+      if (value < 0 || value > 2) return fail(FALKON_EINVAL, "single_eval must be 0, 1 or 2");
+      ctx->opt.single_eval = (int)value;
+      return FALKON_OK;
+    case FALKON_OPT_STRIP_BYTES:
+      if (value < ((int64_t)64 << 20)) return fail(FALKON_EINVAL, "strip bytes must be >= 64 MiB");
+      ctx->opt.strip_bytes = value;
+      return FALKON_OK;
+    case FALKON_OPT_TC_CLUSTER:
+      if (value != 1 && value != 2) return fail(FALKON_EINVAL, "tc_cluster must be 1 or 2");
+      ctx->opt.tc_cluster = (int)value;
       return FALKON_OK;
     default:
       return fail(FALKON_EINVAL, "unknown option");

@@ -65,6 +65,8 @@ enum WsSlot {
   WS_MW32,        // fp32 [n_pad][kv] pass-A output block (multi-output)
   WS_MU64,        // fp64 [m][kv] pass-B output block (multi-output)
   WS_MULTI,       // fp64 multi-output fit state
+  WS_KSTRIP,      // fp32 k strip of the single-evaluation product [rows][ldk]
+  WS_SE_ACC,      // fp64 [splits][m] accumulators of the strip GEMV
   WS_COUNT
 };
 
@@ -83,6 +85,10 @@ struct Options {
                         // 4.78 s vs 4.96 s for 8 = 128 x 128 tiles, 1 CTA/SM; 16 = 16 warps)
   int potrf_outer = 8;  // outer POTRF block in units of NB = 128 (trailing-update depth;
                         // measured m = 5e4: 2 -> 5.46 s, 4 -> 5.21 s, 8 -> 5.10 s)
+  int single_eval = 2;  // 0 two-pass, 1 single evaluation (k strip through HBM), 2 auto
+  int tc_cluster = 2;   // tensor path: clusters of 2 CTAs multicasting the Q boxes (measured
+                        // MSD 21.7 -> 20.9 ms, TIMIT 431 -> 424 ms), or 1 CTA
+  int64_t strip_bytes = (int64_t)16 << 30;
 };
 
 }  // namespace falkon
@@ -168,6 +174,13 @@ int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const floa
 // kv > 1 (8 or 16): z is [q][kv] fp32 and the outputs [p][kv] (multi-vector product)
 int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, double *out64,
             float *out32, int kv = 1);
+// single evaluation: true when single-vector products use the k strip
+bool tc_single_eval(const falkon_ctx *ctx, const Prepared &pp);
+// u = Knm^T (Knm z) on this rank with every kernel value evaluated once: per strip of rows,
+// pass A stores the strip's k values (fp32, row-major) while computing w, then a streaming
+// GEMV reads them back for u += strip^T w.  w32: fp32 n_pad output (w of every row).
+int tc_product_single_eval(falkon_ctx *ctx, const Prepared &pp, const float *z, float *w32,
+                           double *u);
 
 // ------------------------------------------------------------------ preconditioner (precond.cu)
 int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel, double sigma,

@@ -133,6 +133,38 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA multicast (cluster): the box lands at the same shared-memory offset in every CTA of
+// `mask` and completes `bytes` on each destination's mbarrier at the offset of `bar`.
+__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *map, int c0, int c1,
+                                               uint64_t *bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// mbarrier wait that traps (kernel error instead of a hung GPU) if a phase never completes:
+// every legitimate wait in these kernels is bounded by one tile's work (micro- to milliseconds)
+__device__ __forceinline__ void mbar_wait_safe(uint64_t *bar, uint32_t phase) {
+  uint32_t it = 0;
+  long long t0 = 0;
+  while (!mbar_try_wait(bar, phase)) {
+    if ((++it & 1023u) == 0) {
+      const long long t = clock64();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 8000000000LL) __trap();
+    }
+  }
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -160,6 +192,14 @@ __device__ __forceinline__ void tc_commit(uint64_t *bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(bar))
+      : "memory");
+}
+// commit arriving on the barrier at this offset in every CTA of `mask` (cluster multicast)
+__device__ __forceinline__ void tc_commit_mc(uint64_t *bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
       : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -199,6 +239,9 @@ struct TcArgs {
   int stages;    // depth of the Q-box ring
   double *out64;
   float *out32;
+  int64_t p_base;  // first P row of this launch (TMA row coordinate offset; 0 = all rows)
+  float *kst;      // single-evaluation strip: k values stored row-major [np][ldk] (or null)
+  int64_t ldk;
 };
 
 constexpr int TC_EPI_WARPS = 8;   // 2 per SM sub-partition: (TMEM lane group, column half)
@@ -232,20 +275,30 @@ __device__ __forceinline__ float tc_exp2(float t, int e) {
   return ex2_approx(t);
 }
 
-// 32 accumulator columns: k = exp2(min(t, 0)), acc += k * z (4 independent FFMA chains)
-template <int MODE, bool MASK>
+// 32 accumulator columns: k = exp2(min(t, 0)), acc += k * z (4 independent FFMA chains).
+// KST (single-evaluation strip): the 32 k values are also stored to kdst[j * TC_M], j < lim
+// (the strip is column-major inside each 128-row tile, so each warp store is coalesced), and
+// the second contraction reads them back instead of recomputing the cross term and the exp.
+template <int MODE, bool MASK, bool KST = false>
 __device__ __forceinline__ void tc_epi_chunk(const uint32_t (&r)[32], const float *__restrict__ z,
-                                             int lim, float (&acc)[4]) {
+                                             int lim, float (&acc)[4], float *kdst = nullptr) {
   const float4 *zp = reinterpret_cast<const float4 *>(z);
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
     const float4 zz = __ldg(zp + g);
     float zv[4] = {zz.x, zz.y, zz.z, zz.w};
+    float kv[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int j = 4 * g + e;
       if (MASK && j >= lim) zv[e] = 0.f;
-      acc[e] = fmaf(tc_exp2<MODE>(__uint_as_float(r[j]), e), zv[e], acc[e]);
+      kv[e] = tc_exp2<MODE>(__uint_as_float(r[j]), e);
+      acc[e] = fmaf(kv[e], zv[e], acc[e]);
+    }
+    if (KST) {  // column j of the tile: the warp's 32 rows are 128 contiguous bytes
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (!MASK || 4 * g + e < lim) __stcs(kdst + (4 * g + e) * TC_M, kv[e]);  // evict-first
     }
   }
 }
@@ -288,7 +341,12 @@ __device__ __forceinline__ void tc_cp_128x256b(uint32_t tmem_dst, uint64_t sdesc
 // STREAM: large d (2*d16 > 384): the P tile cannot stay resident, so each pipeline stage
 // carries the matching 64-wide K box of BOTH segments of P and Q ([h|l] layout with
 // 64-aligned segments): 16 + 16 + 32 + 32 KB, three MMAs per 16-wide chunk.
-template <int MODE, int NT, bool TS, bool STREAM = false, int EPIW = TC_EPI_WARPS, int KV = 1>
+// CL = 2: clusters of two CTAs on consecutive P tiles (same Q range): each CTA loads one
+// 128-row half of every Q box and multicasts it to both, halving the L2 -> SM traffic of the
+// streamed operand; a stage is refilled only after BOTH CTAs' MMAs have released it (empty
+// barriers count CL arrivals, commits are multicast).
+template <int MODE, int NT, bool TS, bool STREAM = false, int EPIW = TC_EPI_WARPS, int KV = 1,
+          bool KST = false, int CL = 1>
 __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     tc_kvp_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                   TcArgs a) {
@@ -323,7 +381,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -342,15 +400,18 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // partner's barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t crank = CL > 1 ? cluster_rank() : 0;
+  constexpr uint16_t CMASK = (uint16_t)((1u << CL) - 1);
   const uint32_t tmem_a = tmem + 2 * NT;  // TS: P tile columns (8 per 16-wide chunk)
 
   if (warp == 0) {
     // TMA producer: the whole warp walks the ring, one elected lane issues the copies
     if (!STREAM && elect_one()) {
       mbar_expect_tx(afull, (uint32_t)(a.nbox * TC_A_BOX));
-      for (int b = 0; b < a.nbox; ++b) tma_load_2d(sA + b * TC_A_BOX, &tmP, b * TC_BK, (int)p0, afull);
+      for (int b = 0; b < a.nbox; ++b) tma_load_2d(sA + b * TC_A_BOX, &tmP, b * TC_BK, (int)(a.p_base + p0), afull);
     }
     __syncwarp();
     const int segk = a.nk * 16;  // STREAM: elements per segment
@@ -359,21 +420,34 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     for (int t = 0; t < ntiles; ++t) {
       const int q0 = (int)(qlo + (int64_t)t * NT);
       for (int b = 0; b < a.nbox; ++b) {
-        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_wait_safe(&empty[stage], phase ^ 1);
         if (elect_one()) {
           if (MODE == 11) {  // diagnostic: no Q loads
             mbar_arrive(&full[stage]);
           } else if (STREAM) {
             uint8_t *st = sB + stage * BBOX;
             mbar_expect_tx(&full[stage], BBOX);
-            tma_load_2d(st, &tmP, b * TC_BK, (int)p0, &full[stage]);                     // h_p
-            tma_load_2d(st + TC_A_BOX, &tmP, segk + b * TC_BK, (int)p0, &full[stage]);   // l_p
-            tma_load_2d(st + 2 * TC_A_BOX, &tmQ, b * TC_BK, q0, &full[stage]);           // h_q
-            tma_load_2d(st + 2 * TC_A_BOX + NT * TC_BK * 2, &tmQ, segk + b * TC_BK, q0,
-                        &full[stage]);                                                   // l_q
+            tma_load_2d(st, &tmP, b * TC_BK, (int)(a.p_base + p0), &full[stage]);        // h_p
+            tma_load_2d(st + TC_A_BOX, &tmP, segk + b * TC_BK, (int)(a.p_base + p0),
+                        &full[stage]);  // l_p
+            if (CL == 1) {
+              tma_load_2d(st + 2 * TC_A_BOX, &tmQ, b * TC_BK, q0, &full[stage]);         // h_q
+              tma_load_2d(st + 2 * TC_A_BOX + NT * TC_BK * 2, &tmQ, segk + b * TC_BK, q0,
+                          &full[stage]);                                                 // l_q
+            } else {  // this CTA's 128-row half of h_q and l_q, multicast to the cluster
+              const int qh = q0 + (int)crank * TC_M;
+              const uint32_t ho = crank * TC_A_BOX;
+              tma_load_2d_mc(st + 2 * TC_A_BOX + ho, &tmQ, b * TC_BK, qh, &full[stage], CMASK);
+              tma_load_2d_mc(st + 2 * TC_A_BOX + NT * TC_BK * 2 + ho, &tmQ, segk + b * TC_BK, qh,
+                             &full[stage], CMASK);
+            }
           } else {
             mbar_expect_tx(&full[stage], BBOX);
-            tma_load_2d(sB + stage * BBOX, &tmQ, b * TC_BK, q0, &full[stage]);
+            if (CL == 1)
+              tma_load_2d(sB + stage * BBOX, &tmQ, b * TC_BK, q0, &full[stage]);
+            else
+              tma_load_2d_mc(sB + stage * BBOX + crank * TC_A_BOX, &tmQ, b * TC_BK,
+                             q0 + (int)crank * TC_M, &full[stage], CMASK);
           }
         }
         __syncwarp();
@@ -393,7 +467,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     auto adesc = [&](int c) -> uint64_t {
       return a0 + (uint64_t)(((c >> 2) * TC_A_BOX + (c & 3) * 32) >> 4);
     };
-    if (!STREAM) mbar_wait(afull, 0);
+    if (!STREAM) mbar_wait_safe(afull, 0);
     tc_fence_after();
     if (TS) {
       if (elect_one())
@@ -404,11 +478,11 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     uint32_t phase = 0;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t & 1;
-      mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+      mbar_wait_safe(&tempty[acc], ((t >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t dtm = tmem + (uint32_t)(acc * NT);
       for (int b = 0; b < a.nbox; ++b) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait_safe(&full[stage], phase);
         tc_fence_after();
         if (STREAM && elect_one()) {
           const uint64_t ah = b0 + (uint64_t)((stage * BBOX) >> 4);
@@ -424,7 +498,8 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
               tc_mma_f16(dtm, ah + o, bl + o, idesc, 1u);                  // h_p . l_q
             }
           }
-          tc_commit(&empty[stage]);
+          if (CL == 1) tc_commit(&empty[stage]);
+          else tc_commit_mc(&empty[stage], CMASK);
         } else if (!STREAM && elect_one()) {
           const uint64_t bs = b0 + (uint64_t)((stage * BBOX) >> 4);
 #pragma unroll
@@ -442,7 +517,8 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
               }
             }
           }
-          tc_commit(&empty[stage]);
+          if (CL == 1) tc_commit(&empty[stage]);
+          else tc_commit_mc(&empty[stage], CMASK);
         }
         __syncwarp();
         if (++stage == S) {
@@ -480,7 +556,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
         asm volatile("bar.sync 2, %0;" ::"n"(32 * EPIW) : "memory");
       }
       const int accb = t & 1;
-      mbar_wait(&tfull[accb], (t >> 1) & 1);
+      mbar_wait_safe(&tfull[accb], (t >> 1) & 1);
       tc_fence_after();
       const int cnt = (int)lmin(NT, qhi - q0) - col0;
       const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(accb * NT + col0);
@@ -539,14 +615,38 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     uint32_t rr[2][32];
     for (int t = 0; t < ntiles; ++t) {
       const int accb = t & 1;
-      mbar_wait(&tfull[accb], (t >> 1) & 1);
+      mbar_wait_safe(&tfull[accb], (t >> 1) & 1);
       tc_fence_after();
       const int64_t q0 = qlo + (int64_t)t * NT;
       const int cnt = (int)lmin(NT, qhi - q0) - col0;  // valid columns of this half
       const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(accb * NT + col0);
       const float *zt = a.z + q0 + col0;
+      // KST: strip tile blockIdx.x, layout [tile][q][TC_M rows]; padding rows (p >= np) are
+      // stored too (finite values; the GEMV weights them by w = 0)
+      float *kd = KST ? a.kst + ((int64_t)blockIdx.x * a.ldk + q0 + col0) * TC_M + row : nullptr;
+      const bool kok = p0 < a.np;  // a cluster's padding CTA (whole tile past the strip) stores nothing
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      if (MODE == 9) {  // diagnostic: no TMEM traffic
+      if (KST) {
+        const int cw = cnt < HALF ? cnt : HALF;  // this warp's columns
+        if (cw == HALF) {  // software-pipelined as below
+          tmem_ld32(tb, rr[0]);
+          tmem_wait_ld_regs(rr[0]);
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            if (c + 1 < NCH) tmem_ld32(tb + (uint32_t)((c + 1) * 32), rr[(c + 1) & 1]);
+            if (kok) tc_epi_chunk<MODE, false, true>(rr[c & 1], zt + c * 32, 32, acc, kd + c * 32 * TC_M);
+            else tc_epi_chunk<MODE, false>(rr[c & 1], zt + c * 32, 32, acc);
+            if (c + 1 < NCH) tmem_wait_ld_regs(rr[(c + 1) & 1]);
+          }
+        } else {
+          for (int c = 0; c * 32 < cw; ++c) {
+            tmem_ld32(tb + (uint32_t)(c * 32), rr[0]);
+            tmem_wait_ld_regs(rr[0]);
+            if (kok) tc_epi_chunk<MODE, true, true>(rr[0], zt + c * 32, cw - c * 32, acc, kd + c * 32 * TC_M);
+            else tc_epi_chunk<MODE, true>(rr[0], zt + c * 32, cw - c * 32, acc);
+          }
+        }
+      } else if (MODE == 9) {  // diagnostic: no TMEM traffic
 #pragma unroll
         for (int j = 0; j < 32; ++j) rr[0][j] = __float_as_uint(-(float)j);
         for (int c = 0; c * 32 < cnt; ++c) tc_epi_chunk<0, true>(rr[0], zt + c * 32, cnt - c * 32, acc);
@@ -585,6 +685,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // the partner's last multicasts / commits into this CTA are done
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -680,15 +781,46 @@ static int tc_stages(int nbox, int nt, int kv = 1) {
 }
 
 
-int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, double *out64,
-            float *out32, int kv) {
+// Co-resident CTAs of a 2-CTA-cluster launch (2 x cudaOccupancyMaxActiveClusters; a GPC with
+// an odd number of free SMs leaves one idle), cached per kernel.
+static int64_t tc_cluster_slots(falkon_ctx *ctx, const void *fn, int threads, size_t smem) {
+  static const void *last_fn = nullptr;
+  static int64_t last = 0;
+  if (fn == last_fn && last > 0) return last;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * ctx->sm_count);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, fn, &cfg) != cudaSuccess || nc <= 0) {
+    cudaGetLastError();
+    return ctx->sm_count;
+  }
+  last_fn = fn;
+  last = 2 * (int64_t)nc;
+  return last;
+}
+
+// One fused pass over P rows [p_begin, p_begin + p_count) (p_count < 0: all).  kst != null
+// (pass A, kv = 1): the k values are also stored row-major into kst[(p - p_begin) * ldk + q].
+static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z,
+                     double *out64, float *out32, int kv, int64_t p_begin, int64_t p_count,
+                     float *kst, int64_t ldk) {
   const CUtensorMap *maps = reinterpret_cast<const CUtensorMap *>(pp.tmaps);
   const int d16 = pp.dq;
   const bool stream = tc_stream(pp.d);
   // resident: boxes of a whole packed row; streaming: boxes of one segment
   const int nbox = stream ? d16 / TC_BK : (int)cdiv<int64_t>(2 * d16, TC_BK);
-  const int64_t np = passA ? pp.n : pp.m, nq = passA ? pp.m : pp.n;
+  const int64_t np = p_count >= 0 ? p_count : (passA ? pp.n : pp.m), nq = passA ? pp.m : pp.n;
   if (np <= 0) return FALKON_OK;
+  if (kst && (!passA || kv != 1)) return fail(FALKON_EINVAL, "tc_launch: k strip needs pass A, kv 1");
   const bool ts = kv == 1 && !stream && tc_use_ts(d16);
   const int nt = ts ? TC_N_TS : TC_N;
   const int stages = stream ? 2 : tc_stages(nbox, nt, kv);
@@ -721,6 +853,20 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   }
 #undef FK_TC
   if (stream) fn = mode == 11 ? tc_kvp_kernel<11, TC_N, false, true> : tc_kvp_kernel<0, TC_N, false, true>;
+  // 2-CTA clusters with Q multicast (FALKON_OPT_TC_CLUSTER): MODE 0, SS, single vector
+  const int cl = (ctx->opt.tc_cluster == 2 && kv == 1 && !ts && (mode == 0 || kst)) ? 2 : 1;
+  if (cl == 2 && !kst)
+    fn = stream ? tc_kvp_kernel<0, TC_N, false, true, 8, 1, false, 2>
+                : tc_kvp_kernel<0, TC_N, false, false, 16, 1, false, 2>;
+  if (kst) {  // single-evaluation strip (MODE 0; exp offload modes do not apply)
+    if (cl == 2)
+      fn = stream ? tc_kvp_kernel<0, TC_N, false, true, 8, 1, true, 2>
+                  : tc_kvp_kernel<0, TC_N, false, false, 16, 1, true, 2>;
+    else
+      fn = stream ? tc_kvp_kernel<0, TC_N, false, true, 8, 1, true>
+                  : tc_kvp_kernel<0, TC_N, false, false, 16, 1, true>;
+    epiw = stream ? 8 : 16;
+  }
   if (kv > 1) {  // multi-vector epilogue (8 epilogue warps: KV fp32 + KV fp64 sums per thread)
     epiw = 8;
     if (kv == 8) fn = stream ? tc_kvp_kernel<0, TC_N, false, true, 8, 8> : tc_kvp_kernel<0, TC_N, false, false, 8, 8>;
@@ -730,21 +876,23 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   const int threads = 128 + 32 * epiw;
   FK_CUDA(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                TC_SMEM_MAX));
-  // grid: P tiles x Q splits, sized to whole waves of one CTA per SM
-  const int64_t gx = cdiv<int64_t>(np, TC_M);
+  // grid: P tiles (a whole number of clusters) x Q splits, sized to whole waves of the
+  // co-resident CTAs (one per SM; with clusters, 2 x the co-resident clusters)
+  const int64_t gx = round_up<int64_t>(cdiv<int64_t>(np, TC_M), cl);
   const int64_t qt = cdiv<int64_t>(std::max<int64_t>(nq, 1), nt);
+  const int64_t slots = cl == 1 ? ctx->sm_count : tc_cluster_slots(ctx, (const void *)fn, threads, smem);
   int64_t best_s = 1;
   double best_eff = -1.0;
   for (int64_t s = 1; s <= 32; ++s) {
     if (s > 1 && qt / s < 4) break;
     const int64_t ctas = gx * s;
-    const int64_t waves = cdiv<int64_t>(ctas, ctx->sm_count);
-    const double eff = (double)ctas / (double)(waves * ctx->sm_count);
+    const int64_t waves = cdiv<int64_t>(ctas, slots);
+    const double eff = (double)ctas / (double)(waves * slots);
     if (eff > best_eff + 0.02) {
       best_eff = eff;
       best_s = s;
     }
-    if (ctas >= 8 * ctx->sm_count && eff > 0.9) break;
+    if (ctas >= 8 * slots && eff > 0.9) break;
   }
   int64_t qps = round_up<int64_t>(cdiv<int64_t>(nq, best_s), nt);
   const int64_t splits = std::max<int64_t>(1, cdiv<int64_t>(nq, qps));
@@ -764,15 +912,170 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   args.stages = stages;
   args.out64 = part;
   args.out32 = splits == 1 ? out32 : nullptr;
+  args.p_base = p_begin;
+  args.kst = kst;
+  args.ldk = ldk;
   {
     LaunchScope ls(ctx, passA ? FALKON_T_PASS_A : FALKON_T_PASS_B);
-    fn<<<dim3((unsigned)gx, (unsigned)splits), threads, smem, ctx->stream>>>(
-        passA ? maps[0] : maps[2], passA ? maps[1] : maps[3], args);
+    if (cl == 1) {
+      fn<<<dim3((unsigned)gx, (unsigned)splits), threads, smem, ctx->stream>>>(
+          passA ? maps[0] : maps[2], passA ? maps[1] : maps[3], args);
+    } else {  // Q boxes of 128 rows (the P-shaped map of the Q operand), cluster launch
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)gx, (unsigned)splits);
+      cfg.blockDim = dim3((unsigned)threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      FK_CUDA(cudaLaunchKernelEx(&cfg, fn, passA ? maps[0] : maps[2], passA ? maps[2] : maps[0], args));
+    }
   }
   FK_LAUNCH_CHECK();
   if (splits > 1 || (!out64 && !out32))
     FK_TRY(reduce_partials(ctx, part, splits, np * kv, out64, out32));
   return FALKON_OK;
+}
+
+int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, double *out64,
+            float *out32, int kv) {
+  return tc_launch(ctx, pp, passA, z, out64, out32, kv, 0, -1, nullptr, 0);
+}
+
+// ------------------------------------------------------------------ single evaluation (NEXT-4)
+// Two-pass products evaluate every kernel value twice (pass A needs the whole row of K for
+// w_i, pass B needs the finished w).  For large d the fp16x3 cross term (6 d16 flops per
+// entry on the tensor pipe) costs more than writing k once and reading it back (8 B per entry
+// of HBM traffic), so rows are processed in strips: pass A over the strip also stores its k
+// values, then this GEMV streams them back:  acc[s][j] (+)= sum_{i in split s} k_ij w_i.
+// Strip layout [tile][j][128 rows] (written coalesced by the epilogue): a warp reads centre
+// j's 128 values of a tile as one 512-byte float4 load; lane l holds w of rows 4l..4l+3 of
+// the tile.  A warp owns SE_CPW centres (independent loads in flight), lanes keep fp32 sums of
+// <= 128 terms flushed into fp64 (reading c12), one shuffle reduction per centre at the end,
+// one fp64 accumulator row per row split (no atomics: deterministic).
+constexpr int SE_WARPS = 8;
+constexpr int SE_CPW = 8;                     // centres per warp
+constexpr int SE_COLS = SE_WARPS * SE_CPW;    // centres per CTA
+constexpr int SE_FLUSH = 32;                  // tiles per fp32 partial (4 x 32 = 128 terms)
+__global__ void __launch_bounds__(32 * SE_WARPS) se_gemv_kernel(const float *__restrict__ K, int64_t ldk,
+                                                                const float *__restrict__ w, int64_t rows,
+                                                                int64_t tiles_per_split, int64_t m,
+                                                                double *__restrict__ acc, int first) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t jb = (int64_t)blockIdx.x * SE_COLS + warp * SE_CPW;
+  if (jb >= m) return;
+  const int64_t ntile = cdiv<int64_t>(rows, TC_M);
+  const int64_t t0 = (int64_t)blockIdx.y * tiles_per_split;
+  const int64_t t1 = lmin(ntile, t0 + tiles_per_split);
+  int64_t jc[SE_CPW];
+#pragma unroll
+  for (int c = 0; c < SE_CPW; ++c) jc[c] = lmin(jb + c, m - 1);  // clamped: duplicates discarded
+  double a64[SE_CPW];
+  float a32[SE_CPW];
+#pragma unroll
+  for (int c = 0; c < SE_CPW; ++c) a64[c] = 0.0, a32[c] = 0.f;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t r = t * TC_M + 4 * lane;
+    float4 wv;
+    if (r + 3 < rows) {
+      wv = __ldg(reinterpret_cast<const float4 *>(w + r));
+    } else {
+      wv.x = r < rows ? w[r] : 0.f;
+      wv.y = r + 1 < rows ? w[r + 1] : 0.f;
+      wv.z = r + 2 < rows ? w[r + 2] : 0.f;
+      wv.w = 0.f;
+    }
+    const float *kt = K + t * ldk * TC_M + 4 * lane;
+    float4 kv[SE_CPW];
+#pragma unroll
+    for (int c = 0; c < SE_CPW; ++c) kv[c] = __ldcs(reinterpret_cast<const float4 *>(kt + jc[c] * TC_M));
+#pragma unroll
+    for (int c = 0; c < SE_CPW; ++c) {
+      float s = a32[c];
+      s = fmaf(kv[c].x, wv.x, s);
+      s = fmaf(kv[c].y, wv.y, s);
+      s = fmaf(kv[c].z, wv.z, s);
+      a32[c] = fmaf(kv[c].w, wv.w, s);
+    }
+    if ((t - t0) % SE_FLUSH == SE_FLUSH - 1) {
+#pragma unroll
+      for (int c = 0; c < SE_CPW; ++c) a64[c] += (double)a32[c], a32[c] = 0.f;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < SE_CPW; ++c) {
+    double v = a64[c] + (double)a32[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    a64[c] = v;
+  }
+  if (lane < SE_CPW) {
+    double v = a64[0];
+#pragma unroll
+    for (int c = 1; c < SE_CPW; ++c)
+      if (lane == c) v = a64[c];
+    const int64_t j = jb + lane;
+    if (j < m) {
+      double *o = acc + (int64_t)blockIdx.y * m + j;
+      *o = first ? v : *o + v;
+    }
+  }
+}
+
+bool tc_single_eval(const falkon_ctx *ctx, const Prepared &pp) {
+  if (pp.path != FALKON_PATH_TENSOR || ctx->opt.single_eval == 0) return false;
+  if (ctx->opt.single_eval == 1) return true;
+  return tc_stream(pp.d);  // auto: d16 > 192 (TIMIT d = 440: 6 * 448 flops vs 8 B per entry)
+}
+
+int tc_product_single_eval(falkon_ctx *ctx, const Prepared &pp, const float *z, float *w32,
+                           double *u) {
+  const int64_t n = pp.n, m = pp.m;
+  const int64_t ldk = m;
+  // rows per strip: a whole number of 128-row P tiles within the strip budget, which is capped
+  // at half of the free device memory (plus the strip already held)
+  int64_t budget = ctx->opt.strip_bytes;
+  {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+      budget = std::min<int64_t>(budget, (int64_t)(fr / 2 + ctx->ws_bytes[WS_KSTRIP]));
+    else
+      cudaGetLastError();
+  }
+  const int64_t tile_bytes = (int64_t)4 * TC_M * ldk;
+  // equal strips (a short last strip would run a fraction of a wave)
+  const int64_t ntiles = cdiv<int64_t>(n, TC_M);
+  int64_t tiles = std::min<int64_t>(std::max<int64_t>(1, budget / tile_bytes), ntiles);
+  tiles = cdiv<int64_t>(ntiles, cdiv<int64_t>(ntiles, tiles));
+  const int64_t rows = tiles * TC_M;
+  void *kp, *ap;
+  FK_TRY(ws_get(ctx, WS_KSTRIP, (size_t)tiles * tile_bytes, &kp));
+  // GEMV grid: centre blocks x tile splits, at least ~4 waves of 8-warp CTAs
+  const int64_t cb = cdiv<int64_t>(m, SE_COLS);
+  const int64_t want = std::max<int64_t>(1, cdiv<int64_t>(4 * ctx->sm_count * 8, cb));
+  const int64_t splits = std::min<int64_t>(want, tiles);
+  const int64_t tps = cdiv<int64_t>(tiles, splits);
+  FK_TRY(ws_get(ctx, WS_SE_ACC, sizeof(double) * (size_t)splits * m, &ap));
+  float *K = (float *)kp;
+  double *acc = (double *)ap;
+  for (int64_t r0 = 0; r0 < n; r0 += rows) {
+    const int64_t nr = std::min<int64_t>(rows, n - r0);
+    FK_TRY(tc_launch(ctx, pp, true, z, nullptr, w32 + r0, 1, r0, nr, K, ldk));
+    LaunchScope ls(ctx, FALKON_T_PASS_B);
+    const int64_t sp = cdiv<int64_t>(cdiv<int64_t>(nr, TC_M), tps);
+    se_gemv_kernel<<<dim3((unsigned)cb, (unsigned)sp), 32 * SE_WARPS, 0, ctx->stream>>>(
+        K, ldk, w32 + r0, nr, tps, m, acc, r0 == 0 ? 1 : 0);
+    FK_LAUNCH_CHECK();
+    if (r0 == 0 && sp < splits)  // later strips accumulate into every split row
+      FK_CUDA(cudaMemsetAsync(acc + sp * m, 0, sizeof(double) * (size_t)(splits - sp) * m,
+                              ctx->stream));
+  }
+  return reduce_partials(ctx, acc, splits, m, u, nullptr);
 }
 
 }  // namespace falkon

@@ -1,0 +1,4 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:tc_kvp_kernel -s 2 -c 1 -o gpurun_out/se3_se python bench.py --config timit --quick --steps 1 --warmup 1 --single-eval 1 --n 120000 > gpurun_out/se3_ncu_se.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:tc_kvp_kernel -s 2 -c 1 -o gpurun_out/se3_tp python bench.py --config timit --quick --steps 1 --warmup 1 --single-eval 0 --n 120000 > gpurun_out/se3_ncu_tp.log 2>&1

@@ -45,7 +45,7 @@ def test_roofline_algorithmic_work():
     import argparse
     import bench
     import synth
-    args = argparse.Namespace(path="auto")
+    args = argparse.Namespace(path="auto", steps=1, single_eval=None)
     cfg = synth.CONFIGS["msd"]
     kt = {"pass_a": (10.0, 1), "pass_b": (9.0, 1)}
     r = bench.roofline(args, cfg, kt, 20.0, cfg.n, cfg.m, 148)
@@ -55,3 +55,24 @@ def test_roofline_algorithmic_work():
     r = bench.roofline(args, cfg, kt, 20.0, cfg.n, cfg.m, 148)
     assert r["bound"] == "alu" and r["unit"] == "G kernel-evals/s"
     assert abs(r["achieved"] - cfg.n * cfg.m / 10e-3 / 1e9) < 1e-9
+
+
+def test_roofline_single_evaluation_strips():
+    """TIMIT (d = 440) takes the single-evaluation product by default: pass A runs once per row
+    strip, so the per-launch work is n m / launches; the strip GEMV gets an HBM roofline at
+    4 B per entry."""
+    sys.path.insert(0, ROOT)
+    import argparse
+    import bench
+    import synth
+    cfg = synth.CONFIGS["timit"]
+    args = argparse.Namespace(path="auto", steps=2, single_eval=None)
+    assert bench.single_eval_active(args, cfg.d)
+    kt = {"pass_a": (520.0, 52), "pass_b": (140.0, 52)}  # 26 strips x 2 products
+    r = bench.roofline(args, cfg, kt, 700.0, cfg.n, cfg.m, 148)
+    assert r["kernel"] == "pass_a" and r["launches"] == 52
+    assert abs(r["achieved"] - 2 * cfg.d * cfg.n * cfg.m * 2 / 520e-3 / 1e12) < 1e-6
+    g = r["strip_gemv"]
+    assert g["bound"] == "hbm" and abs(g["achieved"] - 4 * cfg.n * cfg.m * 2 / 140e-3 / 1e9) < 1e-6
+    assert not bench.single_eval_active(argparse.Namespace(path="auto", single_eval=None),
+                                        synth.CONFIGS["msd"].d)
