@@ -236,6 +236,9 @@ def roofline(args, cfg, kt, ms_total, n_local, m, sms):
                                    "ms_per_product": kt["pass_b"][0] / args.steps}
         if tc_eval_peak <= mufu_eval_peak:
             ach_tf = 2.0 * d * ach_eval / 1e12
+            sus = peaks.get("bf16_tflops_sustained")
+            if sus:  # context only: the power-capped sustained rate (frac uses the burst peak)
+                extra["frac_vs_sustained_peak"] = ach_tf / (float(sus) / 3.0)
             return {"bound": "tensor", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": ach_tf / peak_tf,
                     "peak_source": f"{peak_src} bf16 dense {peaks['bf16_tflops']} TF/s / 3 "

@@ -854,10 +854,17 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
 #undef FK_TC
   if (stream) fn = mode == 11 ? tc_kvp_kernel<11, TC_N, false, true> : tc_kvp_kernel<0, TC_N, false, true>;
   // 2-CTA clusters with Q multicast (FALKON_OPT_TC_CLUSTER): MODE 0, SS, single vector
-  const int cl = (ctx->opt.tc_cluster == 2 && kv == 1 && !ts && (mode == 0 || kst)) ? 2 : 1;
-  if (cl == 2 && !kst)
-    fn = stream ? tc_kvp_kernel<0, TC_N, false, true, 8, 1, false, 2>
-                : tc_kvp_kernel<0, TC_N, false, false, 16, 1, false, 2>;
+  const int cl = (ctx->opt.tc_cluster == 2 && kv == 1 && !ts && epiw == 16 &&
+                  (mode <= 3 || kst)) || (ctx->opt.tc_cluster == 2 && kv == 1 && stream &&
+                                          (mode == 0 || kst))
+                     ? 2 : 1;
+  if (cl == 2 && !kst) {
+    if (stream) fn = tc_kvp_kernel<0, TC_N, false, true, 8, 1, false, 2>;
+    else if (mode == 1) fn = tc_kvp_kernel<1, TC_N, false, false, 16, 1, false, 2>;
+    else if (mode == 2) fn = tc_kvp_kernel<2, TC_N, false, false, 16, 1, false, 2>;
+    else if (mode == 3) fn = tc_kvp_kernel<3, TC_N, false, false, 16, 1, false, 2>;
+    else fn = tc_kvp_kernel<0, TC_N, false, false, 16, 1, false, 2>;
+  }
   if (kst) {  // single-evaluation strip (MODE 0; exp offload modes do not apply)
     if (cl == 2)
       fn = stream ? tc_kvp_kernel<0, TC_N, false, true, 8, 1, true, 2>
