@@ -216,8 +216,8 @@ def roofline(args, cfg, kt, ms_total, n_local, m, sms):
               "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)"}
     if kt_path_tensor(args, d):
         d16 = -(-(d + 2) // 16) * 16
-        if d16 > 192:  # streaming kernel: 64-aligned segments
-            d16 = -(-(d + 2) // 64) * 64
+        if d16 > 192:  # streaming kernel: 32-aligned segments
+            d16 = -(-(d + 2) // 32) * 32
         peak_tf = float(peaks["bf16_tflops"]) / 3.0
         ach_eval = evals / (dom_ms * 1e-3)
         tc_eval_peak = peak_tf * 1e12 / (2.0 * d)       # fp32-class cross term bound

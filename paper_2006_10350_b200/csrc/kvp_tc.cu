@@ -40,6 +40,7 @@ constexpr int TC_M = 128;
 constexpr int TC_N = 256;                         // Q rows per tile, shared-memory A (SS)
 constexpr int TC_N_TS = 192;                      // Q rows per tile, A in TMEM (TS)
 constexpr int TC_BK = 64;                          // fp16 per K box (128 B = one swizzle row)
+constexpr int TC_SBK = 32;  // streaming kernel: fp16 per K box (64 B rows, SWIZZLE_64B), 48 KB stages
 constexpr int TC_THREADS = 128 + 32 * 8;          // 4 control warps + 8 epilogue warps
 constexpr int TC_SMEM_MAX = 227 * 1024;
 constexpr int TC_A_BOX = TC_M * TC_BK * 2;         // 16 KB
@@ -53,10 +54,10 @@ int center_mean(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, double **
 
 static inline int tc_d16(int64_t d) { return (int)round_up<int64_t>(d + 2, 16); }
 // segment length of the packed [h | l] row: 16-aligned when the P tile stays resident in
-// shared memory (2 * d16 <= 384), else 64-aligned for the streaming kernel
+// shared memory (2 * d16 <= 384), else 32-aligned for the streaming kernel (32-wide K boxes)
 static inline bool tc_stream(int64_t d) { return tc_d16(d) > TC_MAX_D16; }
 static inline int tc_seg(int64_t d) {
-  return tc_stream(d) ? (int)round_up<int64_t>(d + 2, 64) : tc_d16(d);
+  return tc_stream(d) ? (int)round_up<int64_t>(d + 2, TC_SBK) : tc_d16(d);
 }
 // TS (A operand in TMEM) needs 2 accumulators of TC_N_TS columns + 16 columns per d16/16
 // chunk pair: 2*192 + 16*nk <= 512  <=>  d16 <= 128.
@@ -179,6 +180,16 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)(1024 >> 4) << 32;   // SBO
   d |= (uint64_t)1 << 46;             // descriptor version (sm_100)
   d |= (uint64_t)2 << 61;             // SWIZZLE_128B
+  return d;
+}
+// K-major SWIZZLE_64B descriptor (8-row groups of 64 B, SBO 512 B): streaming kernel
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;             // SWIZZLE_64B
   return d;
 }
 __device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
@@ -351,7 +362,10 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     tc_kvp_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                   TcArgs a) {
   static_assert(!(TS && STREAM), "TS needs the resident P tile");
-  constexpr int BBOX = STREAM ? 2 * (TC_A_BOX + NT * TC_BK * 2) : NT * TC_BK * 2;  // stage bytes
+  constexpr int SBK = STREAM ? TC_SBK : TC_BK;     // K width of the streamed boxes
+  constexpr int SA_BOX = TC_M * SBK * 2;             // streaming: one P box (8 KB)
+  constexpr int SQ_BOX = NT * SBK * 2;               // streaming: one Q box (16 KB)
+  constexpr int BBOX = STREAM ? 2 * (SA_BOX + SQ_BOX) : NT * TC_BK * 2;  // stage bytes
   constexpr int GRP = EPIW / 4;          // column groups (epilogue warps per TMEM lane group)
   constexpr int HALF = NT / GRP;         // columns per epilogue warp
   constexpr int NCH = HALF / 32;         // 32-column chunks per epilogue warp
@@ -427,18 +441,18 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
           } else if (STREAM) {
             uint8_t *st = sB + stage * BBOX;
             mbar_expect_tx(&full[stage], BBOX);
-            tma_load_2d(st, &tmP, b * TC_BK, (int)(a.p_base + p0), &full[stage]);        // h_p
-            tma_load_2d(st + TC_A_BOX, &tmP, segk + b * TC_BK, (int)(a.p_base + p0),
+            tma_load_2d(st, &tmP, b * SBK, (int)(a.p_base + p0), &full[stage]);          // h_p
+            tma_load_2d(st + SA_BOX, &tmP, segk + b * SBK, (int)(a.p_base + p0),
                         &full[stage]);  // l_p
             if (CL == 1) {
-              tma_load_2d(st + 2 * TC_A_BOX, &tmQ, b * TC_BK, q0, &full[stage]);         // h_q
-              tma_load_2d(st + 2 * TC_A_BOX + NT * TC_BK * 2, &tmQ, segk + b * TC_BK, q0,
+              tma_load_2d(st + 2 * SA_BOX, &tmQ, b * SBK, q0, &full[stage]);             // h_q
+              tma_load_2d(st + 2 * SA_BOX + SQ_BOX, &tmQ, segk + b * SBK, q0,
                           &full[stage]);                                                 // l_q
             } else {  // this CTA's 128-row half of h_q and l_q, multicast to the cluster
               const int qh = q0 + (int)crank * TC_M;
-              const uint32_t ho = crank * TC_A_BOX;
-              tma_load_2d_mc(st + 2 * TC_A_BOX + ho, &tmQ, b * TC_BK, qh, &full[stage], CMASK);
-              tma_load_2d_mc(st + 2 * TC_A_BOX + NT * TC_BK * 2 + ho, &tmQ, segk + b * TC_BK, qh,
+              const uint32_t ho = crank * SA_BOX;
+              tma_load_2d_mc(st + 2 * SA_BOX + ho, &tmQ, b * SBK, qh, &full[stage], CMASK);
+              tma_load_2d_mc(st + 2 * SA_BOX + SQ_BOX + ho, &tmQ, segk + b * SBK, qh,
                              &full[stage], CMASK);
             }
           } else {
@@ -462,7 +476,8 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     // descriptors are linear in the shared-memory address (start address in the low bits),
     // so chunk / stage offsets are plain integer adds on precomputed bases.
     const uint32_t idesc = (1u << 4) | ((uint32_t)(NT >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
-    const uint64_t a0 = sw128_desc(smem_u32(sA)), b0 = sw128_desc(smem_u32(sB));
+    const uint64_t a0 = sw128_desc(smem_u32(sA));
+    const uint64_t b0 = STREAM ? sw64_desc(smem_u32(sB)) : sw128_desc(smem_u32(sB));
     const int nk = a.nk;
     auto adesc = [&](int c) -> uint64_t {
       return a0 + (uint64_t)(((c >> 2) * TC_A_BOX + (c & 3) * 32) >> 4);
@@ -486,13 +501,13 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
         tc_fence_after();
         if (STREAM && elect_one()) {
           const uint64_t ah = b0 + (uint64_t)((stage * BBOX) >> 4);
-          const uint64_t al = ah + (uint64_t)(TC_A_BOX >> 4);
-          const uint64_t bh = ah + (uint64_t)((2 * TC_A_BOX) >> 4);
-          const uint64_t bl = bh + (uint64_t)((NT * TC_BK * 2) >> 4);
+          const uint64_t al = ah + (uint64_t)(SA_BOX >> 4);
+          const uint64_t bh = ah + (uint64_t)((2 * SA_BOX) >> 4);
+          const uint64_t bl = bh + (uint64_t)(SQ_BOX >> 4);
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            if (b * 4 + jj < nk && MODE != 10) {
-              const uint64_t o = (uint64_t)(jj * 2);  // +32 B within the 128 B swizzle row
+          for (int jj = 0; jj < SBK / 16; ++jj) {
+            if (b * (SBK / 16) + jj < nk && MODE != 10) {
+              const uint64_t o = (uint64_t)(jj * 2);  // +32 B within the 64 B swizzle row
               tc_mma_f16(dtm, ah + o, bh + o, idesc, (b | jj) ? 1u : 0u);  // h_p . h_q
               tc_mma_f16(dtm, al + o, bh + o, idesc, 1u);                  // l_p . h_q
               tc_mma_f16(dtm, ah + o, bl + o, idesc, 1u);                  // h_p . l_q
@@ -713,15 +728,17 @@ static PFN_encodeTiled_t get_encode() {
   return fn;
 }
 
-static int make_map(CUtensorMap *map, const __half *base, int64_t rows, int k_elems, int box_rows) {
+static int make_map(CUtensorMap *map, const __half *base, int64_t rows, int k_elems, int box_rows,
+                    bool stream = false) {
   PFN_encodeTiled_t enc = get_encode();
   if (!enc) return fail(FALKON_EUNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)k_elems, (cuuint64_t)std::max<int64_t>(rows, 1)};
   cuuint64_t strides[1] = {(cuuint64_t)k_elems * 2};
-  cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)(stream ? TC_SBK : TC_BK), (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void *)base, dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   stream ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FALKON_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return FALKON_OK;
@@ -758,11 +775,12 @@ int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const floa
   pp->xa = nullptr;
   pp->cb = nullptr;
   CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(pp->tmaps);
-  FK_TRY(make_map(&maps[0], (const __half *)xp, n, kp, TC_M));  // X as P (pass A)
-  const int nt = (!tc_stream(d) && tc_use_ts(d16)) ? TC_N_TS : TC_N;
-  FK_TRY(make_map(&maps[1], (const __half *)cp, m, kp, nt));  // C as Q (pass A)
-  FK_TRY(make_map(&maps[2], (const __half *)cp, m, kp, TC_M));  // C as P (pass B)
-  FK_TRY(make_map(&maps[3], (const __half *)xp, n, kp, nt));  // X as Q (pass B)
+  const bool st = tc_stream(d);
+  FK_TRY(make_map(&maps[0], (const __half *)xp, n, kp, TC_M, st));  // X as P (pass A)
+  const int nt = (!st && tc_use_ts(d16)) ? TC_N_TS : TC_N;
+  FK_TRY(make_map(&maps[1], (const __half *)cp, m, kp, nt, st));  // C as Q (pass A)
+  FK_TRY(make_map(&maps[2], (const __half *)cp, m, kp, TC_M, st));  // C as P (pass B)
+  FK_TRY(make_map(&maps[3], (const __half *)xp, n, kp, nt, st));  // X as Q (pass B)
   return FALKON_OK;
 }
 
@@ -817,15 +835,18 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
   const int d16 = pp.dq;
   const bool stream = tc_stream(pp.d);
   // resident: boxes of a whole packed row; streaming: boxes of one segment
-  const int nbox = stream ? d16 / TC_BK : (int)cdiv<int64_t>(2 * d16, TC_BK);
+  const int nbox = stream ? d16 / TC_SBK : (int)cdiv<int64_t>(2 * d16, TC_BK);
   const int64_t np = p_count >= 0 ? p_count : (passA ? pp.n : pp.m), nq = passA ? pp.m : pp.n;
   if (np <= 0) return FALKON_OK;
   if (kst && (!passA || kv != 1)) return fail(FALKON_EINVAL, "tc_launch: k strip needs pass A, kv 1");
   const bool ts = kv == 1 && !stream && tc_use_ts(d16);
   const int nt = ts ? TC_N_TS : TC_N;
-  const int stages = stream ? 2 : tc_stages(nbox, nt, kv);
-  const size_t smem = stream ? 1024 + (size_t)2 * 2 * (TC_A_BOX + TC_B_BOX) + 256 +
-                                   tc_tail_bytes(nt, kv, true)
+  // streaming: stages of 48 KB (P and Q boxes of both segments, 32 wide) — 4 fit
+  const size_t sstage = (size_t)2 * (TC_M + TC_N) * TC_SBK * 2;
+  int sst = TC_MAX_STAGES;
+  while (sst > 2 && 1024 + sst * sstage + 256 + tc_tail_bytes(nt, kv, true) > (size_t)TC_SMEM_MAX) --sst;
+  const int stages = stream ? sst : tc_stages(nbox, nt, kv);
+  const size_t smem = stream ? 1024 + (size_t)stages * sstage + 256 + tc_tail_bytes(nt, kv, true)
                              : tc_smem_bytes(nbox, stages, nt, kv);
   if (smem > (size_t)TC_SMEM_MAX) return fail(FALKON_EUNSUPPORTED, "tc_pass: shared memory");
   int mode = ctx->opt.exp_offload;

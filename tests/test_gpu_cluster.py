@@ -38,6 +38,7 @@ SHAPES = [
     (3001, 517, 28, 3.8),      # ragged, 24 x 5 tiles
     (129, 5, 33, 4.0),         # 2 x 1 tiles: pass B is one real CTA + its padding partner
     (700, 250, 440, 14.5),     # streaming-P kernel
+    (600, 200, 330, 12.0),     # streaming, 32-aligned segment (332 -> 352) ends mid-box pair
     (20000, 3000, 90, 7.0),    # several waves
 ]
 
