@@ -460,9 +460,10 @@ def main():
     # ---- one full Falkon fit (rows a1-a9) ----
     fit = None
     if not args.no_fit:
-        yh = torch.from_numpy(synth.gen_y(cfg.seed, X.cpu().numpy() if Xh is None else Xh.numpy(),
-                                          lo, cfg.task))
-        y = yh.cuda()
+        if Xh is None:  # device-generated X (TAXI-size): targets generated on the device too
+            y = synth.gen_y_torch(cfg.seed, X, lo, cfg.task)
+        else:
+            y = torch.from_numpy(synth.gen_y(cfg.seed, Xh.numpy(), lo, cfg.task)).cuda()
         alpha = torch.zeros(m, dtype=torch.float64, device="cuda")
         iters = args.fit_iters if args.fit_iters is not None else cfg.iters
         try:

@@ -239,3 +239,31 @@ def gen_X_torch(seed: int, row0: int, nrows: int, d: int, device="cuda", stream:
         out[s:s + r.numel()] = (torch.sqrt(-2.0 * torch.log(u1)) *
                                 torch.cos(2.0 * torch.pi * u2)).to(torch.float32)
     return out
+
+
+def _t_normals(seed: int, stream: int, index):
+    """Device version of _normals (same hash and Box-Muller, fp64)."""
+    import torch
+    key = (seed * 0x100000001B3 + stream * 0x5851F42D4C957F2D) & 0xFFFFFFFFFFFFFFFF
+    if key >= 1 << 63:
+        key -= 1 << 64
+    h = _t_splitmix64(_t_splitmix64(index ^ key))
+    u1 = (((h >> 32) & 0xFFFFFFFF).to(torch.float64) + 1.0) / 4294967296.0
+    u2 = (h & 0xFFFFFFFF).to(torch.float64) / 4294967296.0
+    return torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(2.0 * torch.pi * u2)
+
+
+def gen_y_torch(seed: int, X, row0: int, task: str = "reg", chunk_rows: int = 1 << 24):
+    """Device version of gen_y for a device-resident X (rows [row0, row0+len(X)))."""
+    import torch
+    n = X.shape[0]
+    k = min(3, X.shape[1])
+    y = torch.empty(n, dtype=torch.float32, device=X.device)
+    for s in range(0, n, chunk_rows):
+        e = min(n, s + chunk_rows)
+        r = torch.arange(row0 + s, row0 + e, dtype=torch.int64, device=X.device)
+        v = torch.sin(X[s:e, :k].to(torch.float64).sum(dim=1)) + 0.3 * _t_normals(seed, STREAM_NOISE, r)
+        if task == "cls":
+            v = torch.where(v >= 0.0, 1.0, -1.0)
+        y[s:e] = v.to(torch.float32)
+    return y

@@ -363,3 +363,13 @@ def test_synth_device_generator_matches_host():
     a = synth.gen_X(4, 987654321, 3000, 9)
     b = synth.gen_X_torch(4, 987654321, 3000, 9, device="cpu").numpy()
     assert np.array_equal(a, b)
+
+
+def test_device_target_generator_matches_host():
+    """synth.gen_y_torch (targets of device-generated X) reproduces synth.gen_y."""
+    import torch
+    X = synth.gen_X(4, 123456789, 5000, 9)
+    for task in ("reg", "cls"):
+        a = synth.gen_y(4, X, 123456789, task)
+        b = synth.gen_y_torch(4, torch.from_numpy(X), 123456789, task, chunk_rows=1500).numpy()
+        assert np.max(np.abs(a.astype(np.float64) - b)) <= 1e-6
