@@ -72,8 +72,10 @@ enum {
                                    2 = 1/4, 3 = 1/2 of the entries (rest on MUFU) */
   FALKON_OPT_POTRF_OUTER = 6,   /* blocked Cholesky: depth of the trailing fp64 GEMM updates in
                                    units of 128 columns (1..64, default 8) */
-  FALKON_OPT_GEMM_WARPS = 7,    /* fp64 DMMA GEMM CTA: 8 (128 x 128 tile, 8 warps), 16 (16 warps)
-                                   or 2 (128 x 64 tiles, 2 CTAs of 8 warps per SM) */
+  FALKON_OPT_GEMM_WARPS = 7,    /* fp64 DMMA GEMM CTA: 8 (128 x 128 tile, 8 warps), 16 (16 warps),
+                                   2 (128 x 64 tiles, 2 CTAs of 8 warps per SM) or 5 (default:
+                                   TMA-fed producer warp + 8 DMMA warps for the GEMMs whose A and B
+                                   are the same view, 2 elsewhere) */
   FALKON_OPT_SINGLE_EVAL = 8,   /* single-vector products on the tensor path: 0 = two passes (the
                                    cross term and exp evaluated twice), 1 = single evaluation:
                                    pass A also stores k(x_i, c_j) for a strip of rows in HBM and

@@ -498,8 +498,9 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
       ctx->opt.exp_offload = (int)value;
       return FALKON_OK;
     case FALKON_OPT_GEMM_WARPS:
-      if (value != 8 && value != 16 && value != 2)
-        return fail(FALKON_EINVAL, "gemm variant must be 8, 16 (warps, 1 CTA/SM) or 2 (2 CTAs/SM)");
+      if (value != 8 && value != 16 && value != 2 && value != 5)
+        return fail(FALKON_EINVAL, "gemm variant must be 8, 16 (warps, 1 CTA/SM), 2 (2 CTAs/SM) "
+                                   "or 5 (TMA-fed producer warp + 8 DMMA warps where A = B)");
       ctx->opt.gemm_warps = (int)value;
       return FALKON_OK;
     case FALKON_OPT_POTRF_OUTER:

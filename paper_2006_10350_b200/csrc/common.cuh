@@ -81,8 +81,10 @@ struct Options {
   int tc_terms = 3;
   int kernel_timing = 0;
   int exp_offload = 0;  // tensor path: share of exp2 evaluated on the FMA pipe (0..3)
-  int gemm_warps = 2;   // fp64 GEMM variant: 2 = 128 x 64 tiles, 2 CTAs/SM (measured m = 5e4:
-                        // 4.78 s vs 4.96 s for 8 = 128 x 128 tiles, 1 CTA/SM; 16 = 16 warps)
+  int gemm_warps = 5;   // fp64 GEMM variant: 5 = TMA-fed producer warp + 8 DMMA warps where
+                        // A and B are the same view (trailing updates, LAUUM; measured m = 5e4
+                        // 4.45 s, bitwise-identical factors), else 2; 2 = 128 x 64 tiles,
+                        // 2 CTAs/SM (4.76 s); 8 = 128 x 128 tiles, 1 CTA/SM (4.96 s); 16 warps
   int potrf_outer = 8;  // outer POTRF block in units of NB = 128 (trailing-update depth;
                         // measured m = 5e4: 2 -> 5.46 s, 4 -> 5.21 s, 8 -> 5.10 s)
   int single_eval = 2;  // 0 two-pass, 1 single evaluation (k strip through HBM), 2 auto

@@ -27,6 +27,8 @@
 
 #include <algorithm>
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace falkon {
@@ -355,14 +357,14 @@ __device__ __forceinline__ void gemm_async_chunk(const View &v, double (*s)[ROWS
 
 template <int TN>
 __device__ __noinline__ void gemm_epilogue(const GemmArgs a, const double *sC, int64_t i0,
-                                           int64_t j0) {
+                                           int64_t j0, int tid, int nthr) {
   constexpr int CLD = TN + 1;
   constexpr int BATCH = 8;  // independent reads in flight per thread
-  for (int e0 = threadIdx.x; e0 < GT * TN; e0 += BATCH * blockDim.x) {
+  for (int e0 = tid; e0 < GT * TN; e0 += BATCH * nthr) {
     double cv[BATCH];
 #pragma unroll
     for (int u = 0; u < BATCH; ++u) {
-      const int e = e0 + u * blockDim.x;
+      const int e = e0 + u * nthr;
       const int li_t = a.C.trans ? (e % GT) : (e / TN);
       const int lj_t = a.C.trans ? (e / GT) : (e % TN);
       const int64_t li = i0 + li_t, lj = j0 + lj_t;
@@ -373,7 +375,7 @@ __device__ __noinline__ void gemm_epilogue(const GemmArgs a, const double *sC, i
 #pragma unroll
     for (int u = 0; u < BATCH; ++u) {
       // storage order: consecutive threads walk the contiguous dimension of C's storage
-      const int e = e0 + u * blockDim.x;
+      const int e = e0 + u * nthr;
       const int li_t = a.C.trans ? (e % GT) : (e / TN);
       const int lj_t = a.C.trans ? (e / GT) : (e % TN);
       const int64_t li = i0 + li_t, lj = j0 + lj_t;
@@ -529,7 +531,242 @@ __global__ void __launch_bounds__(128 * WN, (WN == 2 && NT == 4) ? 2 : 1)
       for (int h = 0; h < 2; ++h)
         sC[(wr * 32 + mt * 8 + g) * CLD + wc * (8 * NT) + nt * 8 + 2 * q + h] = acc[mt][nt][h];
   __syncthreads();
-  gemm_epilogue<TN>(a, sC, i0, j0);
+  gemm_epilogue<TN>(a, sC, i0, j0, threadIdx.x, blockDim.x);
+}
+
+// ------------------------------------------------------------------ TMA-fed variant
+// For the big GEMMs (trailing updates, LAUUM: A and B are the same view of the m x m buffer):
+// 128 x 64 CTA tile, 8 compute warps of 32 x 32 and one producer warp, 1 CTA per SM, an
+// 8-stage ring of 24 KB k-chunks.  The producer loads each dense chunk operand with ONE 2-D
+// tensor-map TMA: a non-transposed view (k contiguous) as [rows][16 k] with SWIZZLE_128B
+// (conflict-free fragment loads), a transposed view (rows contiguous) as [16 k][rows]; chunks
+// touching the diagonal, masked parts or the k tail fall back to per-element cp.async in the
+// same layout.  Compute warps only wait on mbarriers, load fragments and issue DMMAs.  Same k
+// order per accumulator as gemm_f64_kernel: bitwise-identical results.
+constexpr int TM_TN = 64;
+constexpr int TM_STAGES = 8;
+constexpr int TM_A = GT * GK, TM_B = TM_TN * GK;  // doubles per chunk operand
+struct TmaMaps {
+  CUtensorMap a, b;
+};
+__device__ __forceinline__ void tma2d_g2s(void *dst, const CUtensorMap *map, int c0, int c1,
+                                          uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// byte offset of chunk element (r, k) in the stage layout
+template <int TRANS, int ROWS>
+__device__ __forceinline__ uint32_t tm_off(int r, int k) {
+  if (TRANS) return (uint32_t)(k * ROWS + r) * 8u;
+  return (uint32_t)(r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3));
+}
+template <int TRANS, int ROWS>
+__device__ __forceinline__ void tm_slow(const View &v, uint8_t *s, int64_t row0, int64_t rmax,
+                                        int64_t k, int64_t kmax, int lane) {
+  for (int e = lane; e < ROWS * GK; e += 32) {
+    const int rr = TRANS ? e % ROWS : e / GK, kk = TRANS ? e / ROWS : e % GK;
+    const int64_t r = row0 + rr, kg = k + kk;
+    bool ok = r < rmax && kg < kmax;
+    const double *src = ok ? vsrc(v, r, kg, ok) : v.base;
+    cp_async8z(s + tm_off<TRANS, ROWS>(rr, kk), src, ok);
+  }
+}
+
+template <int TRANS>
+__global__ void __launch_bounds__(288, 1)
+    gemm_f64_tma_kernel(const __grid_constant__ TmaMaps maps, GemmArgs a) {
+  constexpr int TN = TM_TN, NT = 4, WN = 2;
+  constexpr int R = GT / TN;
+  int64_t ti, tj;
+  if (a.tri_tiles) {
+    const int64_t t = blockIdx.x;
+    ti = (int64_t)((sqrt(8.0 * (double)t / R + 1.0) - 1.0) * 0.5);
+    while (R * (ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    while (R * ti * (ti + 1) / 2 > t) --ti;
+    tj = t - R * ti * (ti + 1) / 2;
+  } else {
+    ti = blockIdx.y;
+    tj = blockIdx.x;
+  }
+  const int64_t i0 = ti * GT, j0 = tj * TN;
+  if (i0 >= a.M || j0 >= a.N) return;
+  const int64_t kb = a.k_from_row ? lmax(a.k0, a.ra + i0) : a.k0;
+  const int64_t ke = a.k1;
+  const int nch = ke > kb ? (int)cdiv<int64_t>(ke - kb, GK) : 0;
+
+  extern __shared__ __align__(1024) uint8_t tsm_raw[];
+  uint8_t *tsm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int STAGE_B = (TM_A + TM_B) * 8;
+  uint64_t *full = reinterpret_cast<uint64_t *>(tsm + TM_STAGES * STAGE_B);
+  uint64_t *empty = full + TM_STAGES;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int st = 0; st < TM_STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ra = a.ra + i0, rb = a.rb + j0;
+  const int64_t ramax = a.ra + a.M, rbmax = a.rb + a.N;
+
+  if (warp == 8) {  // producer
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % TM_STAGES;
+      mbar_wait(&empty[st], ((c / TM_STAGES) & 1) ^ 1);
+      const int64_t kc = kb + (int64_t)c * GK;
+      uint8_t *sa = tsm + st * STAGE_B, *sb = sa + TM_A * 8;
+      const bool kfull = kc + GK <= ke;
+      const bool fa = kfull && view_dense(a.A, ra, GT, kc, GK);
+      const bool fb = kfull && view_dense(a.B, rb, TN, kc, GK);
+      if (!fa) tm_slow<TRANS, GT>(a.A, sa, ra, ramax, kc, ke, lane);
+      if (!fb) tm_slow<TRANS, TN>(a.B, sb, rb, rbmax, kc, ke, lane);
+      if (!(fa && fb)) asm volatile("cp.async.wait_all;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        mbar_expect_tx(&full[st], (fa ? TM_A * 8 : 0) + (fb ? TM_B * 8 : 0));
+        // TRANS: coords {row (inner), k}; else {k (inner), row}
+        if (fa) tma2d_g2s(sa, &maps.a, TRANS ? (int)ra : (int)kc, TRANS ? (int)kc : (int)ra, &full[st]);
+        if (fb) tma2d_g2s(sb, &maps.b, TRANS ? (int)rb : (int)kc, TRANS ? (int)kc : (int)rb, &full[st]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  const int wr = warp / WN, wc = warp % WN;
+  const int g = lane >> 2, q = lane & 3;
+  double acc[4][NT][2];
+  const bool cdense = view_dense(a.C, a.rc + i0, GT, a.cc + j0, TN) && i0 + GT <= a.M &&
+                      j0 + TN <= a.N;
+  const int64_t csr = a.C.trans ? 1 : a.C.ld, csc = a.C.trans ? a.C.ld : 1;
+  double *cfrag =
+      a.C.base + (a.rc + i0 + wr * 32 + g) * csr + (a.cc + j0 + wc * (8 * NT) + 2 * q) * csc;
+  if (cdense && a.beta != 0.0) {
+    const double sb = a.beta / a.alpha;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[mt][nt][h] = sb * cfrag[(mt * 8) * csr + (nt * 8 + h) * csc];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  }
+  for (int c = 0; c < nch; ++c) {
+    const int st = c % TM_STAGES;
+    mbar_wait(&full[st], (c / TM_STAGES) & 1);
+    const uint8_t *sa = tsm + st * STAGE_B, *sb = sa + TM_A * 8;
+    const int64_t kc = kb + (int64_t)c * GK;
+#pragma unroll
+    for (int ks = 0; ks < GK / 4; ++ks) {
+      const int kq = ks * 4 + q;
+      double af[4], bf[NT];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+        af[mt] = *reinterpret_cast<const double *>(sa + tm_off<TRANS, GT>(wr * 32 + mt * 8 + g, kq));
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        bf[nt] = *reinterpret_cast<const double *>(sb + tm_off<TRANS, TN>(wc * (8 * NT) + nt * 8 + g, kq));
+      if (a.kscale) {  // T D T^T of Alg. 2: B(j, k) D(k) on the fragment
+        const int64_t kk = kc + kq;
+        const double sc = kk < ke ? __ldg(a.kscale + kk) : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) bf[nt] *= sc;
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], af[mt], bf[nt]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  if (cdense) {
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          cfrag[(mt * 8) * csr + (nt * 8 + h) * csc] = a.alpha * acc[mt][nt][h];
+    return;
+  }
+  asm volatile("bar.sync 1, 256;" ::: "memory");  // all compute warps are past the ring
+  double *sC = reinterpret_cast<double *>(tsm);  // [GT][TN + 1]
+  constexpr int CLD = TN + 1;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        sC[(wr * 32 + mt * 8 + g) * CLD + wc * (8 * NT) + nt * 8 + 2 * q + h] = acc[mt][nt][h];
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  gemm_epilogue<TN>(a, sC, i0, j0, tid, 256);
+}
+
+typedef CUresult (*PFN_encodeTiled_p)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                      const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                      const cuuint32_t *, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+static PFN_encodeTiled_p encode_fn() {
+  static PFN_encodeTiled_p fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled_p)p;
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+// map of view v's storage (an ld x ld square of doubles) for chunks of `rows` x GK
+static bool tm_map(CUtensorMap *map, const View &v, int64_t extent, int rows) {
+  PFN_encodeTiled_p enc = encode_fn();
+  if (!enc || (v.ld & 1) || (reinterpret_cast<uintptr_t>(v.base) & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)v.ld, (cuuint64_t)extent};
+  cuuint64_t strides[1] = {(cuuint64_t)v.ld * 8};
+  cuuint32_t box[2] = {(cuuint32_t)(v.trans ? rows : GK), (cuuint32_t)(v.trans ? GK : rows)};
+  cuuint32_t es[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)v.base, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             v.trans ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// true if launched (A and B the same square view with even ld), false: use the generic kernel
+static bool gemm_launch_tma(falkon_ctx *ctx, const GemmArgs &a, int *rc) {
+  *rc = FALKON_OK;
+  if (a.A.base != a.B.base || a.A.trans != a.B.trans || a.A.ld != a.B.ld) return false;
+  TmaMaps maps;
+  if (!tm_map(&maps.a, a.A, a.A.ld, GT) || !tm_map(&maps.b, a.B, a.B.ld, TM_TN)) return false;
+  constexpr int TN = TM_TN, R = GT / TN;
+  const size_t smem = 1024 + (size_t)TM_STAGES * (TM_A + TM_B) * 8 + 16 * TM_STAGES;
+  auto fn = a.A.trans ? gemm_f64_tma_kernel<1> : gemm_f64_tma_kernel<0>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    *rc = fail(FALKON_ECUDA, "gemm_f64_tma_kernel smem attribute");
+    return true;
+  }
+  const int64_t tm = cdiv<int64_t>(a.M, GT), tn = cdiv<int64_t>(a.N, TN);
+  LaunchScope ls(ctx, FALKON_T_PRECOND);
+  if (a.tri_tiles)
+    fn<<<(unsigned)(R * tm * (tm + 1) / 2), 288, smem, ctx->stream>>>(maps, a);
+  else
+    fn<<<dim3((unsigned)tn, (unsigned)tm), 288, smem, ctx->stream>>>(maps, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) *rc = fail(FALKON_ECUDA, std::string("gemm_f64_tma_kernel: ") + cudaGetErrorString(e));
+  return true;
 }
 
 template <int WN, int NT>
@@ -551,6 +788,10 @@ static int gemm_launch(falkon_ctx *ctx, const GemmArgs &a) {
 
 static int gemm(falkon_ctx *ctx, const GemmArgs &a) {
   if (a.M <= 0 || a.N <= 0) return FALKON_OK;
+  if (ctx->opt.gemm_warps == 5) {  // TMA-fed warp-specialised kernel where it applies
+    int rc;
+    if (gemm_launch_tma(ctx, a, &rc)) return rc;
+  }
   switch (ctx->opt.gemm_warps) {
     case 16: return gemm_launch<4, 4>(ctx, a);
     case 2: return gemm_launch<2, 4>(ctx, a);  // 2 CTAs of 8 warps per SM
