@@ -545,7 +545,11 @@ __global__ void __launch_bounds__(128 * WN, (WN == 2 && NT == 4) ? 2 : 1)
 // order per accumulator as gemm_f64_kernel: bitwise-identical results.
 constexpr int TM_TN = 64;
 constexpr int TM_STAGES = 8;
-constexpr int TM_A = GT * GK, TM_B = TM_TN * GK;  // doubles per chunk operand
+// doubles per chunk operand: [rows][16 k] swizzled, or [16 k][rows + 4] for a transposed view
+// (the TMA box is 4 elements wider than the tile, so the rows land padded — the same
+// conflict-free fragment layout as gemm_f64_kernel; the 4 extra values are never read)
+template <int TRANS, int ROWS>
+constexpr int tm_elems() { return TRANS ? GK * (ROWS + GPAD) : ROWS * GK; }
 struct TmaMaps {
   CUtensorMap a, b;
 };
@@ -560,7 +564,7 @@ __device__ __forceinline__ void tma2d_g2s(void *dst, const CUtensorMap *map, int
 // byte offset of chunk element (r, k) in the stage layout
 template <int TRANS, int ROWS>
 __device__ __forceinline__ uint32_t tm_off(int r, int k) {
-  if (TRANS) return (uint32_t)(k * ROWS + r) * 8u;
+  if (TRANS) return (uint32_t)(k * (ROWS + GPAD) + r) * 8u;
   return (uint32_t)(r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3));
 }
 template <int TRANS, int ROWS>
@@ -599,6 +603,7 @@ __global__ void __launch_bounds__(288, 1)
 
   extern __shared__ __align__(1024) uint8_t tsm_raw[];
   uint8_t *tsm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int TM_A = tm_elems<TRANS, GT>(), TM_B = tm_elems<TRANS, TM_TN>();
   constexpr int STAGE_B = (TM_A + TM_B) * 8;
   uint64_t *full = reinterpret_cast<uint64_t *>(tsm + TM_STAGES * STAGE_B);
   uint64_t *empty = full + TM_STAGES;
@@ -738,7 +743,7 @@ static bool tm_map(CUtensorMap *map, const View &v, int64_t extent, int rows) {
   if (!enc || (v.ld & 1) || (reinterpret_cast<uintptr_t>(v.base) & 15)) return false;
   cuuint64_t dims[2] = {(cuuint64_t)v.ld, (cuuint64_t)extent};
   cuuint64_t strides[1] = {(cuuint64_t)v.ld * 8};
-  cuuint32_t box[2] = {(cuuint32_t)(v.trans ? rows : GK), (cuuint32_t)(v.trans ? GK : rows)};
+  cuuint32_t box[2] = {(cuuint32_t)(v.trans ? rows + GPAD : GK), (cuuint32_t)(v.trans ? GK : rows)};
   cuuint32_t es[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)v.base, dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -752,7 +757,10 @@ static bool gemm_launch_tma(falkon_ctx *ctx, const GemmArgs &a, int *rc) {
   TmaMaps maps;
   if (!tm_map(&maps.a, a.A, a.A.ld, GT) || !tm_map(&maps.b, a.B, a.B.ld, TM_TN)) return false;
   constexpr int TN = TM_TN, R = GT / TN;
-  const size_t smem = 1024 + (size_t)TM_STAGES * (TM_A + TM_B) * 8 + 16 * TM_STAGES;
+  const size_t smem = 1024 + (size_t)TM_STAGES * 8 *
+                                 (a.A.trans ? tm_elems<1, GT>() + tm_elems<1, TM_TN>()
+                                            : tm_elems<0, GT>() + tm_elems<0, TM_TN>()) +
+                      16 * TM_STAGES;
   auto fn = a.A.trans ? gemm_f64_tma_kernel<1> : gemm_f64_tma_kernel<0>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     *rc = fail(FALKON_ECUDA, "gemm_f64_tma_kernel smem attribute");
