@@ -111,6 +111,10 @@ struct falkon_ctx {
   double t_ms[FALKON_T_COUNT] = {};
   int64_t t_launches[FALKON_T_COUNT] = {};
   int64_t launches = 0;
+  // co-resident CTAs of cluster launches, per kernel (kvp_tc.cu tc_cluster_slots)
+  static constexpr int NSLOTCACHE = 8;
+  const void *slot_fn[NSLOTCACHE] = {};
+  int64_t slot_n[NSLOTCACHE] = {};
 };
 
 namespace falkon {

@@ -715,16 +715,15 @@ typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint
                                       CUtensorMapFloatOOBfill);
 
 static PFN_encodeTiled_t get_encode() {
-  static PFN_encodeTiled_t fn = nullptr;
-  if (!fn) {
+  static const PFN_encodeTiled_t fn = []() -> PFN_encodeTiled_t {  // thread-safe one-time lookup
     void *p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = (PFN_encodeTiled_t)p;
-    else
-      cudaGetLastError();
-  }
+      return (PFN_encodeTiled_t)p;
+    cudaGetLastError();
+    return nullptr;
+  }();
   return fn;
 }
 
@@ -802,9 +801,8 @@ static int tc_stages(int nbox, int nt, int kv = 1) {
 // Co-resident CTAs of a 2-CTA-cluster launch (2 x cudaOccupancyMaxActiveClusters; a GPC with
 // an odd number of free SMs leaves one idle), cached per kernel.
 static int64_t tc_cluster_slots(falkon_ctx *ctx, const void *fn, int threads, size_t smem) {
-  static const void *last_fn = nullptr;
-  static int64_t last = 0;
-  if (fn == last_fn && last > 0) return last;
+  for (int i = 0; i < falkon_ctx::NSLOTCACHE; ++i)  // per-context cache (contexts are independent)
+    if (ctx->slot_fn[i] == fn && ctx->slot_n[i] > 0) return ctx->slot_n[i];
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * ctx->sm_count);
   cfg.blockDim = dim3((unsigned)threads);
@@ -821,9 +819,14 @@ static int64_t tc_cluster_slots(falkon_ctx *ctx, const void *fn, int threads, si
     cudaGetLastError();
     return ctx->sm_count;
   }
-  last_fn = fn;
-  last = 2 * (int64_t)nc;
-  return last;
+  const int64_t slots = 2 * (int64_t)nc;
+  for (int i = 0; i < falkon_ctx::NSLOTCACHE; ++i)
+    if (!ctx->slot_fn[i]) {
+      ctx->slot_fn[i] = fn;
+      ctx->slot_n[i] = slots;
+      break;
+    }
+  return slots;
 }
 
 // One fused pass over P rows [p_begin, p_begin + p_count) (p_count < 0: all).  kst != null

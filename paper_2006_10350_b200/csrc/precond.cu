@@ -725,16 +725,15 @@ typedef CUresult (*PFN_encodeTiled_p)(CUtensorMap *, CUtensorMapDataType, cuuint
                                       CUtensorMapSwizzle, CUtensorMapL2promotion,
                                       CUtensorMapFloatOOBfill);
 static PFN_encodeTiled_p encode_fn() {
-  static PFN_encodeTiled_p fn = nullptr;
-  if (!fn) {
+  static const PFN_encodeTiled_p fn = []() -> PFN_encodeTiled_p {  // thread-safe one-time lookup
     void *p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = (PFN_encodeTiled_p)p;
-    else
-      cudaGetLastError();
-  }
+      return (PFN_encodeTiled_p)p;
+    cudaGetLastError();
+    return nullptr;
+  }();
   return fn;
 }
 // map of view v's storage (an ld x ld square of doubles) for chunks of `rows` x GK
