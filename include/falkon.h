@@ -84,9 +84,12 @@ enum {
                                    cross term costs more than the 8 B/entry strip round trip) */
   FALKON_OPT_STRIP_BYTES = 9,   /* single evaluation: device bytes of the k strip (default 16 GiB,
                                    minimum 64 MiB; rows per strip = bytes / (4 m)) */
-  FALKON_OPT_TC_CLUSTER = 10    /* tensor path: 1 = one CTA per P tile; 2 = clusters of two CTAs on
+  FALKON_OPT_TC_CLUSTER = 10,   /* tensor path: 1 = one CTA per P tile; 2 = clusters of two CTAs on
                                    consecutive P tiles, each loading half of every streamed Q box
                                    and multicasting it to both (halves the L2 -> SM traffic) */
+  FALKON_OPT_LOOKAHEAD = 11     /* blocked Cholesky: 1 (default) = the next outer panel's
+                                   factorisation runs on a high-priority stream while the bulk of
+                                   the trailing update runs on a low-priority one; 0 = serial */
 };
 
 /* Per-launch-class accumulated device times in ms (falkon_ctx_timings). */

@@ -23,7 +23,7 @@ KERNELS = {"gaussian": GAUSSIAN, "laplacian": LAPLACIAN}
 PATH_AUTO, PATH_SIMT, PATH_TENSOR = 0, 1, 2
 OPT_PATH, OPT_TC_MIN_D, OPT_TC_TERMS, OPT_KERNEL_TIMING, OPT_EXP_OFFLOAD = 1, 2, 3, 4, 5
 OPT_POTRF_OUTER, OPT_GEMM_WARPS = 6, 7
-OPT_SINGLE_EVAL, OPT_STRIP_BYTES, OPT_TC_CLUSTER = 8, 9, 10
+OPT_SINGLE_EVAL, OPT_STRIP_BYTES, OPT_TC_CLUSTER, OPT_LOOKAHEAD = 8, 9, 10, 11
 SINGLE_EVAL_OFF, SINGLE_EVAL_ON, SINGLE_EVAL_AUTO = 0, 1, 2
 TIMING_NAMES = ["prep", "pass_a", "pass_b", "reduce", "allreduce", "precond", "trsv", "vec"]
 

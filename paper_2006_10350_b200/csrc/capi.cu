@@ -464,6 +464,8 @@ int falkon_ctx_destroy(falkon_ctx *ctx) {
     cudaEventDestroy(e.start);
     cudaEventDestroy(e.stop);
   }
+  if (ctx->hi_stream) cudaStreamDestroy(ctx->hi_stream);
+  if (ctx->lo_stream) cudaStreamDestroy(ctx->lo_stream);
   cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return FALKON_OK;
@@ -514,6 +516,9 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
     case FALKON_OPT_STRIP_BYTES:
       if (value < ((int64_t)64 << 20)) return fail(FALKON_EINVAL, "strip bytes must be >= 64 MiB");
       ctx->opt.strip_bytes = value;
+      return FALKON_OK;
+    case FALKON_OPT_LOOKAHEAD:
+      ctx->opt.lookahead = value ? 1 : 0;
       return FALKON_OK;
     case FALKON_OPT_TC_CLUSTER:
       if (value != 1 && value != 2) return fail(FALKON_EINVAL, "tc_cluster must be 1 or 2");

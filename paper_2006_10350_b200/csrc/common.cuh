@@ -87,6 +87,7 @@ struct Options {
                         // 2 CTAs/SM (4.76 s); 8 = 128 x 128 tiles, 1 CTA/SM (4.96 s); 16 warps
   int potrf_outer = 8;  // outer POTRF block in units of NB = 128 (trailing-update depth;
                         // measured m = 5e4: 2 -> 5.46 s, 4 -> 5.21 s, 8 -> 5.10 s)
+  int lookahead = 1;    // blocked Cholesky: overlap the next panel with the trailing update
   int single_eval = 2;  // 0 two-pass, 1 single evaluation (k strip through HBM), 2 auto
   int tc_cluster = 2;   // tensor path: clusters of 2 CTAs multicasting the Q boxes (measured
                         // MSD 21.7 -> 20.9 ms, TIMIT 431 -> 424 ms), or 1 CTA
@@ -111,6 +112,9 @@ struct falkon_ctx {
   double t_ms[FALKON_T_COUNT] = {};
   int64_t t_launches[FALKON_T_COUNT] = {};
   int64_t launches = 0;
+  // blocked Cholesky lookahead (precond.cu): high-priority stream for the panel chain, low
+  // priority for the bulk trailing update; created on first use
+  cudaStream_t hi_stream = nullptr, lo_stream = nullptr;
   // co-resident CTAs of cluster launches, per kernel (kvp_tc.cu tc_cluster_slots)
   static constexpr int NSLOTCACHE = 8;
   const void *slot_fn[NSLOTCACHE] = {};

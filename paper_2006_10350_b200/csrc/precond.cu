@@ -29,6 +29,8 @@
 
 #include <cuda.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace falkon {
@@ -807,6 +809,142 @@ static int gemm(falkon_ctx *ctx, const GemmArgs &a) {
 }
 
 // ------------------------------------------------------------------ blocked Cholesky
+// Inner steps of one outer panel [K0, K1): per 128-column block, the diagonal factor + inverse,
+// the panel solve (GEMM with W = L_kk^-1) and the update of the rest of the outer panel.
+static int potrf_panel(falkon_ctx *ctx, View S, int64_t m, int64_t K0, int64_t K1, double *Wbuf,
+                       double *Dinv, unsigned long long *fail, size_t dsm) {
+  View W{Wbuf, NB, 0, 0, nullptr};
+  for (int64_t k0 = K0; k0 < K1; k0 += NB) {
+    const int nb = (int)std::min<int64_t>(NB, m - k0);
+    {
+      LaunchScope ls(ctx, FALKON_T_PRECOND);
+      potrf_diag_kernel<<<1, 512, dsm, ctx->stream>>>(S, k0, nb, Wbuf, Dinv, fail);
+    }
+    FK_LAUNCH_CHECK();
+    const int64_t k1 = k0 + nb, rem = m - k1;
+    if (rem <= 0) break;
+    GemmArgs p{};
+    p.A = S;
+    p.B = W;
+    p.C = S;
+    p.M = rem;
+    p.N = nb;
+    p.ra = k1;
+    p.rb = 0;
+    p.rc = k1;
+    p.cc = k0;
+    p.k0 = k0;
+    p.k1 = k1;
+    p.B.base = Wbuf - k0;
+    p.alpha = 1.0;
+    p.beta = 0.0;
+    FK_TRY(gemm(ctx, p));
+    if (k1 < K1) {
+      GemmArgs u{};
+      u.A = S;
+      u.B = S;
+      u.C = S;
+      u.M = rem;
+      u.N = K1 - k1;
+      u.ra = k1;
+      u.rb = k1;
+      u.rc = k1;
+      u.cc = k1;
+      u.k0 = k0;
+      u.k1 = k1;
+      u.alpha = -1.0;
+      u.beta = 1.0;
+      FK_TRY(gemm(ctx, u));
+    }
+  }
+  return FALKON_OK;
+}
+
+// S(c0:, c0:c1) -= L(c0:, K0:K1) L(c0:c1, K0:K1)^T restricted to the lower triangle: columns
+// [c0, c1) of the trailing matrix (c1 = m with tri tiles for the whole rest).
+static int potrf_update(falkon_ctx *ctx, View S, int64_t m, int64_t K0, int64_t K1, int64_t c0,
+                        int64_t c1) {
+  if (c0 >= c1) return FALKON_OK;
+  GemmArgs t{};
+  t.A = S;
+  t.B = S;
+  t.C = S;
+  t.M = m - c0;
+  t.N = c1 - c0;
+  t.ra = c0;
+  t.rb = c0;
+  t.rc = c0;
+  t.cc = c0;
+  t.k0 = K0;
+  t.k1 = K1;
+  t.tri_tiles = c1 == m ? 1 : 0;
+  t.alpha = -1.0;
+  t.beta = 1.0;
+  return gemm(ctx, t);
+}
+
+// Lookahead (the classic right-looking schedule with depth 1): after outer panel j, the update
+// of the NEXT panel's columns (a_j) runs on the high-priority stream right away and panel j+1
+// is factored there, while the bulk of the trailing update (b_j, columns beyond panel j+1) runs
+// on the low-priority stream.  Ordering: b_j waits for panel j (event P_j); a_j waits for
+// b_{j-1} (both write panel j+1's columns); panel j+1 follows a_j on the same stream and
+// b_{j-1} covered its columns' older updates.  The diagonal-block factorisations and small
+// panel GEMMs (latency-bound, a few SMs) thus hide under the big GEMM.
+static int potrf_lookahead(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, double *Dinv,
+                           unsigned long long *failw) {
+  const size_t dsm = sizeof(double) * NB * (NB + 1);
+  FK_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)dsm));
+  if (!ctx->hi_stream) {
+    int least = 0, greatest = 0;
+    FK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    FK_CUDA(cudaStreamCreateWithPriority(&ctx->hi_stream, cudaStreamNonBlocking, greatest));
+    FK_CUDA(cudaStreamCreateWithPriority(&ctx->lo_stream, cudaStreamNonBlocking, least));
+  }
+  const int NBO = NB * ctx->opt.potrf_outer;
+  const int64_t nob = cdiv<int64_t>(m, NBO);
+  std::vector<cudaEvent_t> ev((size_t)(2 * nob + 2));
+  for (auto &e : ev) FK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t *evP = ev.data(), *evB = ev.data() + nob, *evFork = ev.data() + 2 * nob,
+              *evEnd = evFork + 1;
+  cudaStream_t base = ctx->stream, hi = ctx->hi_stream, lo = ctx->lo_stream;
+  int rc = FALKON_OK;
+  auto on = [&](cudaStream_t s) { ctx->stream = s; };
+  do {
+    if (cudaEventRecord(*evFork, base) != cudaSuccess) {
+      rc = fail(FALKON_ECUDA, "cudaEventRecord (potrf fork)");
+      break;
+    }
+    cudaStreamWaitEvent(hi, *evFork, 0);
+    cudaStreamWaitEvent(lo, *evFork, 0);
+    for (int64_t j = 0; j < nob; ++j) {
+      const int64_t K0 = j * NBO, K1 = std::min<int64_t>(K0 + NBO, m);
+      const int64_t K2 = std::min<int64_t>(K1 + NBO, m);
+      on(hi);
+      if ((rc = potrf_panel(ctx, S, m, K0, K1, Wbuf, Dinv, failw, dsm))) break;
+      if (K1 >= m) break;
+      cudaEventRecord(evP[j], hi);
+      if (j > 0) cudaStreamWaitEvent(hi, evB[j - 1], 0);
+      if ((rc = potrf_update(ctx, S, m, K0, K1, K1, K2))) break;  // a_j: next panel's columns
+      if (K2 < m) {
+        on(lo);
+        cudaStreamWaitEvent(lo, evP[j], 0);
+        if ((rc = potrf_update(ctx, S, m, K0, K1, K2, m))) break;  // b_j: the rest
+      }
+      cudaEventRecord(evB[j], lo);
+    }
+    // join both streams back into the caller's stream
+    cudaEventRecord(*evEnd, hi);
+    cudaStreamWaitEvent(base, *evEnd, 0);
+    cudaEventRecord(*evEnd, lo);
+    cudaStreamWaitEvent(base, *evEnd, 0);
+  } while (0);
+  ctx->stream = base;
+  for (auto &e : ev) cudaEventDestroy(e);
+  if (rc == FALKON_OK) FK_LAUNCH_CHECK();
+  return rc;
+}
+
 static int potrf(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, double *Dinv,
                  unsigned long long *fail) {
   const size_t dsm = sizeof(double) * NB * (NB + 1);
@@ -819,6 +957,7 @@ static int potrf(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, double *Dinv,
   // fewer passes
   // over the trailing matrix and doubles the GEMM depth per tile).
   const int NBO = NB * ctx->opt.potrf_outer;
+  if (ctx->opt.lookahead && m > 2 * (int64_t)NBO) return potrf_lookahead(ctx, S, m, Wbuf, Dinv, fail);
   for (int64_t K0 = 0; K0 < m; K0 += NBO) {
     const int64_t K1 = std::min<int64_t>(K0 + NBO, m);
     for (int64_t k0 = K0; k0 < K1; k0 += NB) {

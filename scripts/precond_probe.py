@@ -40,7 +40,9 @@ out["fp16_mm_8192_tflops"] = rate(lambda: a16 @ a16, 2.0 * N ** 3)[0]
 ctx = binding.Context(0)
 import itertools
 REF = {}
-for warps, outer in itertools.product([int(x) for x in os.environ.get("PROBE_WARPS", "8").split(",")],
+for la in [int(x) for x in os.environ.get("PROBE_LOOKAHEAD", "1").split(",")]:
+ ctx.set_option(binding.OPT_LOOKAHEAD, la)
+ for warps, outer in itertools.product([int(x) for x in os.environ.get("PROBE_WARPS", "8").split(",")],
                                       [int(x) for x in os.environ.get("PROBE_OUTER", "8").split(",")]):
   ctx.set_option(binding.OPT_POTRF_OUTER, outer)
   ctx.set_option(binding.OPT_GEMM_WARPS, warps)
@@ -58,15 +60,15 @@ for warps, outer in itertools.product([int(x) for x in os.environ.get("PROBE_WAR
     ctx.precond_build(C, 0, cfg.sigma, cfg.lam, 1e-8, P, dT, dA, W)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    out[f"precond_w{warps}_o{outer}_m{m}_s"] = dt
+    out[f"precond_la{la}_w{warps}_o{outer}_m{m}_s"] = dt
     key = ("ref", m)
     if key not in REF:
         REF[key] = (P.clone(), dT.clone(), dA.clone())
     else:
         Pr, dTr, dAr = REF[key]
-        out[f"precond_w{warps}_o{outer}_m{m}_maxdiff"] = max(
+        out[f"precond_la{la}_w{warps}_o{outer}_m{m}_maxdiff"] = max(
             float((P - Pr).abs().max()), float((dT - dTr).abs().max()), float((dA - dAr).abs().max()))
-    out[f"precond_w{warps}_o{outer}_m{m}_tflops_m3"] = m ** 3 / dt / 1e12
+    out[f"precond_la{la}_w{warps}_o{outer}_m{m}_tflops_m3"] = m ** 3 / dt / 1e12
     del P, W
     torch.cuda.empty_cache()
 print(json.dumps(out), flush=True)
