@@ -167,3 +167,34 @@ def test_triangular_solves_multi_column(ctx, m, k):
             ctx.precond_solve_multi(P, dT, dA, W, which, trans, Xd)
             ref = sla.solve_triangular(F, B.T, lower=False, trans="T" if trans else "N")
             assert rel_l2(host(Xd).T, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("m,d", [(3000, 28), (2999, 9), (4352, 90)])
+def test_preconditioner_schedules_agree(lib, m, d):
+    """The GEMM variants (TMA-fed producer-warp kernel 5 / cp.async kernel 2) and the
+    lookahead schedule (next panel on a high-priority stream, bulk trailing update on a
+    low-priority one) compute every factor entry with the same k order, so for a given outer
+    blocking the factors are bitwise identical; every schedule matches the oracle at fp64
+    level.  m = 2999: odd ld (no TMA maps, fallback); outer block 1 x 128 makes the lookahead
+    run over many panels (a different blocking: a different fp64 summation association)."""
+    from paper_2006_10350_b200 import binding
+    C = synth.gen_X(m + 7, 0, m, d)
+    To, Ao = oracle.preconditioner(C, G, 3.0, 1e-6, 1e-8)
+    ref = {}
+    for gemm_v, la, outer in [(2, 0, 8), (5, 0, 8), (5, 1, 8), (2, 0, 1), (5, 1, 1), (2, 1, 1)]:
+        c = binding.Context(0)
+        try:
+            c.set_option(binding.OPT_GEMM_WARPS, gemm_v)
+            c.set_option(binding.OPT_LOOKAHEAD, la)
+            c.set_option(binding.OPT_POTRF_OUTER, outer)
+            T, A, _, info = _build(c, C, G, 3.0, 1e-6, 1e-8)
+        finally:
+            c.close()
+        assert info["failed_factor"] == -1
+        assert np.max(np.abs(T - To)) <= 1e-9 * max(1.0, np.max(np.abs(To)))
+        assert np.max(np.abs(A - Ao)) <= 1e-8 * max(1.0, np.max(np.abs(Ao)))
+        if outer in ref:
+            assert np.array_equal(T, ref[outer][0]) and np.array_equal(A, ref[outer][1]), \
+                (gemm_v, la, outer)
+        else:
+            ref[outer] = (T, A)
