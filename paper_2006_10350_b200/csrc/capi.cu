@@ -222,8 +222,8 @@ static int product(falkon_ctx *ctx, Fit &F, const double *v, double *u,
                    const float *dw = nullptr) {
   const int64_t m = F.pp.m;
   FK_TRY(f64_to_f32(ctx, v, F.v32, m, round_up<int64_t>(m, 128)));
-  if (!dw && F.pp.n > 0 && tc_single_eval(ctx, F.pp)) {  // NEXT-4: one evaluation per entry
-    FK_TRY(tc_product_single_eval(ctx, F.pp, F.v32, F.w32, u));
+  if (F.pp.n > 0 && tc_single_eval(ctx, F.pp)) {  // NEXT-4: one evaluation per entry
+    FK_TRY(tc_product_single_eval(ctx, F.pp, F.v32, F.w32, u, dw));
     return nccl_allreduce_f64(ctx, u, m);
   }
   FK_TRY(pass_A(ctx, F.pp, F.v32, nullptr, F.w32));
@@ -465,6 +465,7 @@ int falkon_ctx_destroy(falkon_ctx *ctx) {
     cudaEventDestroy(e.stop);
   }
   if (ctx->hi_stream) cudaStreamDestroy(ctx->hi_stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->lo_stream) cudaStreamDestroy(ctx->lo_stream);
   cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -555,11 +556,83 @@ static int matvec_common(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, 
   return alloc_fit_vectors(ctx, F);
 }
 
+// Host X on the two-pass tensor path: the rows go up in chunks on a copy stream, and each
+// chunk is packed and run through pass A as soon as it lands, so the H2D transfer overlaps the
+// product (pass B needs every w, so it follows the last chunk).  Same packing and tiles as the
+// staged path; a chunk's pass A may split the centres differently, so w can differ in the fp64
+// order of the per-split partials (relative 1e-16 level).
+static int matvec_host_pipelined(falkon_ctx *ctx, const float *X, int64_t n, int64_t d,
+                                 const float *C, int64_t m, int kernel, double sigma, Fit &F,
+                                 const double *vd, double *ud) {
+  const void *Cd;
+  FK_TRY(stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd));
+  FK_TRY(prepare_operands(ctx, nullptr, n, d, (const float *)Cd, m, kernel, sigma, &F.pp));
+  FK_TRY(alloc_fit_vectors(ctx, F));
+  void *xs;
+  FK_TRY(ws_get(ctx, WS_STAGE_X, sizeof(float) * n * d, &xs));
+  if (!ctx->copy_stream)
+    FK_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  FK_TRY(f64_to_f32(ctx, vd, F.v32, m, round_up<int64_t>(m, 128)));
+  const int nchunk = 8;
+  const int64_t rows = round_up<int64_t>(cdiv<int64_t>(n, nchunk), 128);
+  cudaEvent_t ev[nchunk + 1];
+  for (auto &e : ev) FK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  int rc = FALKON_OK;
+  // the copies may only start once the staging buffer is free (prior work on ctx->stream)
+  cudaEventRecord(ev[nchunk], ctx->stream);
+  cudaStreamWaitEvent(ctx->copy_stream, ev[nchunk], 0);
+  int c = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += rows, ++c) {
+    const int64_t nr = std::min<int64_t>(rows, n - r0);
+    float *dst = (float *)xs + r0 * d;
+    if (cudaMemcpyAsync(dst, X + r0 * d, sizeof(float) * nr * d, cudaMemcpyHostToDevice,
+                        ctx->copy_stream) != cudaSuccess) {
+      rc = fail(FALKON_ECUDA, "cudaMemcpyAsync (host X chunk)");
+      break;
+    }
+    cudaEventRecord(ev[c], ctx->copy_stream);
+  }
+  c = 0;
+  for (int64_t r0 = 0; rc == FALKON_OK && r0 < n; r0 += rows, ++c) {
+    const int64_t nr = std::min<int64_t>(rows, n - r0);
+    cudaStreamWaitEvent(ctx->stream, ev[c], 0);
+    if ((rc = tc_pack_rows(ctx, F.pp, (const float *)xs + r0 * d, r0, nr))) break;
+    if ((rc = tc_pass_A_rows(ctx, F.pp, F.v32, F.w32, r0, nr))) break;
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  FK_TRY(rc);
+  FK_TRY(pass_B(ctx, F.pp, F.w32, ud));
+  return nccl_allreduce_f64(ctx, ud, m);
+}
+
 int falkon_knm_matvec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t d, const float *C,
                       int64_t m, int kernel, double sigma, const double *v, double *u) {
   FK_TRY(check_common(ctx, n_local, d, m, kernel, sigma));
   if ((!X && n_local > 0) || !C || !v || !u) return fail(FALKON_EINVAL, "NULL array");
   Fit F;
+  if (n_local >= 8 * 1024 && !is_device_ptr(X) && tc_supported(ctx, kernel, d)) {
+    Prepared probe;
+    probe.path = FALKON_PATH_TENSOR;
+    probe.d = d;
+    if (!tc_single_eval(ctx, probe)) {
+      const void *vd;
+      FK_TRY(stage_in(ctx, WS_STAGE_V, v, sizeof(double) * m, &vd));
+      const bool host_out = !is_device_ptr(u);
+      double *ud = u;
+      if (host_out) {
+        void *w;
+        FK_TRY(ws_get(ctx, WS_STAGE_OUT, sizeof(double) * m, &w));
+        ud = (double *)w;
+      }
+      FK_TRY(matvec_host_pipelined(ctx, X, n_local, d, C, m, kernel, sigma, F,
+                                   (const double *)vd, ud));
+      if (host_out) {
+        FK_CUDA(cudaMemcpyAsync(u, ud, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
+        FK_CUDA(cudaStreamSynchronize(ctx->stream));
+      }
+      return FALKON_OK;
+    }
+  }
   FK_TRY(matvec_common(ctx, X, n_local, d, C, m, kernel, sigma, F));
   const void *vd;
   FK_TRY(stage_in(ctx, WS_STAGE_V, v, sizeof(double) * m, &vd));

@@ -115,6 +115,7 @@ struct falkon_ctx {
   // blocked Cholesky lookahead (precond.cu): high-priority stream for the panel chain, low
   // priority for the bulk trailing update; created on first use
   cudaStream_t hi_stream = nullptr, lo_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host-X pipeline of falkon_knm_matvec
   // co-resident CTAs of cluster launches, per kernel (kvp_tc.cu tc_cluster_slots)
   static constexpr int NSLOTCACHE = 8;
   const void *slot_fn[NSLOTCACHE] = {};
@@ -160,9 +161,13 @@ struct Prepared {
   const float *xa = nullptr;
   const void *Cp = nullptr;
   const float *cb = nullptr;
+  const double *mu = nullptr;  // tensor path: centring shift (device, d)
+  double g = 0.0;              // tensor path: coordinate scale sqrt(log2 e) / sigma
   alignas(64) unsigned char tmaps[4 * 128];  // CUtensorMap x4 (tensor path)
 };
 
+// X == nullptr (tensor path only): the packed-X buffer and maps are set up for n rows but no
+// row is packed yet (tc_pack_rows fills row ranges, e.g. while later rows are still in flight)
 int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const float *C,
                      int64_t m, int kernel, double sigma, Prepared *pp);
 // w = Knm z  (pass A).  z: fp32 m (device).  w64 (n, optional) and/or w32 (n, optional).
@@ -184,13 +189,18 @@ int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const floa
 // kv > 1 (8 or 16): z is [q][kv] fp32 and the outputs [p][kv] (multi-vector product)
 int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, double *out64,
             float *out32, int kv = 1);
+// tensor path, rows [r0, r0 + nr): pack them from Xrows (nr x d fp32, device), and pass A over
+// them alone (w32 + r0 receives their w).  Used by the host-X pipeline of falkon_knm_matvec.
+int tc_pack_rows(falkon_ctx *ctx, const Prepared &pp, const float *Xrows, int64_t r0, int64_t nr);
+int tc_pass_A_rows(falkon_ctx *ctx, const Prepared &pp, const float *z, float *w32, int64_t r0,
+                   int64_t nr);
 // single evaluation: true when single-vector products use the k strip
 bool tc_single_eval(const falkon_ctx *ctx, const Prepared &pp);
 // u = Knm^T (Knm z) on this rank with every kernel value evaluated once: per strip of rows,
 // pass A stores the strip's k values (fp32, row-major) while computing w, then a streaming
 // GEMV reads them back for u += strip^T w.  w32: fp32 n_pad output (w of every row).
 int tc_product_single_eval(falkon_ctx *ctx, const Prepared &pp, const float *z, float *w32,
-                           double *u);
+                           double *u, const float *dw = nullptr);
 
 // ------------------------------------------------------------------ preconditioner (precond.cu)
 int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel, double sigma,

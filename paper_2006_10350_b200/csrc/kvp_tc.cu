@@ -762,12 +762,14 @@ int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const floa
     tc_pack_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(C, m, d, mu, g, d16, (__half *)cp);
   }
   FK_LAUNCH_CHECK();
-  if (n > 0) {
+  if (n > 0 && X) {
     LaunchScope ls(ctx, FALKON_T_PREP);
     const int64_t blocks = std::min<int64_t>(cdiv<int64_t>(n, threads / 32), (int64_t)ctx->sm_count * 64);
     tc_pack_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(X, n, d, mu, g, d16, (__half *)xp);
     FK_LAUNCH_CHECK();
   }
+  pp->mu = mu;
+  pp->g = g;
   pp->dq = d16;
   pp->Xp = xp;
   pp->Cp = cp;
@@ -978,6 +980,22 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   return tc_launch(ctx, pp, passA, z, out64, out32, kv, 0, -1, nullptr, 0);
 }
 
+int tc_pack_rows(falkon_ctx *ctx, const Prepared &pp, const float *Xrows, int64_t r0, int64_t nr) {
+  if (nr <= 0) return FALKON_OK;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>(cdiv<int64_t>(nr, threads / 32), (int64_t)ctx->sm_count * 64);
+  LaunchScope ls(ctx, FALKON_T_PREP);
+  tc_pack_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(
+      Xrows, nr, pp.d, pp.mu, pp.g, pp.dq, (__half *)pp.Xp + r0 * (int64_t)(2 * pp.dq));
+  FK_LAUNCH_CHECK();
+  return FALKON_OK;
+}
+
+int tc_pass_A_rows(falkon_ctx *ctx, const Prepared &pp, const float *z, float *w32, int64_t r0,
+                   int64_t nr) {
+  return tc_launch(ctx, pp, true, z, nullptr, w32 + r0, 1, r0, nr, nullptr, 0);
+}
+
 // ------------------------------------------------------------------ single evaluation (NEXT-4)
 // Two-pass products evaluate every kernel value twice (pass A needs the whole row of K for
 // w_i, pass B needs the finished w).  For large d the fp16x3 cross term (6 d16 flops per
@@ -994,7 +1012,8 @@ constexpr int SE_CPW = 8;                     // centres per warp
 constexpr int SE_COLS = SE_WARPS * SE_CPW;    // centres per CTA
 constexpr int SE_FLUSH = 32;                  // tiles per fp32 partial (4 x 32 = 128 terms)
 __global__ void __launch_bounds__(32 * SE_WARPS) se_gemv_kernel(const float *__restrict__ K, int64_t ldk,
-                                                                const float *__restrict__ w, int64_t rows,
+                                                                const float *__restrict__ w,
+                                                                const float *__restrict__ dw, int64_t rows,
                                                                 int64_t tiles_per_split, int64_t m,
                                                                 double *__restrict__ acc, int first) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1015,10 +1034,14 @@ __global__ void __launch_bounds__(32 * SE_WARPS) se_gemv_kernel(const float *__r
     float4 wv;
     if (r + 3 < rows) {
       wv = __ldg(reinterpret_cast<const float4 *>(w + r));
+      if (dw) {  // Knm^T D Knm (GSC LinOp, Alg. 2): the row weights, as scale_rows_kernel
+        const float4 dd = __ldg(reinterpret_cast<const float4 *>(dw + r));
+        wv.x *= dd.x, wv.y *= dd.y, wv.z *= dd.z, wv.w *= dd.w;
+      }
     } else {
-      wv.x = r < rows ? w[r] : 0.f;
-      wv.y = r + 1 < rows ? w[r + 1] : 0.f;
-      wv.z = r + 2 < rows ? w[r + 2] : 0.f;
+      wv.x = r < rows ? w[r] * (dw ? dw[r] : 1.f) : 0.f;
+      wv.y = r + 1 < rows ? w[r + 1] * (dw ? dw[r + 1] : 1.f) : 0.f;
+      wv.z = r + 2 < rows ? w[r + 2] * (dw ? dw[r + 2] : 1.f) : 0.f;
       wv.w = 0.f;
     }
     const float *kt = K + t * ldk * TC_M + 4 * lane;
@@ -1065,7 +1088,7 @@ bool tc_single_eval(const falkon_ctx *ctx, const Prepared &pp) {
 }
 
 int tc_product_single_eval(falkon_ctx *ctx, const Prepared &pp, const float *z, float *w32,
-                           double *u) {
+                           double *u, const float *dw) {
   const int64_t n = pp.n, m = pp.m;
   const int64_t ldk = m;
   // rows per strip: a whole number of 128-row P tiles within the strip budget, which is capped
@@ -1100,7 +1123,7 @@ int tc_product_single_eval(falkon_ctx *ctx, const Prepared &pp, const float *z, 
     LaunchScope ls(ctx, FALKON_T_PASS_B);
     const int64_t sp = cdiv<int64_t>(cdiv<int64_t>(nr, TC_M), tps);
     se_gemv_kernel<<<dim3((unsigned)cb, (unsigned)sp), 32 * SE_WARPS, 0, ctx->stream>>>(
-        K, ldk, w32 + r0, nr, tps, m, acc, r0 == 0 ? 1 : 0);
+        K, ldk, w32 + r0, dw ? dw + r0 : nullptr, nr, tps, m, acc, r0 == 0 ? 1 : 0);
     FK_LAUNCH_CHECK();
     if (r0 == 0 && sp < splits)  // later strips accumulate into every split row
       FK_CUDA(cudaMemsetAsync(acc + sp * m, 0, sizeof(double) * (size_t)(splits - sp) * m,

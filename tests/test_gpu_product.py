@@ -68,6 +68,26 @@ def test_host_pointer_path_matches_device_path(ctx):
     assert np.array_equal(ud, uh)
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_x_pipelined_path(ctx, pinned):
+    """Host X on the tensor path (n >= 8192): rows go up in 8 chunks on a copy stream and each
+    chunk is packed + run through pass A as it lands.  Same result as the device path up to the
+    fp64 order of per-split partials, and the oracle bar."""
+    import torch
+    X, C, v = _problem(30001, 1200, 90, seed=15)
+    ud = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 7.0, zeros(1200)))
+    Xh = torch.from_numpy(X)
+    if pinned:
+        Xh = Xh.pin_memory()
+    uh = np.zeros(1200)
+    ctx.knm_matvec(Xh, C, v, G, 7.0, uh)
+    assert rel_l2(uh, ud) <= 1e-12
+    assert rel_l2(uh, oracle.knm_t_knm_vec(X, C, v, G, 7.0)) <= TOL
+    uh2 = np.zeros(1200)
+    ctx.knm_matvec(Xh, C, v, G, 7.0, uh2)  # deterministic
+    assert np.array_equal(uh, uh2)
+
+
 def test_deterministic_bitwise(ctx):
     X, C, v = _problem(5000, 700, 28, seed=6)
     a = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 3.8, zeros(700)))

@@ -99,3 +99,25 @@ def test_single_eval_fit_parity(se_ctx, n, m, d, sigma, lam, iters):
     f_ref = oracle.predict(Xs, C, a_ref, G, sigma)
     f = se_ctx.predict(dev(Xs), dev(C), a, G, sigma, zeros(2000))
     assert rel_l2(host(f), f_ref) <= 1e-3
+
+
+def test_single_eval_weighted_gsc_parity(se_ctx, ctx):
+    """GSC-Falkon / LogFalkon (Alg. 2) on the single-evaluation product: the strip GEMV applies
+    the row weights D of the weighted LinOp Knm^T D Knm.  Same alpha as the two-pass product
+    up to the problem's conditioning and the oracle bar.  Shape of test_gpu_gsc's well-posed
+    tensor case (alpha moves <= 1e-5 under 6e-8 relative noise on the kernel values)."""
+    from oracle import gsc
+    n, m, d, sigma = 16_001, 300, 90, 7.0
+    X = synth.gen_X(3, 0, n, d)
+    y = synth.gen_y(3, X, 0, "cls")
+    idx = synth.center_indices(3, n, m)
+    C, yC = X[idx].copy(), y[idx].copy()
+    mus, its = [1e-3, 1e-4, 1e-5, 1e-6], [4, 4, 4, 8]
+    out = []
+    for c in (se_ctx, ctx):  # single evaluation forced (one 64 MiB strip) / default two-pass
+        a = zeros(m)
+        c.gsc_fit(dev(X), dev(y), dev(C), dev(yC), G, sigma, "logistic", mus, its, a)
+        out.append(host(a))
+    ao = gsc.gsc_falkon(X, y, C, yC, gsc.LOGISTIC, G, sigma, mus, its)
+    assert rel_l2(out[0], ao) <= 1e-3
+    assert rel_l2(out[0], out[1]) <= 1e-4
