@@ -70,3 +70,22 @@ def test_no_cpu_fallback_when_library_missing(tmp_path):
             binding.load(str(tmp_path / "missing.so"))
     finally:
         binding._LIB = saved
+
+
+def test_binding_enum_values_match_the_header():
+    """The Python binding's option / path / kernel constants are the header's enum values."""
+    from paper_2006_10350_b200 import binding
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    enums = {k: int(v) for k, v in re.findall(r"\b(FALKON_[A-Z_0-9]+)\s*=\s*(\d+)", src)}
+    pairs = {"OPT_PATH": "FALKON_OPT_PATH", "OPT_TC_MIN_D": "FALKON_OPT_TC_MIN_D",
+             "OPT_TC_TERMS": "FALKON_OPT_TC_TERMS", "OPT_KERNEL_TIMING": "FALKON_OPT_KERNEL_TIMING",
+             "OPT_EXP_OFFLOAD": "FALKON_OPT_EXP_OFFLOAD", "OPT_POTRF_OUTER": "FALKON_OPT_POTRF_OUTER",
+             "OPT_GEMM_WARPS": "FALKON_OPT_GEMM_WARPS", "OPT_SINGLE_EVAL": "FALKON_OPT_SINGLE_EVAL",
+             "OPT_STRIP_BYTES": "FALKON_OPT_STRIP_BYTES", "OPT_TC_CLUSTER": "FALKON_OPT_TC_CLUSTER",
+             "OPT_LOOKAHEAD": "FALKON_OPT_LOOKAHEAD", "PATH_AUTO": "FALKON_PATH_AUTO",
+             "PATH_SIMT": "FALKON_PATH_SIMT", "PATH_TENSOR": "FALKON_PATH_TENSOR",
+             "GAUSSIAN": "FALKON_GAUSSIAN", "LAPLACIAN": "FALKON_LAPLACIAN"}
+    for py, c in pairs.items():
+        assert getattr(binding, py) == enums[c], (py, c)
+    opts = {k for k in enums if k.startswith("FALKON_OPT_")}
+    assert opts == {c for c in pairs.values() if c.startswith("FALKON_OPT_")}
