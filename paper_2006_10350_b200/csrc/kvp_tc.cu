@@ -1011,6 +1011,7 @@ constexpr int SE_WARPS = 8;
 constexpr int SE_CPW = 8;                     // centres per warp
 constexpr int SE_COLS = SE_WARPS * SE_CPW;    // centres per CTA
 constexpr int SE_FLUSH = 32;                  // tiles per fp32 partial (4 x 32 = 128 terms)
+template <bool WEIGHTED>
 __global__ void __launch_bounds__(32 * SE_WARPS) se_gemv_kernel(const float *__restrict__ K, int64_t ldk,
                                                                 const float *__restrict__ w,
                                                                 const float *__restrict__ dw, int64_t rows,
@@ -1034,14 +1035,14 @@ __global__ void __launch_bounds__(32 * SE_WARPS) se_gemv_kernel(const float *__r
     float4 wv;
     if (r + 3 < rows) {
       wv = __ldg(reinterpret_cast<const float4 *>(w + r));
-      if (dw) {  // Knm^T D Knm (GSC LinOp, Alg. 2): the row weights, as scale_rows_kernel
+      if (WEIGHTED) {  // Knm^T D Knm (GSC LinOp, Alg. 2): the row weights, as scale_rows_kernel
         const float4 dd = __ldg(reinterpret_cast<const float4 *>(dw + r));
         wv.x *= dd.x, wv.y *= dd.y, wv.z *= dd.z, wv.w *= dd.w;
       }
     } else {
-      wv.x = r < rows ? w[r] * (dw ? dw[r] : 1.f) : 0.f;
-      wv.y = r + 1 < rows ? w[r + 1] * (dw ? dw[r + 1] : 1.f) : 0.f;
-      wv.z = r + 2 < rows ? w[r + 2] * (dw ? dw[r + 2] : 1.f) : 0.f;
+      wv.x = r < rows ? w[r] * (WEIGHTED ? dw[r] : 1.f) : 0.f;
+      wv.y = r + 1 < rows ? w[r + 1] * (WEIGHTED ? dw[r + 1] : 1.f) : 0.f;
+      wv.z = r + 2 < rows ? w[r + 2] * (WEIGHTED ? dw[r + 2] : 1.f) : 0.f;
       wv.w = 0.f;
     }
     const float *kt = K + t * ldk * TC_M + 4 * lane;
@@ -1122,8 +1123,12 @@ int tc_product_single_eval(falkon_ctx *ctx, const Prepared &pp, const float *z, 
     FK_TRY(tc_launch(ctx, pp, true, z, nullptr, w32 + r0, 1, r0, nr, K, ldk));
     LaunchScope ls(ctx, FALKON_T_PASS_B);
     const int64_t sp = cdiv<int64_t>(cdiv<int64_t>(nr, TC_M), tps);
-    se_gemv_kernel<<<dim3((unsigned)cb, (unsigned)sp), 32 * SE_WARPS, 0, ctx->stream>>>(
-        K, ldk, w32 + r0, dw ? dw + r0 : nullptr, nr, tps, m, acc, r0 == 0 ? 1 : 0);
+    if (dw)
+      se_gemv_kernel<true><<<dim3((unsigned)cb, (unsigned)sp), 32 * SE_WARPS, 0, ctx->stream>>>(
+          K, ldk, w32 + r0, dw + r0, nr, tps, m, acc, r0 == 0 ? 1 : 0);
+    else
+      se_gemv_kernel<false><<<dim3((unsigned)cb, (unsigned)sp), 32 * SE_WARPS, 0, ctx->stream>>>(
+          K, ldk, w32 + r0, nullptr, nr, tps, m, acc, r0 == 0 ? 1 : 0);
     FK_LAUNCH_CHECK();
     if (r0 == 0 && sp < splits)  // later strips accumulate into every split row
       FK_CUDA(cudaMemsetAsync(acc + sp * m, 0, sizeof(double) * (size_t)(splits - sp) * m,
