@@ -213,3 +213,19 @@ def test_nccl_collective_path_single_rank():
     finally:
         plain.close()
         coll.close()
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_exp_offload_modes_parity(ctx, mode):
+    """exp2 evaluated on the FMA pipe (degree-5 polynomial, FALKON_OPT_EXP_OFFLOAD) for none,
+    all, 1/4 or 1/2 of the entries: same 1e-4 product bar, including entries far below 2^-126
+    (sigma = 0.6 at d = 28: typical exponents ~ -110; the polynomial path clamps at -126)."""
+    from paper_2006_10350_b200 import binding
+    X, C, v = _problem(3001, 517, 28, seed=31)
+    ctx.set_option(binding.OPT_EXP_OFFLOAD, mode)
+    try:
+        for sigma in (3.8, 0.6):
+            u = ctx.knm_matvec(dev(X), dev(C), dev(v), G, sigma, zeros(517))
+            assert rel_l2(host(u), oracle.knm_t_knm_vec(X, C, v, G, sigma)) <= TOL, sigma
+    finally:
+        ctx.set_option(binding.OPT_EXP_OFFLOAD, 0)
