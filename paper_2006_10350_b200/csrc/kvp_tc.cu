@@ -378,10 +378,11 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   uint8_t *sB = smem + (STREAM ? 0 : a.nbox * TC_A_BOX);  // S x BBOX
   uint64_t *bars = reinterpret_cast<uint64_t *>(sB + S * BBOX);
   uint64_t *full = bars, *empty = bars + TC_MAX_STAGES, *tfull = bars + 2 * TC_MAX_STAGES,
-           *tempty = tfull + 2, *afull = tempty + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(afull + 1);
+           *tempty = tfull + 2, *afull = tempty + 2, *zfull = afull + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(zfull + 2);
   // [TC_M] fp64 half-row partials, 16-B aligned: the kv epilogue's z staging buffer that
-  // follows is accessed as float4 (bars + slot end at byte 184 of the 256-byte region)
+  // follows is accessed as float4 / bulk-copy target (bars + slot end at byte 200 of the
+  // 256-byte region)
   double *red = reinterpret_cast<double *>(
       (reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));
 
@@ -402,6 +403,8 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       mbar_init(&tempty[i], EPIW);
     }
     mbar_init(afull, 1);
+    mbar_init(&zfull[0], 1);
+    mbar_init(&zfull[1], 1);
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmP)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
@@ -433,6 +436,18 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     uint32_t phase = 0;
     for (int t = 0; t < ntiles; ++t) {
       const int q0 = (int)(qlo + (int64_t)t * NT);
+      if (KV > 1 && !STREAM) {
+        // the tile's z block ([NT][KV] fp32, contiguous) into z buffer t & 1 by one bulk copy,
+        // once the epilogue has released tile t - 2 (the tempty phase the MMA warp also waits on)
+        mbar_wait_safe(&tempty[t & 1], ((t >> 1) & 1) ^ 1);
+        if (elect_one()) {
+          float *zsm = reinterpret_cast<float *>(red + (size_t)TC_M * (KV > 3 ? KV : 3));
+          const uint32_t bytes = (uint32_t)(lmin(NT, a.nq - q0) * KV * 4);
+          mbar_expect_tx(&zfull[t & 1], bytes);
+          bulk_g2s(zsm + (t & 1) * NT * KV, a.z + (int64_t)q0 * KV, bytes, &zfull[t & 1]);
+        }
+        __syncwarp();
+      }
       for (int b = 0; b < a.nbox; ++b) {
         mbar_wait_safe(&empty[stage], phase ^ 1);
         if (elect_one()) {
@@ -545,14 +560,13 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       __syncwarp();
     }
   } else if (KV > 1 && warp >= 4) {
-    // multi-vector epilogue: thread = P row; the Q tile's z block ([NT][KV] fp32) is staged in
-    // shared memory (double-buffered, one named barrier per tile), KV/2 packed FFMA2 chains per
-    // tile in fp32, then KV fp64 sums
+    // multi-vector epilogue: thread = P row; the Q tile's z block ([NT][KV] fp32) arrives in
+    // shared memory by the producer's bulk copy (double-buffered, mbarrier per buffer), KV/2
+    // packed FFMA2 chains per tile in fp32, then KV fp64 sums
     const int ew = warp - 4;
     const int lg = ew & 3;
     const int half = ew >> 2;
     const int row = lg * 32 + lane;
-    const int etid = ew * 32 + lane;  // 0 .. 32 * EPIW - 1
     const int64_t p = p0 + row;
     const int col0 = half * HALF;
     float *zsm = reinterpret_cast<float *>(red + (size_t)TC_M * (KV > 3 ? KV : 3));  // [2][NT][KV]
@@ -562,14 +576,8 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     uint32_t rr[2][32];
     for (int t = 0; t < ntiles; ++t) {
       const int64_t q0 = qlo + (int64_t)t * NT;
-      if (!STREAM) {  // streaming kernel: no shared memory left, z is read through L1
-        float4 *dst = reinterpret_cast<float4 *>(zsm + (t & 1) * NT * KV);
-        const float4 *src = reinterpret_cast<const float4 *>(a.z + q0 * KV);
-        const int64_t lim4 = (lmin(NT, a.nq - q0) * KV) / 4;
-        for (int e = etid; e < NT * KV / 4; e += 32 * EPIW)
-          dst[e] = e < lim4 ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-        asm volatile("bar.sync 2, %0;" ::"n"(32 * EPIW) : "memory");
-      }
+      if (!STREAM)  // z block staged by the producer's bulk copy (streaming: read through L1)
+        mbar_wait_safe(&zfull[t & 1], (t >> 1) & 1);
       const int accb = t & 1;
       mbar_wait_safe(&tfull[accb], (t >> 1) & 1);
       tc_fence_after();
