@@ -317,7 +317,14 @@ __device__ __forceinline__ void tc_epi_chunk(const uint32_t (&r)[32], const floa
 // Multi-vector epilogue (Kv for V in R^{q x KV}): 32 accumulator columns,
 // k = exp2(min(t, 0)) once per entry, then acc[c] += k * z[j][c] for the KV vectors (z is
 // [q][KV] fp32).  MASK: columns j >= lim are skipped (their z rows may be past the buffer).
-template <bool MASK, int KV>
+__device__ __forceinline__ float4 lds128(const float *p) {  // explicit shared-memory load
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+template <bool MASK, int KV, bool SMEM = false>
 __device__ __forceinline__ void tc_epi_chunk_kv(const uint32_t (&r)[32], const float *__restrict__ z,
                                                 int lim, float2 (&acc)[KV > 1 ? KV / 2 : 1]) {
 #pragma unroll
@@ -328,7 +335,8 @@ __device__ __forceinline__ void tc_epi_chunk_kv(const uint32_t (&r)[32], const f
     const float4 *zp = reinterpret_cast<const float4 *>(z + j * KV);
 #pragma unroll
     for (int g = 0; g < KV / 4; ++g) {  // z in shared memory: LDS.128 broadcast per warp
-      const float4 zz = zp[g];  // smem (resident kernel) or global (streaming)
+      // smem (resident kernel: LDS, not a generic load) or global (streaming)
+      const float4 zz = SMEM ? lds128(reinterpret_cast<const float *>(zp + g)) : zp[g];
       acc[2 * g] = __ffma2_rn(kk, make_float2(zz.x, zz.y), acc[2 * g]);
       acc[2 * g + 1] = __ffma2_rn(kk, make_float2(zz.z, zz.w), acc[2 * g + 1]);
     }
@@ -593,14 +601,14 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           if (c + 1 < NCH) tmem_ld32(tb + (uint32_t)((c + 1) * 32), rr[(c + 1) & 1]);
-          tc_epi_chunk_kv<false, KV>(rr[c & 1], zt + c * 32 * KV, 32, acc);
+          tc_epi_chunk_kv<false, KV, !STREAM>(rr[c & 1], zt + c * 32 * KV, 32, acc);
           if (c + 1 < NCH) tmem_wait_ld_regs(rr[(c + 1) & 1]);
         }
       } else {
         for (int c = 0; c * 32 < cnt; ++c) {
           tmem_ld32(tb + (uint32_t)(c * 32), rr[0]);
           tmem_wait_ld_regs(rr[0]);
-          tc_epi_chunk_kv<true, KV>(rr[0], zt + c * 32 * KV, cnt - c * 32, acc);
+          tc_epi_chunk_kv<true, KV, !STREAM>(rr[0], zt + c * 32 * KV, cnt - c * 32, acc);
         }
       }
       tc_fence_before();
