@@ -286,13 +286,13 @@ __device__ __forceinline__ float tc_exp2(float t, int e) {
   return ex2_approx(t);
 }
 
-// 32 accumulator columns: k = exp2(min(t, 0)), acc += k * z (4 independent FFMA chains).
+// 32 accumulator columns: k = exp2(min(t, 0)), acc += k * z (4 independent chains, 2 FFMA2).
 // KST (single-evaluation strip): the 32 k values are also stored to kdst[j * TC_M], j < lim
 // (the strip is column-major inside each 128-row tile, so each warp store is coalesced), and
 // the second contraction reads them back instead of recomputing the cross term and the exp.
 template <int MODE, bool MASK, bool KST = false>
 __device__ __forceinline__ void tc_epi_chunk(const uint32_t (&r)[32], const float *__restrict__ z,
-                                             int lim, float (&acc)[4], float *kdst = nullptr) {
+                                             int lim, float2 (&acc)[2], float *kdst = nullptr) {
   const float4 *zp = reinterpret_cast<const float4 *>(z);
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
@@ -304,8 +304,10 @@ __device__ __forceinline__ void tc_epi_chunk(const uint32_t (&r)[32], const floa
       const int j = 4 * g + e;
       if (MASK && j >= lim) zv[e] = 0.f;
       kv[e] = tc_exp2<MODE>(__uint_as_float(r[j]), e);
-      acc[e] = fmaf(kv[e], zv[e], acc[e]);
     }
+    // chains e = 0..3 as two packed pairs (FFMA2: same per-lane fmaf, half the issue slots)
+    acc[0] = __ffma2_rn(make_float2(kv[0], kv[1]), make_float2(zv[0], zv[1]), acc[0]);
+    acc[1] = __ffma2_rn(make_float2(kv[2], kv[3]), make_float2(zv[2], zv[3]), acc[1]);
     if (KST) {  // column j of the tile: the warp's 32 rows are 128 contiguous bytes
 #pragma unroll
       for (int e = 0; e < 4; ++e)
@@ -656,7 +658,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       // stored too (finite values; the GEMV weights them by w = 0)
       float *kd = KST ? a.kst + ((int64_t)blockIdx.x * a.ldk + q0 + col0) * TC_M + row : nullptr;
       const bool kok = p0 < a.np;  // a cluster's padding CTA (whole tile past the strip) stores nothing
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       if (KST) {
         const int cw = cnt < HALF ? cnt : HALF;  // this warp's columns
         if (cw == HALF) {  // software-pipelined as below
@@ -701,7 +703,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[accb]);
-      acc64 += (double)((acc[0] + acc[1]) + (acc[2] + acc[3]));
+      acc64 += (double)((acc[0].x + acc[0].y) + (acc[1].x + acc[1].y));
     }
     // combine the column groups of each row in a fixed order (deterministic)
     if (half > 0) red[(half - 1) * TC_M + row] = acc64;
