@@ -276,8 +276,26 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// Two entries of exp2_poly at once on the packed f32x2 pipe (FADD2/FFMA2: half the issue slots
+// of the scalar form; per lane the same operations, so the same values as exp2_poly).  x <= 0.
+__device__ __forceinline__ float2 exp2_poly2(float a, float b) {
+  const float2 x = make_float2(fmaxf(a, -126.f), fmaxf(b, -126.f));
+  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);  // x - r, exact
+  float2 p = make_float2(1.327646430581808e-3f, 1.327646430581808e-3f);
+  p = __ffma2_rn(p, f, make_float2(9.675540961325169e-3f, 9.675540961325169e-3f));
+  p = __ffma2_rn(p, f, make_float2(5.550713464617729e-2f, 5.550713464617729e-2f));
+  p = __ffma2_rn(p, f, make_float2(2.4022120237350464e-1f, 2.4022120237350464e-1f));
+  p = __ffma2_rn(p, f, make_float2(6.931469440460205e-1f, 6.931469440460205e-1f));
+  p = __ffma2_rn(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 // Epilogue modes (template): 0 = every exp2 on MUFU; 1 = all on the FMA pipe; 2 = one of
-// four columns on the FMA pipe; 3 = two of four; 8/9 = diagnostics (no exp / no TMEM read).
+// four columns on the FMA pipe; 3 = two of four (2 and 3 evaluate their FMA-pipe entries in
+// pairs, exp2_poly2); 8/9 = diagnostics (no exp / no TMEM read).
 template <int MODE>
 __device__ __forceinline__ float tc_exp2(float t, int e) {
   t = fminf(t, 0.f);
@@ -294,6 +312,16 @@ template <int MODE, bool MASK, bool KST = false>
 __device__ __forceinline__ void tc_epi_chunk(const uint32_t (&r)[32], const float *__restrict__ z,
                                              int lim, float2 (&acc)[2], float *kdst = nullptr) {
   const float4 *zp = reinterpret_cast<const float4 *>(z);
+  float kp[32];  // MODE 2/3: the FMA-pipe entries, evaluated in pairs
+  if (MODE == 2 || MODE == 3) {
+#pragma unroll
+    for (int j = 0; j < 32; j += (MODE == 2 ? 8 : 4)) {
+      const int j2 = MODE == 2 ? j + 4 : j + 2;  // (e 0 of groups g, g+1) / (e 0, e 2 of g)
+      const float2 k2 = exp2_poly2(fminf(__uint_as_float(r[j]), 0.f), fminf(__uint_as_float(r[j2]), 0.f));
+      kp[j] = k2.x;
+      kp[j2] = k2.y;
+    }
+  }
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
     const float4 zz = __ldg(zp + g);
@@ -303,7 +331,8 @@ __device__ __forceinline__ void tc_epi_chunk(const uint32_t (&r)[32], const floa
     for (int e = 0; e < 4; ++e) {
       const int j = 4 * g + e;
       if (MASK && j >= lim) zv[e] = 0.f;
-      kv[e] = tc_exp2<MODE>(__uint_as_float(r[j]), e);
+      if ((MODE == 2 && e == 0) || (MODE == 3 && (e & 1) == 0)) kv[e] = kp[j];
+      else kv[e] = tc_exp2<(MODE == 2 || MODE == 3) ? 0 : MODE>(__uint_as_float(r[j]), e);
     }
     // chains e = 0..3 as two packed pairs (FFMA2: same per-lane fmaf, half the issue slots)
     acc[0] = __ffma2_rn(make_float2(kv[0], kv[1]), make_float2(zv[0], zv[1]), acc[0]);
