@@ -73,10 +73,20 @@ def sqdist(X1: np.ndarray, X2: np.ndarray, direct: bool | None = None) -> np.nda
     if direct is None:
         direct = d <= DIRECT_DIFF_MAX_D
     if direct:
-        D = np.zeros((X1.shape[0], X2.shape[0]), dtype=np.float64)
-        for k in range(d):
-            diff = X1[:, k:k + 1] - X2[None, :, k]
-            D += diff * diff
+        # D_ij = sum_k (x1_ik - x2_jk)^2, k in order.  Column chunks of X2 with in-place
+        # ufuncs keep the temporaries cache-sized (the same operations per element).
+        n1, n2 = X1.shape[0], X2.shape[0]
+        D = np.zeros((n1, n2), dtype=np.float64)
+        X2T = np.ascontiguousarray(X2.T)
+        cw = max(1, min(n2, (1 << 18) // max(n1, 1)))
+        diff = np.empty((n1, cw), dtype=np.float64)
+        for j0 in range(0, n2, cw):
+            j1 = min(n2, j0 + cw)
+            Dv, dv = D[:, j0:j1], diff[:, :j1 - j0]
+            for k in range(d):
+                np.subtract(X1[:, k:k + 1], X2T[k, None, j0:j1], out=dv)
+                np.multiply(dv, dv, out=dv)
+                Dv += dv
         return D
     n1 = np.einsum("ij,ij->i", X1, X1)
     n2 = np.einsum("ij,ij->i", X2, X2)
@@ -116,14 +126,24 @@ def knm_vec(X, C, v, kernel: int, sigma: float, block_rows: int | None = None) -
     return w
 
 
-def knm_t_vec(X, C, w, kernel: int, sigma: float, block_rows: int | None = None) -> np.ndarray:
-    """u = Knm^T w = sum_b k(X_b, C)^T w_b (Alg. 1 line 9, reading c2)."""
+def knm_t_vec(X, C, w, kernel: int, sigma: float, block_rows: int | None = None,
+              workers: int = 1) -> np.ndarray:
+    """u = Knm^T w = sum_b k(X_b, C)^T w_b (Alg. 1 line 9, reading c2).
+    ``workers > 1``: the row blocks are split over forked processes (as knm_t_knm_vec)."""
     X = np.asarray(X, dtype=np.float64)
     w = np.asarray(w, dtype=np.float64)
     q = _block_rows(C.shape[0], block_rows)
+    if workers > 1 and X.shape[0] > q:
+        return _pool_sum(X, C, w, kernel, sigma, q, workers, "t")
+    return _kt_range((X, C, w, kernel, sigma, q, 0, X.shape[0]))
+
+
+def _kt_range(args):
+    X, C, w, kernel, sigma, q, lo, hi = args
     u = np.zeros(C.shape[0], dtype=np.float64)
-    for s in range(0, X.shape[0], q):
-        u += kernel_block(X[s:s + q], C, kernel, sigma).T @ w[s:s + q]
+    for s in range(lo, hi, q):
+        e = min(s + q, hi)
+        u += kernel_block(X[s:e], C, kernel, sigma).T @ w[s:e]
     return u
 
 
@@ -139,10 +159,33 @@ def _ktkv_range(args):
 _POOL_STATE = {}
 
 
-def _ktkv_worker(bounds):
+def _pool_worker(bounds):
     st = _POOL_STATE
-    return _ktkv_range((st["X"], st["C"], st["v"], st["kernel"], st["sigma"], st["q"],
-                        bounds[0], bounds[1]))
+    fn = _kt_range if st["op"] == "t" else _ktkv_range
+    return fn((st["X"], st["C"], st["v"], st["kernel"], st["sigma"], st["q"],
+               bounds[0], bounds[1]))
+
+
+def _pool_sum(X, C, v, kernel, sigma, q, workers, op):
+    """Row blocks split over `workers` forked processes; each sums its own blocks
+    (Knm^T(Knm v) for op "tkv", Knm^T v for op "t"); the per-worker sums are added in
+    worker order."""
+    n = X.shape[0]
+    nblk = -(-n // q)
+    per = -(-nblk // workers)
+    bounds = [(i * per * q, min(n, (i + 1) * per * q)) for i in range(workers) if i * per * q < n]
+    _POOL_STATE.update(X=X, C=C, v=v, kernel=kernel, sigma=sigma, q=q, op=op)
+    import multiprocessing as mp
+    try:
+        with ProcessPoolExecutor(max_workers=len(bounds), mp_context=mp.get_context("fork"),
+                                 initializer=_limit_blas_threads) as ex:
+            parts = list(ex.map(_pool_worker, bounds))
+    finally:
+        _POOL_STATE.clear()
+    u = np.zeros(C.shape[0], dtype=np.float64)
+    for p in parts:
+        u += p
+    return u
 
 
 def knm_t_knm_vec(X, C, v, kernel: int, sigma: float, block_rows: int | None = None,
@@ -150,30 +193,16 @@ def knm_t_knm_vec(X, C, v, kernel: int, sigma: float, block_rows: int | None = N
     """u = Knm^T (Knm v) = sum_b k(X_b, C)^T (k(X_b, C) v).
 
     ``workers > 1`` splits the row blocks over forked processes (each sums its own
-    blocks; the per-worker sums are added in worker order).  Used only to time the
-    oracle on all host cores (bench.py cpu_baseline); the arithmetic is unchanged."""
+    blocks; the per-worker sums are added in worker order).  Used to time the oracle on
+    all host cores (bench.py cpu_baseline) and for large parity runs; the arithmetic of
+    every block is unchanged."""
     X = np.asarray(X, dtype=np.float64)
     C = np.asarray(C, dtype=np.float64)
     v = np.asarray(v, dtype=np.float64)
     q = _block_rows(C.shape[0], block_rows)
-    n = X.shape[0]
-    if workers <= 1 or n <= q:
-        return _ktkv_range((X, C, v, kernel, sigma, q, 0, n))
-    nblk = -(-n // q)
-    per = -(-nblk // workers)
-    bounds = [(i * per * q, min(n, (i + 1) * per * q)) for i in range(workers) if i * per * q < n]
-    _POOL_STATE.update(X=X, C=C, v=v, kernel=kernel, sigma=sigma, q=q)
-    import multiprocessing as mp
-    try:
-        with ProcessPoolExecutor(max_workers=len(bounds), mp_context=mp.get_context("fork"),
-                                 initializer=_limit_blas_threads) as ex:
-            parts = list(ex.map(_ktkv_worker, bounds))
-    finally:
-        _POOL_STATE.clear()
-    u = np.zeros(C.shape[0], dtype=np.float64)
-    for p in parts:
-        u += p
-    return u
+    if workers <= 1 or X.shape[0] <= q:
+        return _ktkv_range((X, C, v, kernel, sigma, q, 0, X.shape[0]))
+    return _pool_sum(X, C, v, kernel, sigma, q, workers, "tkv")
 
 
 def _limit_blas_threads():
@@ -189,25 +218,50 @@ def _limit_blas_threads():
 # Preconditioner, Alg. 1 lines 13-17, Eq. (7)
 # --------------------------------------------------------------------------------------
 def kmm(C, kernel: int, sigma: float) -> np.ndarray:
-    """K_mm = k(X_m, X_m) in fp64 (Alg. 1 line 14; fp64 as PAPER.md:480)."""
-    return kernel_block(C, C, kernel, sigma)
+    """K_mm = k(X_m, X_m) in fp64 (Alg. 1 line 14; fp64 as PAPER.md:480).
+    Filled row block by row block into one m x m array (each block is kernel_block of
+    those rows against all centres), so the peak memory is one m^2 buffer plus a block."""
+    C = np.asarray(C, dtype=np.float64)
+    m = C.shape[0]
+    K = np.empty((m, m), dtype=np.float64)
+    q = _block_rows(m, None)
+    for s in range(0, m, q):
+        K[s:s + q] = kernel_block(C[s:s + q], C, kernel, sigma)
+    return K
+
+
+def _chol_upper_inplace(M: np.ndarray) -> np.ndarray:
+    """Upper R with R^T R = M, computed by LAPACK dpotrf IN the buffer of M (C-contiguous,
+    symmetric; its upper triangle is read).  The C-ordered upper triangle of M is the
+    Fortran-ordered lower triangle of the same memory, so dpotrf('L') on that Fortran view
+    gives L = R^T there, and R is returned as the C-contiguous view L.T (no copy)."""
+    assert M.flags["C_CONTIGUOUS"]
+    L = sla.cholesky(M.T, lower=True, overwrite_a=True, check_finite=False)
+    return L.T
 
 
 def preconditioner(C, kernel: int, sigma: float, lam: float, jitter: float = DEFAULT_JITTER):
     """(T, A), both UPPER triangular with
         T^T T = K_mm + delta I                       (line 15; K_mm = T^T T)
         A^T A = (1/m) T T^T + lam I                  (lines 16-17; reading c3/c4)
-    delta = `jitter` (reading c6)."""
+    delta = `jitter` (reading c6).  Memory-lean but the same arithmetic as the formulas:
+    delta and lam are added to the diagonals in place (adding the zero off-diagonal
+    entries of delta I / lam I is exact), each Cholesky overwrites its input buffer, so
+    the peak is two m x m fp64 buffers (T and A)."""
     K = kmm(C, kernel, sigma)
     m = K.shape[0]
-    K = K + jitter * np.eye(m)
+    diag = np.arange(m)
+    K[diag, diag] += jitter
     try:
-        T = sla.cholesky(K, lower=False)
+        T = _chol_upper_inplace(K)
     except np.linalg.LinAlgError:
         raise NotPositiveDefinite(0) from None
-    M = (T @ T.T) / m + lam * np.eye(m)
+    del K
+    M = T @ T.T
+    M /= m
+    M[diag, diag] += lam
     try:
-        A = sla.cholesky(M, lower=False)
+        A = _chol_upper_inplace(M)
     except np.linalg.LinAlgError:
         raise NotPositiveDefinite(1) from None
     return T, A
@@ -233,9 +287,10 @@ def linop(beta, X, C, T, A, lam: float, kernel: int, sigma: float, n_global: int
     return _solve_upper(A, _solve_upper(T, c, trans=True) + lam * n * v, trans=True)
 
 
-def rhs(X, y, C, T, A, kernel: int, sigma: float, block_rows: int | None = None):
+def rhs(X, y, C, T, A, kernel: int, sigma: float, block_rows: int | None = None,
+        workers: int = 1):
     """R = A^-T T^-T Knm^T y  (Alg. 1 line 9, reading c2)."""
-    c = knm_t_vec(X, C, y, kernel, sigma, block_rows)
+    c = knm_t_vec(X, C, y, kernel, sigma, block_rows, workers)
     return _solve_upper(A, _solve_upper(T, c, trans=True), trans=True)
 
 
@@ -272,12 +327,12 @@ def fit(X, y, C, kernel: int, sigma: float, lam: float, iters: int,
         workers: int = 1):
     """Falkon, Alg. 1 (PAPER.md:105-117): preconditioner, R, CG(LinOp, R, t),
     alpha = T^-1 A^-1 beta.  C (= X_m) is an input (sampling lives in synth, reading c11).
-    `workers` only parallelises the row blocks of the products (knm_t_knm_vec)."""
+    `workers` only parallelises the row blocks of the products (RHS and LinOp)."""
     X = np.asarray(X, dtype=np.float64)
     y = np.asarray(y, dtype=np.float64)
     C = np.asarray(C, dtype=np.float64)
     T, A = preconditioner(C, kernel, sigma, lam, jitter)
-    R = rhs(X, y, C, T, A, kernel, sigma, block_rows)
+    R = rhs(X, y, C, T, A, kernel, sigma, block_rows, workers)
     beta, it = conjugate_gradient(
         lambda b: linop(b, X, C, T, A, lam, kernel, sigma, block_rows=block_rows, workers=workers),
         R, iters)
