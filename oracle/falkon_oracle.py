@@ -230,14 +230,43 @@ def kmm(C, kernel: int, sigma: float) -> np.ndarray:
     return K
 
 
-def _chol_upper_inplace(M: np.ndarray) -> np.ndarray:
-    """Upper R with R^T R = M, computed by LAPACK dpotrf IN the buffer of M (C-contiguous,
-    symmetric; its upper triangle is read).  The C-ordered upper triangle of M is the
-    Fortran-ordered lower triangle of the same memory, so dpotrf('L') on that Fortran view
-    gives L = R^T there, and R is returned as the C-contiguous view L.T (no copy)."""
-    assert M.flags["C_CONTIGUOUS"]
-    L = sla.cholesky(M.T, lower=True, overwrite_a=True, check_finite=False)
-    return L.T
+# Block size of the blocked Cholesky / triangular solves below.  LAPACK and BLAS calls on
+# whole m x m matrices go through scipy's LP64 (32-bit index) OpenBLAS, whose index
+# arithmetic overflows once m^2 > 2^31 (m > 46,340: dpotrf / dtrsv segfault at m = 5e4);
+# every LAPACK call here is on a NB x NB diagonal block, and the large products are numpy
+# matmuls (ILP64 OpenBLAS) on views of at most NB rows or columns.
+CHOL_NB = 2048
+
+
+def _chol_upper_inplace(M: np.ndarray, nb: int = CHOL_NB) -> np.ndarray:
+    """Upper R with R^T R = M, computed IN the C-contiguous buffer of M (its upper triangle
+    is read; the strict lower triangle is zeroed).  Textbook right-looking blocked Cholesky
+    (the blocked POTRF of App. C Alg. 4, in core): for each diagonal
+    block k
+        R_kk = chol(M_kk)                         (LAPACK dpotrf on an nb x nb block)
+        R_k,j = R_kk^-T M_k,j        (j > k)      (triangular solve, the panel row)
+        M_i,j -= R_k,i^T R_k,j       (k < i <= j) (trailing update, upper blocks only)
+    Raises np.linalg.LinAlgError on a non-positive pivot, as LAPACK."""
+    assert M.flags["C_CONTIGUOUS"] and M.shape[0] == M.shape[1]
+    m = M.shape[0]
+    for k0 in range(0, m, nb):
+        k1 = min(m, k0 + nb)
+        Rkk = sla.cholesky(M[k0:k1, k0:k1], lower=False, check_finite=False)
+        M[k0:k1, k0:k1] = Rkk
+        if k1 == m:
+            break
+        M[k0:k1, k1:] = sla.solve_triangular(Rkk, M[k0:k1, k1:], trans="T", lower=False,
+                                             check_finite=False)
+        P = M[k0:k1, :]  # panel row: R_k,* for columns >= k1
+        for j0 in range(k1, m, nb):
+            j1 = min(m, j0 + nb)
+            M[k1:j1, j0:j1] -= P[:, k1:j1].T @ P[:, j0:j1]
+    for i0 in range(0, m, nb):  # zero the strict lower triangle
+        i1 = min(m, i0 + nb)
+        M[i0:i1, :i0] = 0.0
+        blk = M[i0:i1, i0:i1]
+        blk[np.tril_indices(i1 - i0, -1)] = 0.0
+    return M
 
 
 def preconditioner(C, kernel: int, sigma: float, lam: float, jitter: float = DEFAULT_JITTER):
@@ -267,9 +296,28 @@ def preconditioner(C, kernel: int, sigma: float, lam: float, jitter: float = DEF
     return T, A
 
 
-def _solve_upper(U, b, trans: bool):
-    """U x = b (trans=False) or U^T x = b (trans=True), U upper triangular."""
-    return sla.solve_triangular(U, b, lower=False, trans="T" if trans else "N")
+def _solve_upper(U, b, trans: bool, nb: int = CHOL_NB):
+    """U x = b (trans=False) or U^T x = b (trans=True), U upper triangular: block back
+    (forward) substitution, LAPACK dtrsv on nb x nb diagonal blocks and numpy mat-vecs
+    for the off-diagonal blocks (see CHOL_NB)."""
+    m = U.shape[0]
+    x = np.array(b, dtype=np.float64, copy=True)
+    starts = list(range(0, m, nb))
+    if not trans:  # U x = b: last block first
+        for i0 in reversed(starts):
+            i1 = min(m, i0 + nb)
+            if i1 < m:
+                x[i0:i1] -= U[i0:i1, i1:] @ x[i1:]
+            x[i0:i1] = sla.solve_triangular(U[i0:i1, i0:i1], x[i0:i1], lower=False,
+                                            check_finite=False)
+    else:  # U^T x = b: first block first
+        for i0 in starts:
+            i1 = min(m, i0 + nb)
+            if i0 > 0:
+                x[i0:i1] -= U[:i0, i0:i1].T @ x[:i0]
+            x[i0:i1] = sla.solve_triangular(U[i0:i1, i0:i1], x[i0:i1], lower=False,
+                                            trans="T", check_finite=False)
+    return x
 
 
 # --------------------------------------------------------------------------------------

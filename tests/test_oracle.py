@@ -373,3 +373,26 @@ def test_device_target_generator_matches_host():
         a = synth.gen_y(4, X, 123456789, task)
         b = synth.gen_y_torch(4, torch.from_numpy(X), 123456789, task, chunk_rows=1500).numpy()
         assert np.max(np.abs(a.astype(np.float64) - b)) <= 1e-6
+
+
+def test_blocked_cholesky_and_solves_match_lapack():
+    """The oracle's blocked Cholesky / triangular solves (used so that no LAPACK call sees an
+    m x m matrix: scipy's LP64 OpenBLAS overflows past m = 46,340) equal unblocked LAPACK on
+    SPD matrices, for block sizes that leave ragged last blocks."""
+    import scipy.linalg as sla
+    from oracle import falkon_oracle as fo
+    rng = np.random.default_rng(11)
+    for m, nb in [(301, 7), (130, 64), (64, 64), (9, 2)]:
+        B = rng.standard_normal((m, m))
+        M = B @ B.T + m * np.eye(m)
+        R0 = sla.cholesky(M, lower=False)
+        R = fo._chol_upper_inplace(M.copy(), nb)
+        assert np.allclose(R, R0, rtol=0, atol=1e-12 * np.abs(R0).max())
+        assert np.all(np.tril(R, -1) == 0.0)
+        b = rng.standard_normal(m)
+        for trans in (False, True):
+            x = fo._solve_upper(R0, b, trans, nb)
+            x0 = sla.solve_triangular(R0, b, lower=False, trans="T" if trans else "N")
+            assert np.allclose(x, x0, rtol=1e-12, atol=1e-12)
+    with pytest.raises(np.linalg.LinAlgError):
+        fo._chol_upper_inplace(-np.eye(5), 2)
