@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="msd", choices=list(synth.CONFIGS))
+    ap.add_argument("--config", default="timit", choices=list(synth.CONFIGS),
+                    help="BASELINE.json workload (default: TIMIT, the largest single-GPU config)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-fit", action="store_true", help="skip the full falkon_fit timing")
     ap.add_argument("--fit-iters", type=int, default=None)
@@ -60,6 +61,8 @@ def parse():
                     help="tensor path: 1 CTA or 2-CTA clusters multicasting the Q boxes")
     ap.add_argument("--multi-k", type=int, default=0,
                     help="also time the k-output product Knm^T (Knm V), V in R^{m x k} (NEXT-3)")
+    ap.add_argument("--accum-f64", type=int, default=None, choices=[0, 1],
+                    help="contractions: 0 fp32 v/w, 1 fp64 v/w with DFMA (FALKON_OPT_ACCUM_F64)")
     ap.add_argument("--quick", action="store_true",
                     help="timed product steps only (no e2e, cpu_baseline, fit): for ncu runs")
     return ap.parse_args()
@@ -70,6 +73,23 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without a torchrun environment: re-launch this script as N
+    ranks (one process per GPU) through torch.distributed.run on 127.0.0.1.  Rank 0 prints the
+    JSON line; the return code is torchrun's."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def measured_peaks():
@@ -215,7 +235,7 @@ def roofline(args, cfg, kt, ms_total, n_local, m, sms):
               "share_of_step": kt[dom][0] / ms_total if ms_total else None,
               "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)"}
     if kt_path_tensor(args, d):
-        d16 = -(-(d + 2) // 16) * 16
+        d16 = -(-(d + 2) // 16) * 16  # d coordinates + 2 folded-bias slots (csrc/kvp_tc.cu)
         if d16 > 192:  # streaming kernel: 32-aligned segments
             d16 = -(-(d + 2) // 32) * 32
         peak_tf = float(peaks["bf16_tflops"]) / 3.0
@@ -257,6 +277,27 @@ def roofline(args, cfg, kt, ms_total, n_local, m, sms):
             "unit": "G kernel-evals/s", "frac": ach / peak,
             "peak_source": f"{peak_src} sm_max_mhz {f_hz/1e6:.0f} MHz x {sms} SM x "
                            "(128 FP32 lanes/(d+2) | 16 MUFU) per clk", **common}
+
+
+def product_roofline(args, cfg, sms):
+    """Single-evaluation roofline of the whole product (SURVEY.md §8(d) fraction (i), the
+    headline): per Knm entry the method needs 2d flops of cross term, one bias add, one exp
+    and two contraction MACs, evaluated ONCE.  Gaussian: tensor path = min(fp32-class tensor
+    rate / 2d, MUFU 16 ex2/clk/SM); SIMT path = min(FP32 128 lanes / (d + 3), MUFU).
+    Returns (kernel evals/s per GPU, description)."""
+    peaks, src = measured_peaks()
+    f_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    d = cfg.d
+    mufu = sms * 16 * f_hz
+    if kt_path_tensor(args, d):
+        tc = float(peaks["bf16_tflops"]) / 3.0 * 1e12 / (2.0 * d)
+        pk = min(tc, mufu)
+        return pk, (f"min(tensor {peaks['bf16_tflops']} TF/s / 3 / 2d = {tc:.3g}, MUFU "
+                    f"{sms} SM x 16 x {f_hz/1e6:.0f} MHz = {mufu:.3g}) evals/s ({src} peaks)")
+    fp32 = sms * 128 * f_hz / (d + 3)
+    pk = min(fp32, mufu)
+    return pk, (f"min(FP32 {sms} SM x 128 x {f_hz/1e6:.0f} MHz / (d+3) = {fp32:.3g}, MUFU "
+                f"{mufu:.3g}) evals/s")
 
 
 def host_cores():
@@ -337,7 +378,12 @@ def run_gsc(args, ctx, world, rank, barrier):
 def main():
     args = parse()
     cfg = synth.CONFIGS[args.config]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     world, rank, local = dist_env()
+    if args.gpus != world:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; timing {world} ranks",
+              file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
         return
@@ -358,6 +404,8 @@ def main():
         ctx.set_option(binding.OPT_EXP_OFFLOAD, args.exp_offload)
     if args.single_eval is not None:
         ctx.set_option(binding.OPT_SINGLE_EVAL, args.single_eval)
+    if args.accum_f64 is not None:
+        ctx.set_option(binding.OPT_ACCUM_F64, args.accum_f64)
     if args.tc_cluster is not None:
         ctx.set_option(binding.OPT_TC_CLUSTER, args.tc_cluster)
 
@@ -433,8 +481,11 @@ def main():
     value = n_global * m / (ms_step * 1e-3)
 
     # ---- roofline of the dominant kernel (device-timed inside the timed region) ----
-    roof = roofline(args, cfg, kt, ms_total, n_local, m,
-                    torch.cuda.get_device_properties(local).multi_processor_count)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    roof = roofline(args, cfg, kt, ms_total, n_local, m, sms)
+    pk_evals, pk_desc = product_roofline(args, cfg, sms)
+    roof["frac_product"] = value / world / pk_evals  # fraction (i): whole product, per GPU
+    roof["product_roofline"] = {"evals_per_s": pk_evals, "basis": pk_desc}
 
     if args.quick:
         args.no_fit = True

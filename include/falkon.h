@@ -66,7 +66,9 @@ enum { FALKON_PATH_AUTO = 0, FALKON_PATH_SIMT = 1, FALKON_PATH_TENSOR = 2 };
 enum {
   FALKON_OPT_PATH = 1,          /* FALKON_PATH_*; AUTO = tensor cores for Gaussian with d > threshold */
   FALKON_OPT_TC_MIN_D = 2,      /* AUTO threshold on d for the tensor path (default 8: measured crossover) */
-  FALKON_OPT_TC_TERMS = 3,      /* fp16 split terms of the tensor cross term: 1, 2 or 3 (default 3) */
+  FALKON_OPT_TC_TERMS = 3,      /* fp16 split terms of the tensor cross term: only 3 is built (the
+                                   fp32-accurate h.h + l.h + h.l split); other values return
+                                   FALKON_EUNSUPPORTED (1 and 2 terms fail the alpha bar) */
   FALKON_OPT_KERNEL_TIMING = 4, /* 1: record CUDA events around every launch (falkon_ctx_timings) */
   FALKON_OPT_EXP_OFFLOAD = 5,   /* tensor path: exp2 on the FMA pipe for 0 = none, 1 = all,
                                    2 = 1/4, 3 = 1/2 of the entries (rest on MUFU) */
@@ -87,9 +89,15 @@ enum {
   FALKON_OPT_TC_CLUSTER = 10,   /* tensor path: 1 = one CTA per P tile; 2 = clusters of two CTAs on
                                    consecutive P tiles, each loading half of every streamed Q box
                                    and multicasting it to both (halves the L2 -> SM traffic) */
-  FALKON_OPT_LOOKAHEAD = 11     /* blocked Cholesky: 1 (default) = the next outer panel's
+  FALKON_OPT_LOOKAHEAD = 11,    /* blocked Cholesky: 1 (default) = the next outer panel's
                                    factorisation runs on a high-priority stream while the bulk of
                                    the trailing update runs on a low-priority one; 0 = serial */
+  FALKON_OPT_ACCUM_F64 = 12     /* precision of the two contractions (SURVEY.md §7 hard part 3):
+                                   0 = fp32 v and w, fp32 partial sums flushed to fp64 per tile;
+                                   1 = fp64 v and w, each exact product k(x,c) * v accumulated by
+                                   DFMA in fp64 (k itself stays fp32).  Applies to the single-vector
+                                   products, fits, GSC fits and predictions; multi-output calls
+                                   stay fp32.  See DESIGN.md for the measured default. */
 };
 
 /* Per-launch-class accumulated device times in ms (falkon_ctx_timings). */
@@ -253,7 +261,8 @@ enum {
    start beta_0 = A T alpha (reading g4; same iterates as CG from beta_0).
    X: n_local x d fp32 (row shard).  y: n_local fp32 labels (+-1 for the logistic loss).
    C: m x d fp32, yC: m fp32 labels of the centres (replicated).  mu, iters: n_steps HOST
-   arrays (Alg. 2's geometric path is built by the caller, e.g. binding.newton_path).
+   arrays: the explicit level path of Alg. 2 (reading g5), built by the caller (e.g.
+   synth.GSC_CONFIGS); the library does none of the schedule.
    alpha: m fp64 (replicated).  T = chol(Kmm + delta I) is built once; A is rebuilt per step
    in the same m x m fp64 buffer.  info: phase times summed over steps, iters_run = total CG
    iterations.  Errors: as falkon_fit; EINVAL also for n_steps < 1, unknown loss, mu <= 0. */

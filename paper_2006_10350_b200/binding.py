@@ -24,6 +24,7 @@ PATH_AUTO, PATH_SIMT, PATH_TENSOR = 0, 1, 2
 OPT_PATH, OPT_TC_MIN_D, OPT_TC_TERMS, OPT_KERNEL_TIMING, OPT_EXP_OFFLOAD = 1, 2, 3, 4, 5
 OPT_POTRF_OUTER, OPT_GEMM_WARPS = 6, 7
 OPT_SINGLE_EVAL, OPT_STRIP_BYTES, OPT_TC_CLUSTER, OPT_LOOKAHEAD = 8, 9, 10, 11
+OPT_ACCUM_F64 = 12
 SINGLE_EVAL_OFF, SINGLE_EVAL_ON, SINGLE_EVAL_AUTO = 0, 1, 2
 TIMING_NAMES = ["prep", "pass_a", "pass_b", "reduce", "allreduce", "precond", "trsv", "vec"]
 
@@ -113,41 +114,33 @@ def _check(code: int):
         raise FalkonError(code, msg.decode() if msg else "")
 
 
-def _ptr(a, dtype: str, name: str):
-    """(pointer, numel) of a contiguous torch tensor or numpy array of the given dtype."""
+def _ptr(a, dtype: str, name: str, numel: Optional[int] = None, device: Optional[int] = None):
+    """(pointer, numel) of a contiguous torch tensor or numpy array of the given dtype.
+    `numel`: required element count (ValueError otherwise: the C ABI trusts the sizes);
+    `device`: a CUDA tensor must live on this device ordinal (host arrays are staged)."""
     if a is None:
         return None, 0
     if isinstance(a, np.ndarray):
         if a.dtype != np.dtype(dtype) or not a.flags["C_CONTIGUOUS"]:
             raise TypeError(f"{name}: expected C-contiguous numpy {dtype}, got {a.dtype}")
-        return a.ctypes.data, a.size
-    import torch
-    if isinstance(a, torch.Tensor):
+        p, k = a.ctypes.data, a.size
+    else:
+        import torch
+        if not isinstance(a, torch.Tensor):
+            raise TypeError(f"{name}: expected torch.Tensor or numpy.ndarray, got {type(a)}")
         tdt = {"float32": torch.float32, "float64": torch.float64}[dtype]
         if a.dtype != tdt or not a.is_contiguous():
             raise TypeError(f"{name}: expected contiguous torch {dtype}, got {a.dtype}")
-        return a.data_ptr(), a.numel()
-    raise TypeError(f"{name}: expected torch.Tensor or numpy.ndarray, got {type(a)}")
+        if device is not None and a.is_cuda and a.device.index != device:
+            raise ValueError(f"{name}: on cuda:{a.device.index}, context is on cuda:{device}")
+        p, k = a.data_ptr(), a.numel()
+    if numel is not None and k != numel:
+        raise ValueError(f"{name}: {k} elements, expected {numel}")
+    return p, k
 
 
 def _kernel_id(kernel) -> int:
     return KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
-
-
-def newton_path(mu0: float, q: float, lam: float, t: int, t_final: int):
-    """Level schedule of Alg. 2 GSC-Falkon (reading g5):
-    mu_0, q mu_0, ... while >= lam (stop when mu_{k+1} < lam), then lam with t_final CG
-    iterations.  Returns (mus, iters) for Context.gsc_fit."""
-    if not (mu0 > 0 and 0 < q < 1 and lam > 0):
-        raise ValueError("need mu0 > 0, 0 < q < 1, lam > 0")
-    mus, its, mu = [], [], float(mu0)
-    while True:
-        mus.append(mu)
-        its.append(int(t))
-        mu *= q
-        if mu < lam:
-            break
-    return mus + [float(lam)], its + [int(t_final)]
 
 
 def get_unique_id() -> bytes:
@@ -210,37 +203,41 @@ class Context:
         return int(_LIB.falkon_ctx_launch_count(self.h))
 
     # -- hot path
-    @staticmethod
-    def _xc(X, C):
-        px, nx = _ptr(X, "float32", "X")
-        pc, nc = _ptr(C, "float32", "C")
+    def _xc(self, X, C):
+        if len(X.shape) != 2 or len(C.shape) != 2:
+            raise ValueError("X and C must be 2-D (rows x d)")
         n, d = X.shape
         m = C.shape[0]
         if C.shape[1] != d:
             raise ValueError("X and C must have the same number of columns")
+        px, _ = _ptr(X, "float32", "X", n * d, self.device)
+        pc, _ = _ptr(C, "float32", "C", m * d, self.device)
         return px, n, d, pc, m
+
+    def _v(self, a, dtype, name, numel):
+        return _ptr(a, dtype, name, numel, self.device)[0]
 
     def knm_matvec(self, X, C, v, kernel, sigma, out):
         """out[m] (fp64) = sum over ranks Knm^T (Knm v)."""
         px, n, d, pc, m = self._xc(X, C)
-        pv, _ = _ptr(v, "float64", "v")
-        pu, _ = _ptr(out, "float64", "out")
+        pv = self._v(v, "float64", "v", m)
+        pu = self._v(out, "float64", "out", m)
         _check(_LIB.falkon_knm_matvec(self.h, px, n, d, pc, m, _kernel_id(kernel), float(sigma),
                                       pv, pu))
         return out
 
     def kernel_vec(self, X, C, v, kernel, sigma, out):
         px, n, d, pc, m = self._xc(X, C)
-        pv, _ = _ptr(v, "float64", "v")
-        pw, _ = _ptr(out, "float64", "out")
+        pv = self._v(v, "float64", "v", m)
+        pw = self._v(out, "float64", "out", n)
         _check(_LIB.falkon_kernel_vec(self.h, px, n, d, pc, m, _kernel_id(kernel), float(sigma),
                                       pv, pw))
         return out
 
     def kernel_tvec(self, X, C, w, kernel, sigma, out):
         px, n, d, pc, m = self._xc(X, C)
-        pw, _ = _ptr(w, "float64", "w")
-        pu, _ = _ptr(out, "float64", "out")
+        pw = self._v(w, "float64", "w", n)
+        pu = self._v(out, "float64", "out", m)
         _check(_LIB.falkon_kernel_tvec(self.h, px, n, d, pc, m, _kernel_id(kernel), float(sigma),
                                        pw, pu))
         return out
@@ -250,14 +247,17 @@ class Context:
         return int(_LIB.falkon_precond_work_elems(int(m)))
 
     def precond_build(self, C, kernel, sigma, lam, jitter, P, diagT, diagA, work) -> dict:
-        pc, _ = _ptr(C, "float32", "C")
         m, d = C.shape
+        pc = self._v(C, "float32", "C", m * d)
         info = FitInfo()
         code = _LIB.falkon_precond_build(self.h, pc, m, d, _kernel_id(kernel), float(sigma),
-                                         float(lam), float(jitter), _ptr(P, "float64", "P")[0],
-                                         _ptr(diagT, "float64", "diagT")[0],
-                                         _ptr(diagA, "float64", "diagA")[0],
-                                         _ptr(work, "float64", "work")[0], ctypes.byref(info))
+                                         float(lam), float(jitter),
+                                         self._v(P, "float64", "P", m * m),
+                                         self._v(diagT, "float64", "diagT", m),
+                                         self._v(diagA, "float64", "diagA", m),
+                                         self._v(work, "float64", "work",
+                                                 self.precond_work_elems(m)),
+                                         ctypes.byref(info))
         if code != 0:
             e = FalkonError(code, (_LIB.falkon_last_error() or b"").decode())
             e.info = info.as_dict()
@@ -266,28 +266,30 @@ class Context:
 
     def precond_solve(self, P, diagT, diagA, work, which: int, trans: bool, x):
         m = x.shape[0]
-        _check(_LIB.falkon_precond_solve(self.h, _ptr(P, "float64", "P")[0],
-                                         _ptr(diagT, "float64", "diagT")[0],
-                                         _ptr(diagA, "float64", "diagA")[0],
-                                         _ptr(work, "float64", "work")[0], m, int(which),
-                                         int(bool(trans)), _ptr(x, "float64", "x")[0]))
+        _check(_LIB.falkon_precond_solve(self.h, self._v(P, "float64", "P", m * m),
+                                         self._v(diagT, "float64", "diagT", m),
+                                         self._v(diagA, "float64", "diagA", m),
+                                         self._v(work, "float64", "work", self.precond_work_elems(m)),
+                                         m, int(which), int(bool(trans)),
+                                         self._v(x, "float64", "x", m)))
         return x
 
     def precond_solve_multi(self, P, diagT, diagA, work, which: int, trans: bool, X):
         """In-place solve of every row of X (k x m, each row one right-hand side)."""
         k, m = X.shape
-        _check(_LIB.falkon_precond_solve_multi(self.h, _ptr(P, "float64", "P")[0],
-                                               _ptr(diagT, "float64", "diagT")[0],
-                                               _ptr(diagA, "float64", "diagA")[0],
-                                               _ptr(work, "float64", "work")[0], m, int(which),
-                                               int(bool(trans)), _ptr(X, "float64", "X")[0],
-                                               m, k))
+        _check(_LIB.falkon_precond_solve_multi(self.h, self._v(P, "float64", "P", m * m),
+                                               self._v(diagT, "float64", "diagT", m),
+                                               self._v(diagA, "float64", "diagA", m),
+                                               self._v(work, "float64", "work",
+                                                       self.precond_work_elems(m)),
+                                               m, int(which), int(bool(trans)),
+                                               self._v(X, "float64", "X", k * m), m, k))
         return X
 
     def fit(self, X, y, C, kernel, sigma, lam, iters, alpha, jitter: float = -1.0):
         px, n, d, pc, m = self._xc(X, C)
-        py, _ = _ptr(y, "float32", "y")
-        pa, _ = _ptr(alpha, "float64", "alpha")
+        py = self._v(y, "float32", "y", n)
+        pa = self._v(alpha, "float64", "alpha", m)
         info = FitInfo()
         code = _LIB.falkon_fit(self.h, px, py, n, d, pc, m, _kernel_id(kernel), float(sigma),
                                float(lam), int(iters), float(jitter), pa, ctypes.byref(info))
@@ -301,11 +303,9 @@ class Context:
         """GSC-Falkon / LogFalkon (Alg. 2): Newton steps at levels mus[k] with iters[k] CG
         iterations each; loss "logistic" or "squared"."""
         px, n, d, pc, m = self._xc(X, C)
-        py, _ = _ptr(y, "float32", "y")
-        pyc, myc = _ptr(yC, "float32", "yC")
-        if myc != m:
-            raise ValueError("yC must have m entries")
-        pa, _ = _ptr(alpha, "float64", "alpha")
+        py = self._v(y, "float32", "y", n)
+        pyc = self._v(yC, "float32", "yC", m)
+        pa = self._v(alpha, "float64", "alpha", m)
         k = len(mus)
         if len(iters) != k:
             raise ValueError("mus and iters differ in length")
@@ -322,9 +322,8 @@ class Context:
             raise e
         return alpha, info.as_dict()
 
-    @staticmethod
-    def _mat(a, dtype, name, rows):
-        p, numel = _ptr(a, dtype, name)
+    def _mat(self, a, dtype, name, rows):
+        p, numel = _ptr(a, dtype, name, None, self.device)
         k = numel // max(rows, 1) if rows else 0
         if rows and k * rows != numel:
             raise ValueError(f"{name}: size {numel} is not a multiple of {rows} rows")
@@ -345,7 +344,7 @@ class Context:
         """F = k(X, C) alpha; alpha m x k, out n x k (fp64 row-major)."""
         px, n, d, pc, m = self._xc(X, C)
         pa, k = self._mat(alpha, "float64", "alpha", m)
-        pf, _ = _ptr(out, "float64", "out")
+        pf = self._v(out, "float64", "out", n * k)
         _check(_LIB.falkon_predict_multi(self.h, px, n, d, pc, m, _kernel_id(kernel), float(sigma),
                                          pa, k, pf))
         return out
@@ -369,8 +368,8 @@ class Context:
 
     def predict(self, X, C, alpha, kernel, sigma, out):
         px, n, d, pc, m = self._xc(X, C)
-        pa, _ = _ptr(alpha, "float64", "alpha")
-        pf, _ = _ptr(out, "float64", "out")
+        pa = self._v(alpha, "float64", "alpha", m)
+        pf = self._v(out, "float64", "out", n)
         _check(_LIB.falkon_predict(self.h, px, n, d, pc, m, _kernel_id(kernel), float(sigma),
                                    pa, pf))
         return out

@@ -170,15 +170,17 @@ __device__ __forceinline__ void loss_d12(int loss, double z, double y, double &d
     d2 = 1.0;
   }
 }
-// rows: g (-> fp32 w, pass B input) and D (-> fp32 weights) at the predictions z (reading g1)
+// rows: g (-> w, pass B input: fp32, or fp64 under ACCUM_F64) and D (-> fp32 weights) at the
+// predictions z (reading g1)
+template <typename G>
 __global__ void gsc_row_loss_kernel(const double *__restrict__ z, const float *__restrict__ y,
-                                    int64_t n, int64_t n_pad, int loss, float *__restrict__ g,
+                                    int64_t n, int64_t n_pad, int loss, G *__restrict__ g,
                                     float *__restrict__ dw) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad;
        i += (int64_t)gridDim.x * blockDim.x) {
     double d1 = 0.0, d2 = 0.0;
     if (i < n) loss_d12(loss, z ? z[i] : 0.0, (double)y[i], d1, d2);
-    g[i] = (float)d1;
+    g[i] = (G)d1;
     dw[i] = (float)d2;
   }
 }
@@ -207,7 +209,39 @@ struct Fit {
   Prepared pp;
   float *v32 = nullptr;   // m_pad
   float *w32 = nullptr;   // n_pad
+  double *v64 = nullptr;  // m_pad (ACCUM_F64)
+  double *w64 = nullptr;  // n_pad (ACCUM_F64)
+  bool f64 = false;       // FALKON_OPT_ACCUM_F64: fp64 v / w, DFMA contractions
 };
+
+static int64_t pad128(int64_t n) { return round_up<int64_t>(std::max<int64_t>(n, 1), 128); }
+
+// v (fp64 m, device) -> the pass-A operand of the fit's precision
+static int load_v(falkon_ctx *ctx, Fit &F, const double *v) {
+  if (F.f64) return f64_pad(ctx, v, F.v64, F.pp.m, pad128(F.pp.m));
+  return f64_to_f32(ctx, v, F.v32, F.pp.m, pad128(F.pp.m));
+}
+// pass A on the loaded v: w64 (external, optional) or the fit's own w buffer
+static int pass_A_fit(falkon_ctx *ctx, Fit &F, double *w64) {
+  if (F.f64) return pass_A64(ctx, F.pp, F.v64, w64 ? w64 : F.w64);
+  return pass_A(ctx, F.pp, F.v32, w64, w64 ? nullptr : F.w32);
+}
+// pass B on the fit's w buffer
+static int pass_B_fit(falkon_ctx *ctx, Fit &F, double *u) {
+  if (F.f64) return pass_B64(ctx, F.pp, F.w64, u);
+  return pass_B(ctx, F.pp, F.w32, u);
+}
+// the fit's w buffer from an fp32 (y, g) or fp64 (w) n-vector
+static int load_w32(falkon_ctx *ctx, Fit &F, const float *w) {
+  if (F.pp.n <= 0) return FALKON_OK;
+  if (F.f64) return f32_to_f64_pad(ctx, w, F.w64, F.pp.n, pad128(F.pp.n));
+  return f32_to_f32_pad(ctx, w, F.w32, F.pp.n, pad128(F.pp.n));
+}
+static int load_w64(falkon_ctx *ctx, Fit &F, const double *w) {
+  if (F.pp.n <= 0) return FALKON_OK;
+  if (F.f64) return f64_pad(ctx, w, F.w64, F.pp.n, pad128(F.pp.n));
+  return f64_to_f32(ctx, w, F.w32, F.pp.n, pad128(F.pp.n));
+}
 
 // w[i] *= dw[i] for the rows, 0 in the padding (GSC LinOp: Knm^T D Knm, Alg. 2 line 6)
 __global__ void scale_rows_kernel(float *__restrict__ w, const float *__restrict__ dw, int64_t n,
@@ -221,18 +255,23 @@ __global__ void scale_rows_kernel(float *__restrict__ w, const float *__restrict
 static int product(falkon_ctx *ctx, Fit &F, const double *v, double *u,
                    const float *dw = nullptr) {
   const int64_t m = F.pp.m;
-  FK_TRY(f64_to_f32(ctx, v, F.v32, m, round_up<int64_t>(m, 128)));
+  FK_TRY(load_v(ctx, F, v));
   if (F.pp.n > 0 && tc_single_eval(ctx, F.pp)) {  // NEXT-4: one evaluation per entry
-    FK_TRY(tc_product_single_eval(ctx, F.pp, F.v32, F.w32, u, dw));
+    if (F.f64) FK_TRY(tc_product_single_eval64(ctx, F.pp, F.v64, F.w64, u, dw));
+    else FK_TRY(tc_product_single_eval(ctx, F.pp, F.v32, F.w32, u, dw));
     return nccl_allreduce_f64(ctx, u, m);
   }
-  FK_TRY(pass_A(ctx, F.pp, F.v32, nullptr, F.w32));
+  FK_TRY(pass_A_fit(ctx, F, nullptr));
   if (dw) {
-    const int64_t n_pad = round_up<int64_t>(std::max<int64_t>(F.pp.n, 1), 128);
-    LaunchScope ls(ctx, FALKON_T_VEC);
-    scale_rows_kernel<<<vgrid(n_pad), VT, 0, ctx->stream>>>(F.w32, dw, F.pp.n, n_pad);
+    const int64_t n_pad = pad128(F.pp.n);
+    if (F.f64) {
+      FK_TRY(f64_pad(ctx, F.w64, F.w64, F.pp.n, n_pad, dw));  // w_i * D_ii in fp64, in place
+    } else {
+      LaunchScope ls(ctx, FALKON_T_VEC);
+      scale_rows_kernel<<<vgrid(n_pad), VT, 0, ctx->stream>>>(F.w32, dw, F.pp.n, n_pad);
+    }
   }
-  FK_TRY(pass_B(ctx, F.pp, F.w32, u));
+  FK_TRY(pass_B_fit(ctx, F, u));
   return nccl_allreduce_f64(ctx, u, m);
 }
 
@@ -363,10 +402,17 @@ static int product_multi(falkon_ctx *ctx, Fit &F, const double *V, int64_t vrs, 
 
 static int alloc_fit_vectors(falkon_ctx *ctx, Fit &F) {
   void *a, *b;
-  FK_TRY(ws_get(ctx, WS_V32, sizeof(float) * round_up<int64_t>(F.pp.m, 128), &a));
-  FK_TRY(ws_get(ctx, WS_W32, sizeof(float) * round_up<int64_t>(std::max<int64_t>(F.pp.n, 1), 128), &b));
+  FK_TRY(ws_get(ctx, WS_V32, sizeof(float) * pad128(F.pp.m), &a));
+  FK_TRY(ws_get(ctx, WS_W32, sizeof(float) * pad128(F.pp.n), &b));
   F.v32 = (float *)a;
   F.w32 = (float *)b;
+  F.f64 = ctx->opt.accum_f64 != 0;
+  if (F.f64) {
+    FK_TRY(ws_get(ctx, WS_V64, sizeof(double) * pad128(F.pp.m), &a));
+    FK_TRY(ws_get(ctx, WS_W64, sizeof(double) * pad128(F.pp.n), &b));
+    F.v64 = (double *)a;
+    F.w64 = (double *)b;
+  }
   return FALKON_OK;
 }
 
@@ -489,9 +535,10 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
       if (value < 1) return fail(FALKON_EINVAL, "bad tc_min_d");
       ctx->opt.tc_min_d = (int)value;
       return FALKON_OK;
-    case FALKON_OPT_TC_TERMS:
-      if (value < 1 || value > 3) return fail(FALKON_EINVAL, "tc_terms must be 1, 2 or 3");
-      ctx->opt.tc_terms = (int)value;
+    case FALKON_OPT_TC_TERMS:  // only the fp32-accurate 3-term split is built (reading d1)
+      if (value != 3)
+        return fail(FALKON_EUNSUPPORTED, "tc_terms: only the 3-term fp16 split is implemented "
+                                         "(1 and 2 terms fail the alpha bar, DESIGN.md reading d1)");
       return FALKON_OK;
     case FALKON_OPT_KERNEL_TIMING:
       ctx->opt.kernel_timing = value ? 1 : 0;
@@ -520,6 +567,10 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
       return FALKON_OK;
     case FALKON_OPT_LOOKAHEAD:
       ctx->opt.lookahead = value ? 1 : 0;
+      return FALKON_OK;
+    case FALKON_OPT_ACCUM_F64:
+      if (value != 0 && value != 1) return fail(FALKON_EINVAL, "accum_f64 must be 0 or 1");
+      ctx->opt.accum_f64 = (int)value;
       return FALKON_OK;
     case FALKON_OPT_TC_CLUSTER:
       if (value != 1 && value != 2) return fail(FALKON_EINVAL, "tc_cluster must be 1 or 2");
@@ -567,6 +618,7 @@ static int matvec_host_pipelined(falkon_ctx *ctx, const float *X, int64_t n, int
   const void *Cd;
   FK_TRY(stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd));
   FK_TRY(prepare_operands(ctx, nullptr, n, d, (const float *)Cd, m, kernel, sigma, &F.pp));
+  if (F.pp.path != FALKON_PATH_TENSOR) return FALKON_TC_RANGE;  // C out of fp16 range: staged path
   FK_TRY(alloc_fit_vectors(ctx, F));
   void *xs;
   FK_TRY(ws_get(ctx, WS_STAGE_X, sizeof(float) * n * d, &xs));
@@ -601,6 +653,13 @@ static int matvec_host_pipelined(falkon_ctx *ctx, const float *X, int64_t n, int
   }
   for (auto &e : ev) cudaEventDestroy(e);
   FK_TRY(rc);
+  bool bad = false;  // fp16 range guard of the packed chunks
+  FK_TRY(tc_range_check(ctx, &bad));
+  if (bad) {  // re-prepare from the staged rows: the range guard routes them to the SIMT path
+    FK_TRY(prepare_operands(ctx, (const float *)xs, n, d, (const float *)Cd, m, kernel, sigma, &F.pp));
+    FK_TRY(alloc_fit_vectors(ctx, F));
+    return product(ctx, F, vd, ud);
+  }
   FK_TRY(pass_B(ctx, F.pp, F.w32, ud));
   return nccl_allreduce_f64(ctx, ud, m);
 }
@@ -610,7 +669,8 @@ int falkon_knm_matvec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t 
   FK_TRY(check_common(ctx, n_local, d, m, kernel, sigma));
   if ((!X && n_local > 0) || !C || !v || !u) return fail(FALKON_EINVAL, "NULL array");
   Fit F;
-  if (n_local >= 8 * 1024 && !is_device_ptr(X) && tc_supported(ctx, kernel, d)) {
+  if (n_local >= 8 * 1024 && !is_device_ptr(X) && tc_supported(ctx, kernel, d) &&
+      !ctx->opt.accum_f64) {
     Prepared probe;
     probe.path = FALKON_PATH_TENSOR;
     probe.d = d;
@@ -624,8 +684,15 @@ int falkon_knm_matvec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t 
         FK_TRY(ws_get(ctx, WS_STAGE_OUT, sizeof(double) * m, &w));
         ud = (double *)w;
       }
-      FK_TRY(matvec_host_pipelined(ctx, X, n_local, d, C, m, kernel, sigma, F,
-                                   (const double *)vd, ud));
+      const int prc = matvec_host_pipelined(ctx, X, n_local, d, C, m, kernel, sigma, F,
+                                            (const double *)vd, ud);
+      if (prc == FALKON_TC_RANGE) {  // centres out of fp16 range: the staged (SIMT) path
+        F = Fit();
+        FK_TRY(matvec_common(ctx, X, n_local, d, C, m, kernel, sigma, F));
+        FK_TRY(product(ctx, F, (const double *)vd, ud));
+      } else {
+        FK_TRY(prc);
+      }
       if (host_out) {
         FK_CUDA(cudaMemcpyAsync(u, ud, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
         FK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -667,8 +734,8 @@ int falkon_kernel_vec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t 
     FK_TRY(ws_get(ctx, WS_STAGE_OUT, sizeof(double) * n_local, &p));
     wd = (double *)p;
   }
-  FK_TRY(f64_to_f32(ctx, (const double *)vd, F.v32, m, round_up<int64_t>(m, 128)));
-  FK_TRY(pass_A(ctx, F.pp, F.v32, wd, nullptr));
+  FK_TRY(load_v(ctx, F, (const double *)vd));
+  FK_TRY(pass_A_fit(ctx, F, wd));
   if (host_out) {
     FK_CUDA(cudaMemcpyAsync(w, wd, sizeof(double) * n_local, cudaMemcpyDeviceToHost, ctx->stream));
     FK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -692,9 +759,9 @@ int falkon_kernel_tvec(falkon_ctx *ctx, const float *X, int64_t n_local, int64_t
   if (n_local > 0) {
     const void *wd;
     FK_TRY(stage_in(ctx, WS_STAGE_V, w, sizeof(double) * n_local, &wd));
-    FK_TRY(f64_to_f32(ctx, (const double *)wd, F.w32, n_local, round_up<int64_t>(n_local, 128)));
+    FK_TRY(load_w64(ctx, F, (const double *)wd));
   }
-  FK_TRY(pass_B(ctx, F.pp, F.w32, ud));
+  FK_TRY(pass_B_fit(ctx, F, ud));
   FK_TRY(nccl_allreduce_f64(ctx, ud, m));
   if (host_out) {
     FK_CUDA(cudaMemcpyAsync(u, ud, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
@@ -830,12 +897,8 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
                                sigma, &F.pp)))
       break;
     if ((rc = alloc_fit_vectors(ctx, F))) break;
-    if (n_local > 0) {
-      if ((rc = f32_to_f32_pad(ctx, (const float *)yd, F.w32, n_local,
-                               round_up<int64_t>(n_local, 128))))
-        break;
-    }
-    if ((rc = pass_B(ctx, F.pp, F.w32, r))) break;
+    if ((rc = load_w32(ctx, F, (const float *)yd))) break;
+    if ((rc = pass_B_fit(ctx, F, r))) break;
     if ((rc = nccl_allreduce_f64(ctx, r, m))) break;
     if ((rc = trsv(ctx, P, dT, pw, m, 0, 1, r))) break;  // T^-T
     if ((rc = trsv(ctx, P, dA, pw, m, 1, 1, r))) break;  // A^-T
@@ -1002,18 +1065,22 @@ int falkon_gsc_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_lo
       {
         const double *zz = nullptr;
         if (k > 0 && n_local > 0) {
-          if ((rc = f64_to_f32(ctx, acur, F.v32, m, round_up<int64_t>(m, 128)))) break;
-          if ((rc = pass_A(ctx, F.pp, F.v32, z, nullptr))) break;
+          if ((rc = load_v(ctx, F, acur))) break;
+          if ((rc = pass_A_fit(ctx, F, z))) break;
           zz = z;
         }
         LaunchScope ls(ctx, FALKON_T_VEC);
-        gsc_row_loss_kernel<<<vgrid(n_pad), VT, 0, ctx->stream>>>(zz, (const float *)yd, n_local,
-                                                                   n_pad, loss, F.w32, dw);
+        if (F.f64)
+          gsc_row_loss_kernel<double><<<vgrid(n_pad), VT, 0, ctx->stream>>>(
+              zz, (const float *)yd, n_local, n_pad, loss, F.w64, dw);
+        else
+          gsc_row_loss_kernel<float><<<vgrid(n_pad), VT, 0, ctx->stream>>>(
+              zz, (const float *)yd, n_local, n_pad, loss, F.w32, dw);
       }
       BRK_CUDA(cudaGetLastError());
       // residual at the warm start beta_0 = A T alpha (reading g4):
       //   R - LinOp(beta_0) = -A^-T T^-T (Knm^T g + mu n (Kmm + delta I) alpha)
-      if ((rc = pass_B(ctx, F.pp, F.w32, r))) break;
+      if ((rc = pass_B_fit(ctx, F, r))) break;
       if ((rc = nccl_allreduce_f64(ctx, r, m))) break;
       {
         LaunchScope ls(ctx, FALKON_T_VEC);

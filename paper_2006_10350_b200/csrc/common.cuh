@@ -67,6 +67,7 @@ enum WsSlot {
   WS_MULTI,       // fp64 multi-output fit state
   WS_KSTRIP,      // fp32 k strip of the single-evaluation product [rows][ldk]
   WS_SE_ACC,      // fp64 [splits][m] accumulators of the strip GEMV
+  WS_V64,         // fp64 m_pad: v zero-padded (ACCUM_F64 pass-A input)
   WS_COUNT
 };
 
@@ -92,6 +93,7 @@ struct Options {
   int tc_cluster = 2;   // tensor path: clusters of 2 CTAs multicasting the Q boxes (measured
                         // MSD 21.7 -> 20.9 ms, TIMIT 431 -> 424 ms), or 1 CTA
   int64_t strip_bytes = (int64_t)16 << 30;
+  int accum_f64 = 0;    // FALKON_OPT_ACCUM_F64: fp64 v / w with DFMA contractions
 };
 
 }  // namespace falkon
@@ -163,7 +165,9 @@ struct Prepared {
   const float *cb = nullptr;
   const double *mu = nullptr;  // tensor path: centring shift (device, d)
   double g = 0.0;              // tensor path: coordinate scale sqrt(log2 e) / sigma
-  alignas(64) unsigned char tmaps[4 * 128];  // CUtensorMap x4 (tensor path)
+  // CUtensorMap x6 (tensor path): X as P, C as Q, C as P, X as Q, and the 192-row Q maps of
+  // the opt-in TS kernel (C, X)
+  alignas(64) unsigned char tmaps[6 * 128];
 };
 
 // X == nullptr (tensor path only): the packed-X buffer and maps are set up for n rows but no
@@ -175,6 +179,14 @@ int pass_A(falkon_ctx *ctx, const Prepared &pp, const float *z, double *w64, flo
 // u = Knm^T w (pass B) on this rank (no collective).  w: fp32 n (padded).  u: fp64 m.
 int pass_B(falkon_ctx *ctx, const Prepared &pp, const float *w, double *u);
 int f64_to_f32(falkon_ctx *ctx, const double *src, float *dst, int64_t n, int64_t n_pad);
+// FALKON_OPT_ACCUM_F64 passes: z fp64 (zero-padded to a multiple of 128), contraction by DFMA of
+// the exact fp32 kernel value, fp64 output (w64: n, u: m).
+int pass_A64(falkon_ctx *ctx, const Prepared &pp, const double *z, double *w64);
+int pass_B64(falkon_ctx *ctx, const Prepared &pp, const double *w, double *u);
+// dst[0..n) = src (times scale[i] if scale), dst[n..n_pad) = 0
+int f64_pad(falkon_ctx *ctx, const double *src, double *dst, int64_t n, int64_t n_pad,
+            const float *scale = nullptr);
+int f32_to_f64_pad(falkon_ctx *ctx, const float *src, double *dst, int64_t n, int64_t n_pad);
 // multi-vector passes: z [q][kv] fp32 (q = m for pass A, n_pad rows for pass B), outputs
 // [p][kv] (fp64 and/or fp32); kv = 1, 8 or 16
 int pass_A_multi(falkon_ctx *ctx, const Prepared &pp, const float *z, int kv, double *w64,
@@ -184,11 +196,18 @@ int f32_to_f32_pad(falkon_ctx *ctx, const float *src, float *dst, int64_t n, int
 
 // tensor path (kvp_tc.cu)
 bool tc_supported(const falkon_ctx *ctx, int kernel, int64_t d);
+// returns FALKON_TC_RANGE (internal) when a packed coordinate or bias is out of fp16 range
 int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const float *C, int64_t m,
                double sigma, const double *mu, Prepared *pp);
+constexpr int FALKON_TC_RANGE = 1000;  // internal: tensor-path operands out of fp16 range
+// device flag of the fp16 range guard (reset: zero it on the stream); check: read + sync
+int tc_range_flag(falkon_ctx *ctx, int **flag, bool reset);
+int tc_range_check(falkon_ctx *ctx, bool *bad);
 // kv > 1 (8 or 16): z is [q][kv] fp32 and the outputs [p][kv] (multi-vector product)
 int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, double *out64,
             float *out32, int kv = 1);
+// fp64 z / DFMA contraction variant (FALKON_OPT_ACCUM_F64), single vector
+int tc_pass64(falkon_ctx *ctx, const Prepared &pp, bool passA, const double *z, double *out64);
 // tensor path, rows [r0, r0 + nr): pack them from Xrows (nr x d fp32, device), and pass A over
 // them alone (w32 + r0 receives their w).  Used by the host-X pipeline of falkon_knm_matvec.
 int tc_pack_rows(falkon_ctx *ctx, const Prepared &pp, const float *Xrows, int64_t r0, int64_t nr);
@@ -201,6 +220,9 @@ bool tc_single_eval(const falkon_ctx *ctx, const Prepared &pp);
 // GEMV reads them back for u += strip^T w.  w32: fp32 n_pad output (w of every row).
 int tc_product_single_eval(falkon_ctx *ctx, const Prepared &pp, const float *z, float *w32,
                            double *u, const float *dw = nullptr);
+// the same with fp64 z / w and DFMA contractions (FALKON_OPT_ACCUM_F64); w64: fp64 n_pad
+int tc_product_single_eval64(falkon_ctx *ctx, const Prepared &pp, const double *z, double *w64,
+                             double *u, const float *dw = nullptr);
 
 // ------------------------------------------------------------------ preconditioner (precond.cu)
 int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel, double sigma,
@@ -233,6 +255,14 @@ __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// fp32 k >= 0 (an ex2.approx.ftz result: +0 or a normal number) -> the same value in fp64,
+// by re-biasing the exponent with integer ops (ACCUM_F64 contractions: the DFMA operand is the
+// exact fp32 kernel value; this keeps the conversion off the F2F unit).  +0 maps to 2^-127
+// (absolute error < 6e-39, far below the fp32 rounding of k itself).
+__device__ __forceinline__ double k_to_f64(float k) {
+  const uint32_t b = __float_as_uint(k);
+  return __hiloint2double((int)((b >> 3) + 0x38000000u), (int)(b << 29));
 }
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;

@@ -103,124 +103,6 @@ __global__ void pack_rows_kernel(const float *__restrict__ in, int64_t rows, int
   }
 }
 
-// ------------------------------------------------------------------ fused kvp, d <= 32
-template <int KER, int D, int R>
-__global__ void __launch_bounds__(KVP_THREADS)
-    kvp_small_kernel(const float *__restrict__ P, const float *__restrict__ pa, int64_t np,
-                     const float *__restrict__ Q, const float *__restrict__ qb,
-                     const float *__restrict__ z, int64_t nq, int64_t q_per_split,
-                     double *__restrict__ out64, float *__restrict__ out32) {
-  constexpr int DQ = (D + 3) & ~3;
-  constexpr int QF = KVP_TQ * DQ;  // floats of one Q tile
-  extern __shared__ __align__(128) float smem_f[];
-  // stage s: q tile at smem_f + s*QF, biases at SB + s*TQ, weights at SZ + s*TQ
-  float *const SB = smem_f + 2 * QF;
-  float *const SZ = SB + 2 * KVP_TQ;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_f + 2 * QF + 4 * KVP_TQ);
-
-  const int tid = threadIdx.x;
-  const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
-  const int64_t qhi = min(nq, qlo + q_per_split);
-  const int ntiles = qhi > qlo ? (int)cdiv<int64_t>(qhi - qlo, KVP_TQ) : 0;
-
-  auto issue = [&](int t) {
-    const int64_t q0 = qlo + (int64_t)t * KVP_TQ;
-    const int cnt = (int)lmin(KVP_TQ, qhi - q0);
-    const int cnt4 = (cnt + 3) & ~3;  // arrays are padded: reading up to cnt4 is in bounds
-    const int s = t & 1;
-    const uint32_t bq = (uint32_t)cnt * DQ * 4, bs = (uint32_t)cnt4 * 4;
-    mbar_expect_tx(&bar[s], bq + (KER == FALKON_GAUSSIAN ? bs : 0) + bs);
-    bulk_g2s(smem_f + s * QF, Q + q0 * DQ, bq, &bar[s]);
-    if (KER == FALKON_GAUSSIAN) bulk_g2s(SB + s * KVP_TQ, qb + q0, bs, &bar[s]);
-    bulk_g2s(SZ + s * KVP_TQ, z + q0, bs, &bar[s]);
-  };
-
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    if (ntiles > 0) issue(0);
-    if (ntiles > 1) issue(1);
-  }
-
-  // owned points -> registers
-  float pc[R][D];
-  float pav[R];
-  const int64_t pbase = (int64_t)blockIdx.x * (KVP_THREADS * R) + tid;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int64_t p = min(pbase + (int64_t)r * KVP_THREADS, np - 1);
-#pragma unroll
-    for (int k = 0; k < D; ++k) pc[r][k] = P[p * DQ + k];
-    pav[r] = (KER == FALKON_GAUSSIAN) ? pa[p] : 0.f;
-  }
-  double acc64[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) acc64[r] = 0.0;
-
-  for (int t = 0; t < ntiles; ++t) {
-    const int s = t & 1;
-    mbar_wait(&bar[s], (t >> 1) & 1);
-    const int cnt = (int)lmin(KVP_TQ, qhi - (qlo + (int64_t)t * KVP_TQ));
-    const float *q = smem_f + s * QF;
-    const float *sbs = SB + s * KVP_TQ;
-    const float *szs = SZ + s * KVP_TQ;
-    float acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.f;
-#pragma unroll 2
-    for (int j = 0; j < cnt; ++j) {
-      float qc[DQ];
-#pragma unroll
-      for (int k4 = 0; k4 < DQ / 4; ++k4) {
-        const float4 v4 = reinterpret_cast<const float4 *>(q + j * DQ)[k4];
-        qc[4 * k4 + 0] = v4.x;
-        qc[4 * k4 + 1] = v4.y;
-        qc[4 * k4 + 2] = v4.z;
-        qc[4 * k4 + 3] = v4.w;
-      }
-      const float zj = szs[j];
-      if (KER == FALKON_GAUSSIAN) {
-        const float bj = sbs[j];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          float e = pav[r] + bj;
-#pragma unroll
-          for (int k = 0; k < D; ++k) e = fmaf(pc[r][k], qc[k], e);
-          acc[r] = fmaf(ex2_approx(fminf(e, 0.f)), zj, acc[r]);
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          float dd = 0.f;
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            const float df = pc[r][k] - qc[k];
-            dd = fmaf(df, df, dd);
-          }
-          acc[r] = fmaf(ex2_approx(-sqrt_approx(dd)), zj, acc[r]);
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc64[r] += (double)acc[r];
-    __syncthreads();
-    if (tid == 0 && t + 2 < ntiles) issue(t + 2);
-  }
-
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int64_t p = pbase + (int64_t)r * KVP_THREADS;
-    if (p < np) {
-      if (out64) out64[(int64_t)blockIdx.y * np + p] = acc64[r];
-      if (out32) out32[p] = (float)acc64[r];
-    }
-  }
-}
-
 // ------------------------------------------------------------------ fused kvp, d <= 32, packed FP32x2
 // Tile-transposed layout "TT": points are grouped in tiles of 128; a tile stores coordinate k
 // of its 128 points contiguously ([k][128]), so (a) a Q tile is one contiguous bulk copy,
@@ -251,17 +133,21 @@ __global__ void pack_rows_tt_kernel(const float *__restrict__ in, int64_t rows, 
   if (bias) bias[r] = r < rows ? (float)(-0.5 * s) : 0.f;
 }
 
-template <int KER, int D, int R>
+// ZD (FALKON_OPT_ACCUM_F64): z is fp64 and each exact product k * z is accumulated by DFMA
+// in fp64 (no fp32 rounding of z, of the products or of the partial sums).
+template <int KER, int D, int R, bool ZD = false>
 __global__ void __launch_bounds__(KVP_THREADS)
     kvp_pk_kernel(const float *__restrict__ P, const float *__restrict__ pa, int64_t np,
                   const float *__restrict__ Q, const float *__restrict__ qb,
-                  const float *__restrict__ z, int64_t nq, int64_t q_per_split,
+                  const void *__restrict__ zv, int64_t nq, int64_t q_per_split,
                   double *__restrict__ out64, float *__restrict__ out32) {
   constexpr int QF = KVP_TQ * D;  // floats of one Q tile
+  constexpr int ZW = ZD ? 2 : 1;  // z element width in floats
   extern __shared__ __align__(128) float smem_f[];
   float *const SB = smem_f + 2 * QF;
   float *const SZ = SB + 2 * KVP_TQ;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(SZ + 2 * KVP_TQ);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(SZ + 2 * KVP_TQ * ZW);
+  const char *z = reinterpret_cast<const char *>(zv);
 
   const int tid = threadIdx.x;
   const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
@@ -270,11 +156,11 @@ __global__ void __launch_bounds__(KVP_THREADS)
   auto issue = [&](int t) {
     const int64_t q0 = qlo + (int64_t)t * KVP_TQ;  // multiple of 128: one whole TT tile
     const int s = t & 1;
-    const uint32_t bq = (uint32_t)QF * 4, bs = (uint32_t)KVP_TQ * 4;
-    mbar_expect_tx(&bar[s], bq + (KER == FALKON_GAUSSIAN ? bs : 0) + bs);
+    const uint32_t bq = (uint32_t)QF * 4, bs = (uint32_t)KVP_TQ * 4, bz = bs * ZW;
+    mbar_expect_tx(&bar[s], bq + (KER == FALKON_GAUSSIAN ? bs : 0) + bz);
     bulk_g2s(smem_f + s * QF, Q + (q0 >> 7) * (int64_t)QF, bq, &bar[s]);
     if (KER == FALKON_GAUSSIAN) bulk_g2s(SB + s * KVP_TQ, qb + q0, bs, &bar[s]);
-    bulk_g2s(SZ + s * KVP_TQ, z + q0, bs, &bar[s]);
+    bulk_g2s(SZ + s * KVP_TQ * ZW, z + q0 * 4 * ZW, bz, &bar[s]);
   };
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -303,8 +189,9 @@ __global__ void __launch_bounds__(KVP_THREADS)
     ad[r] = make_float2(a, a);
   }
   double acc64[R];
+  double accd[R][2];  // ZD: two fp64 DFMA chains per owned point
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc64[r] = 0.0;
+  for (int r = 0; r < R; ++r) acc64[r] = accd[r][0] = accd[r][1] = 0.0;
 
   for (int t = 0; t < ntiles; ++t) {
     const int s = t & 1;
@@ -313,15 +200,28 @@ __global__ void __launch_bounds__(KVP_THREADS)
     const float *q = smem_f + s * QF;
     const float4 *b4p = reinterpret_cast<const float4 *>(SB + s * KVP_TQ);
     const float4 *z4p = reinterpret_cast<const float4 *>(SZ + s * KVP_TQ);
+    const double2 *z2p = reinterpret_cast<const double2 *>(SZ + s * KVP_TQ * ZW);
     float2 acc[R][2];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
     for (int j4 = 0; j4 < cnt; j4 += 4) {
-      float4 zz = z4p[j4 >> 2];
-      if (j4 + 4 > cnt) {  // ragged tail of the last tile
-        if (j4 + 1 >= cnt) zz.y = 0.f;
-        if (j4 + 2 >= cnt) zz.z = 0.f;
-        if (j4 + 3 >= cnt) zz.w = 0.f;
+      float4 zz;
+      double2 zd0, zd1;
+      if (ZD) {
+        zd0 = z2p[j4 >> 1];
+        zd1 = z2p[(j4 >> 1) + 1];
+        if (j4 + 4 > cnt) {
+          if (j4 + 1 >= cnt) zd0.y = 0.0;
+          if (j4 + 2 >= cnt) zd1.x = 0.0;
+          if (j4 + 3 >= cnt) zd1.y = 0.0;
+        }
+      } else {
+        zz = z4p[j4 >> 2];
+        if (j4 + 4 > cnt) {  // ragged tail of the last tile
+          if (j4 + 1 >= cnt) zz.y = 0.f;
+          if (j4 + 2 >= cnt) zz.z = 0.f;
+          if (j4 + 3 >= cnt) zz.w = 0.f;
+        }
       }
       float2 e[R][2];
       if (KER == FALKON_GAUSSIAN) {
@@ -370,18 +270,34 @@ __global__ void __launch_bounds__(KVP_THREADS)
             e[r][h].y = ex2_approx(-sqrt_approx(e[r][h].y));
           }
       }
-      const float2 za = make_float2(zz.x, zz.y), zb = make_float2(zz.z, zz.w);
+      if (ZD) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        acc[r][0] = __ffma2_rn(e[r][0], za, acc[r][0]);
-        acc[r][1] = __ffma2_rn(e[r][1], zb, acc[r][1]);
+        for (int r = 0; r < R; ++r) {
+          accd[r][0] = fma(k_to_f64(e[r][0].x), zd0.x, accd[r][0]);
+          accd[r][1] = fma(k_to_f64(e[r][0].y), zd0.y, accd[r][1]);
+          accd[r][0] = fma(k_to_f64(e[r][1].x), zd1.x, accd[r][0]);
+          accd[r][1] = fma(k_to_f64(e[r][1].y), zd1.y, accd[r][1]);
+        }
+      } else {
+        const float2 za = make_float2(zz.x, zz.y), zb = make_float2(zz.z, zz.w);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          acc[r][0] = __ffma2_rn(e[r][0], za, acc[r][0]);
+          acc[r][1] = __ffma2_rn(e[r][1], zb, acc[r][1]);
+        }
       }
     }
+    if (!ZD) {
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-      acc64[r] += (double)((acc[r][0].x + acc[r][0].y) + (acc[r][1].x + acc[r][1].y));
+      for (int r = 0; r < R; ++r)
+        acc64[r] += (double)((acc[r][0].x + acc[r][0].y) + (acc[r][1].x + acc[r][1].y));
+    }
     __syncthreads();
     if (tid == 0 && t + 2 < ntiles) issue(t + 2);
+  }
+  if (ZD) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc64[r] = accd[r][0] + accd[r][1];
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -396,18 +312,20 @@ __global__ void __launch_bounds__(KVP_THREADS)
 // ------------------------------------------------------------------ fused kvp, any d (SIMT)
 // Each thread owns one P point; a tile of 32 Q points is in shared memory; the 32 exponents
 // of the tile are accumulated in registers over 32-wide chunks of the dimension.
-template <int KER>
+template <int KER, bool ZD = false>
 __global__ void __launch_bounds__(KVP_THREADS)
     kvp_generic_kernel(const float *__restrict__ P, const float *__restrict__ pa, int64_t np,
                        const float *__restrict__ Q, const float *__restrict__ qb,
-                       const float *__restrict__ z, int64_t nq, int64_t q_per_split, int dq,
+                       const void *__restrict__ zv, int64_t nq, int64_t q_per_split, int dq,
                        double *__restrict__ out64, float *__restrict__ out32) {
   constexpr int TQ = KVP_TQ_G;
+  constexpr int ZW = ZD ? 2 : 1;  // z element width in floats (ZD: fp64 z, DFMA contraction)
   extern __shared__ __align__(128) float smem_f[];
   const int QF = TQ * dq;
   float *const SB = smem_f + 2 * QF;
   float *const SZ = SB + 2 * TQ;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_f + 2 * QF + 4 * TQ);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(SZ + 2 * TQ * ZW);
+  const char *z = reinterpret_cast<const char *>(zv);
 
   const int tid = threadIdx.x;
   const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
@@ -418,11 +336,11 @@ __global__ void __launch_bounds__(KVP_THREADS)
     const int cnt = (int)lmin(TQ, qhi - q0);
     const int cnt4 = (cnt + 3) & ~3;
     const int s = t & 1;
-    const uint32_t bq = (uint32_t)cnt * dq * 4, bs = (uint32_t)cnt4 * 4;
-    mbar_expect_tx(&bar[s], bq + (KER == FALKON_GAUSSIAN ? bs : 0) + bs);
+    const uint32_t bq = (uint32_t)cnt * dq * 4, bs = (uint32_t)cnt4 * 4, bz = bs * ZW;
+    mbar_expect_tx(&bar[s], bq + (KER == FALKON_GAUSSIAN ? bs : 0) + bz);
     bulk_g2s(smem_f + s * QF, Q + q0 * dq, bq, &bar[s]);
     if (KER == FALKON_GAUSSIAN) bulk_g2s(SB + s * TQ, qb + q0, bs, &bar[s]);
-    bulk_g2s(SZ + s * TQ, z + q0, bs, &bar[s]);
+    bulk_g2s(SZ + s * TQ * ZW, z + q0 * 4 * ZW, bz, &bar[s]);
   };
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -446,6 +364,7 @@ __global__ void __launch_bounds__(KVP_THREADS)
     const float *sqs = smem_f + s * QF;
     const float *sbs = SB + s * TQ;
     const float *szs = SZ + s * TQ;
+    const double *szd = reinterpret_cast<const double *>(SZ + s * TQ * ZW);
     float e[TQ];
 #pragma unroll
     for (int j = 0; j < TQ; ++j) e[j] = (KER == FALKON_GAUSSIAN) ? pav + sbs[j] : 0.f;
@@ -485,15 +404,17 @@ __global__ void __launch_bounds__(KVP_THREADS)
       }
     }
     float acc = 0.f;
+    double ad[2] = {0.0, 0.0};
 #pragma unroll
     for (int j = 0; j < TQ; ++j) {
       if (j < cnt) {
         const float kv = (KER == FALKON_GAUSSIAN) ? ex2_approx(fminf(e[j], 0.f))
                                                   : ex2_approx(-sqrt_approx(e[j]));
-        acc = fmaf(kv, szs[j], acc);
+        if (ZD) ad[j & 1] = fma(k_to_f64(kv), szd[j], ad[j & 1]);
+        else acc = fmaf(kv, szs[j], acc);
       }
     }
-    acc64 += (double)acc;
+    acc64 += ZD ? ad[0] + ad[1] : (double)acc;
     __syncthreads();
     if (tid == 0 && t + 2 < ntiles) issue(t + 2);
   }
@@ -555,10 +476,11 @@ int f32_to_f32_pad(falkon_ctx *ctx, const float *src, float *dst, int64_t n, int
 
 // ------------------------------------------------------------------ dispatch
 typedef void (*kvp_fn)(const float *, const float *, int64_t, const float *, const float *,
-                       const float *, int64_t, int64_t, double *, float *);
+                       const void *, int64_t, int64_t, double *, float *);
 
 template <int KER, int D>
-static kvp_fn pick_small_R(int R) {
+static kvp_fn pick_small_R(int R, bool zd) {
+  if (zd) return R == 4 ? kvp_pk_kernel<KER, D, 4, true> : kvp_pk_kernel<KER, D, 2, true>;
   if (R == 4) return kvp_pk_kernel<KER, D, 4>;
   return kvp_pk_kernel<KER, D, 2>;
 }
@@ -571,10 +493,10 @@ static int small_D(int64_t d) {
 static int small_R(int D) { return D <= 12 ? 4 : 2; }
 
 template <int KER>
-static kvp_fn pick_small(int D, int R) {
+static kvp_fn pick_small(int D, int R, bool zd) {
   switch (D) {
 #define FK_CASE(DD) \
-  case DD: return pick_small_R<KER, DD>(R);
+  case DD: return pick_small_R<KER, DD>(R, zd);
     FK_CASE(1) FK_CASE(2) FK_CASE(3) FK_CASE(4) FK_CASE(5) FK_CASE(6) FK_CASE(7) FK_CASE(8)
     FK_CASE(9) FK_CASE(10) FK_CASE(11) FK_CASE(12) FK_CASE(13) FK_CASE(14) FK_CASE(15)
     FK_CASE(16) FK_CASE(20) FK_CASE(24) FK_CASE(28) FK_CASE(32)
@@ -593,9 +515,10 @@ static int occupancy(const void *fn, int threads, size_t smem) {
 }
 
 // One kvp launch (+ split reduction).  out64 (np, optional) / out32 (np, optional).
+// zd: z is fp64 and the contraction runs in fp64 (FALKON_OPT_ACCUM_F64).
 static int kvp_launch(falkon_ctx *ctx, int kernel, int64_t d, int dq, const float *P,
-                      const float *pa, int64_t np, const float *Q, const float *qb, const float *z,
-                      int64_t nq, int cls, double *out64, float *out32) {
+                      const float *pa, int64_t np, const float *Q, const float *qb, const void *z,
+                      int64_t nq, int cls, double *out64, float *out32, bool zd = false) {
   if (np <= 0) return FALKON_OK;
   const bool small = d <= 32;
   int D = 0, R = 1, TQ;
@@ -606,15 +529,19 @@ static int kvp_launch(falkon_ctx *ctx, int kernel, int64_t d, int dq, const floa
     R = small_R(D);
     const int DQ = (D + 3) & ~3;
     TQ = KVP_TQ;
-    fn = (const void *)(kernel == FALKON_GAUSSIAN ? pick_small<FALKON_GAUSSIAN>(D, R)
-                                                  : pick_small<FALKON_LAPLACIAN>(D, R));
-    smem = (size_t)(2 * TQ * D + 4 * TQ) * 4 + 16;
+    fn = (const void *)(kernel == FALKON_GAUSSIAN ? pick_small<FALKON_GAUSSIAN>(D, R, zd)
+                                                  : pick_small<FALKON_LAPLACIAN>(D, R, zd));
+    smem = (size_t)(2 * TQ * D + (zd ? 6 : 4) * TQ) * 4 + 16;
     (void)DQ;
   } else {
     TQ = KVP_TQ_G;
-    fn = (const void *)(kernel == FALKON_GAUSSIAN ? kvp_generic_kernel<FALKON_GAUSSIAN>
-                                                  : kvp_generic_kernel<FALKON_LAPLACIAN>);
-    smem = (size_t)(2 * TQ * dq + 4 * TQ) * 4 + 16;
+    if (zd)
+      fn = (const void *)(kernel == FALKON_GAUSSIAN ? kvp_generic_kernel<FALKON_GAUSSIAN, true>
+                                                    : kvp_generic_kernel<FALKON_LAPLACIAN, true>);
+    else
+      fn = (const void *)(kernel == FALKON_GAUSSIAN ? kvp_generic_kernel<FALKON_GAUSSIAN>
+                                                    : kvp_generic_kernel<FALKON_LAPLACIAN>);
+    smem = (size_t)(2 * TQ * dq + (zd ? 6 : 4) * TQ) * 4 + 16;
   }
   if (!fn) return fail(FALKON_EINVAL, "no kvp kernel for d=" + std::to_string(d));
   FK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -645,10 +572,10 @@ static int kvp_launch(falkon_ctx *ctx, int kernel, int64_t d, int dq, const floa
       ((kvp_fn)fn)<<<grid, KVP_THREADS, smem, ctx->stream>>>(P, pa, np, Q, qb, z, nq, qps, part,
                                                              splits == 1 ? out32 : nullptr);
     } else {
-      auto g = (kernel == FALKON_GAUSSIAN ? kvp_generic_kernel<FALKON_GAUSSIAN>
-                                          : kvp_generic_kernel<FALKON_LAPLACIAN>);
-      g<<<grid, KVP_THREADS, smem, ctx->stream>>>(P, pa, np, Q, qb, z, nq, qps, dq, part,
-                                                  splits == 1 ? out32 : nullptr);
+      typedef void (*gen_fn)(const float *, const float *, int64_t, const float *, const float *,
+                             const void *, int64_t, int64_t, int, double *, float *);
+      ((gen_fn)fn)<<<grid, KVP_THREADS, smem, ctx->stream>>>(P, pa, np, Q, qb, z, nq, qps, dq,
+                                                             part, splits == 1 ? out32 : nullptr);
     }
   }
   FK_LAUNCH_CHECK();
@@ -675,7 +602,10 @@ int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, cons
   const bool use_tc = tc_supported(ctx, kernel, d);
   if (use_tc) {
     pp->path = FALKON_PATH_TENSOR;
-    return tc_prepare(ctx, X, n, d, C, m, sigma, mu, pp);
+    const int rc = tc_prepare(ctx, X, n, d, C, m, sigma, mu, pp);
+    if (rc != FALKON_TC_RANGE) return rc;
+    // operands out of the fp16 range of the tensor path's split (e.g. unstandardised data or a
+    // tiny sigma): the fp32 SIMT kernels below take this product
   }
   pp->path = FALKON_PATH_SIMT;
   const bool tt = d <= 32;  // packed-FFMA2 kernel: tile-transposed layout, D = small_D(d)
@@ -749,6 +679,54 @@ int pass_B(falkon_ctx *ctx, const Prepared &pp, const float *w, double *u) {
   if (pp.path == FALKON_PATH_TENSOR) return tc_pass(ctx, pp, false, w, u, nullptr);
   return kvp_launch(ctx, pp.kernel, pp.d, pp.dq, (const float *)pp.Cp, pp.cb, pp.m,
                     (const float *)pp.Xp, pp.xa, w, pp.n, FALKON_T_PASS_B, u, nullptr);
+}
+
+int pass_A64(falkon_ctx *ctx, const Prepared &pp, const double *z, double *w64) {
+  if (pp.n <= 0) return FALKON_OK;
+  if (pp.path == FALKON_PATH_TENSOR) return tc_pass64(ctx, pp, true, z, w64);
+  return kvp_launch(ctx, pp.kernel, pp.d, pp.dq, (const float *)pp.Xp, pp.xa, pp.n,
+                    (const float *)pp.Cp, pp.cb, z, pp.m, FALKON_T_PASS_A, w64, nullptr, true);
+}
+
+int pass_B64(falkon_ctx *ctx, const Prepared &pp, const double *w, double *u) {
+  if (pp.n <= 0) {
+    FK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * pp.m, ctx->stream));
+    return FALKON_OK;
+  }
+  if (pp.path == FALKON_PATH_TENSOR) return tc_pass64(ctx, pp, false, w, u);
+  return kvp_launch(ctx, pp.kernel, pp.d, pp.dq, (const float *)pp.Cp, pp.cb, pp.m,
+                    (const float *)pp.Xp, pp.xa, w, pp.n, FALKON_T_PASS_B, u, nullptr, true);
+}
+
+__global__ void pad_copy_f64_kernel(const double *__restrict__ s, double *__restrict__ d, int64_t n,
+                                    int64_t n_pad, const float *__restrict__ scale) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = scale ? s[i] * (double)scale[i] : s[i];
+  else if (i < n_pad) d[i] = 0.0;
+}
+__global__ void pad_copy_f32_f64_kernel(const float *__restrict__ s, double *__restrict__ d,
+                                        int64_t n, int64_t n_pad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = (double)s[i];
+  else if (i < n_pad) d[i] = 0.0;
+}
+
+int f64_pad(falkon_ctx *ctx, const double *src, double *dst, int64_t n, int64_t n_pad,
+            const float *scale) {
+  if (n_pad <= 0) return FALKON_OK;
+  LaunchScope ls(ctx, FALKON_T_PREP);
+  pad_copy_f64_kernel<<<(unsigned)cdiv<int64_t>(n_pad, 256), 256, 0, ctx->stream>>>(src, dst, n,
+                                                                                     n_pad, scale);
+  FK_LAUNCH_CHECK();
+  return FALKON_OK;
+}
+int f32_to_f64_pad(falkon_ctx *ctx, const float *src, double *dst, int64_t n, int64_t n_pad) {
+  if (n_pad <= 0) return FALKON_OK;
+  LaunchScope ls(ctx, FALKON_T_PREP);
+  pad_copy_f32_f64_kernel<<<(unsigned)cdiv<int64_t>(n_pad, 256), 256, 0, ctx->stream>>>(src, dst, n,
+                                                                                         n_pad);
+  FK_LAUNCH_CHECK();
+  return FALKON_OK;
 }
 
 // ------------------------------------------------------------------ multi-vector passes

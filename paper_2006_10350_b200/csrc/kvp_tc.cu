@@ -15,6 +15,12 @@
 // accumulator therefore holds the exponent t_pq itself and the epilogue is just
 // clamp -> ex2 (MUFU) -> FFMA with z_q.  One symmetric packed layout [h (d16) | l (d16)]
 // (d16 = round_up(d + 2, 16)) serves a point on either side of the product.
+// Precision (measured, scripts/k_precision.py, profiles/r2_k_precision.jsonl): the tensor
+// cores truncate (round toward zero) when accumulating in fp32 (scripts/probes/
+// mma_rounding.py), so t carries a bias toward zero of ~ulp(|partial sums|)/2; at TAXI's
+// scale (sigma = 1, |t| ~ 12) K is +2.2e-7 high on average (SIMT path: -4e-8), elsewhere
+// -7e-8 (the ex2.approx bias).  A 3-piece bias fold was tried: no gain (the bias is the
+// accumulation's, not the fold's).
 //
 // CTA structure (1 CTA per SM, 256 threads):
 //   warp 0      TMA producer: the CTA's 128 P rows once (all K, resident in smem), then the
@@ -52,12 +58,13 @@ int reduce_partials(falkon_ctx *ctx, const double *part, int64_t splits, int64_t
                     double *out64, float *out32);
 int center_mean(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, double **mu_out);
 
-static inline int tc_d16(int64_t d) { return (int)round_up<int64_t>(d + 2, 16); }
+constexpr int TC_BIAS_SLOTS = 2;  // spare K slots per segment carrying the folded bias
+static inline int tc_d16(int64_t d) { return (int)round_up<int64_t>(d + TC_BIAS_SLOTS, 16); }
 // segment length of the packed [h | l] row: 16-aligned when the P tile stays resident in
 // shared memory (2 * d16 <= 384), else 32-aligned for the streaming kernel (32-wide K boxes)
 static inline bool tc_stream(int64_t d) { return tc_d16(d) > TC_MAX_D16; }
 static inline int tc_seg(int64_t d) {
-  return tc_stream(d) ? (int)round_up<int64_t>(d + 2, TC_SBK) : tc_d16(d);
+  return tc_stream(d) ? (int)round_up<int64_t>(d + TC_BIAS_SLOTS, TC_SBK) : tc_d16(d);
 }
 // TS (A operand in TMEM) needs 2 accumulators of TC_N_TS columns + 16 columns per d16/16
 // chunk pair: 2*192 + 16*nk <= 512  <=>  d16 <= 128.
@@ -78,9 +85,12 @@ bool tc_supported(const falkon_ctx *ctx, int kernel, int64_t d) {
 
 // ------------------------------------------------------------------ packing
 // One warp per row.  out row = [h_0..h_{d-1}, 1, 1, 0.. | l_0..l_{d-1}, (b-1)_hi, (b-1)_lo, 0..]
+// Range guard: fp16 holds |x| < 65504; a scaled coordinate or folded bias at or above
+// TC_FP16_SAFE sets *range_flag, and the caller falls back to the fp32 SIMT path.
+constexpr double TC_FP16_SAFE = 32768.0;
 __global__ void tc_pack_kernel(const float *__restrict__ in, int64_t rows, int64_t d,
                                const double *__restrict__ mu, double g, int d16,
-                               __half *__restrict__ out) {
+                               __half *__restrict__ out, int *__restrict__ range_flag) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -92,7 +102,11 @@ __global__ void tc_pack_kernel(const float *__restrict__ in, int64_t rows, int64
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const double bm1 = -0.5 * s - 1.0;
+    const double bm1 = -0.5 * s - 1.0;  // bias - 1 (the h.h slots add 2)
+    bool bad = !(fabs(bm1) < TC_FP16_SAFE);  // also catches NaN / inf inputs
+    for (int k = lane; k < d; k += 32)
+      bad |= !(fabs(((double)in[r * d + k] - mu[k]) * g) < TC_FP16_SAFE);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(range_flag, 1);
     const __half bh = __double2half(bm1);
     const __half bl = __double2half(bm1 - (double)__half2float(bh));
     __half *o = out + r * (int64_t)(2 * d16);
@@ -244,6 +258,7 @@ __device__ __forceinline__ void tmem_wait_ld_regs(uint32_t (&r)[32]) {
 
 struct TcArgs {
   const float *z;
+  const double *z64;  // ZD (ACCUM_F64): fp64 z instead of z
   int64_t np, nq, q_per_split;
   int nk;        // 16-wide K chunks per segment (d16 / 16)
   int nbox;      // 64-wide boxes covering one packed row (2*d16)
@@ -295,7 +310,8 @@ __device__ __forceinline__ float2 exp2_poly2(float a, float b) {
 
 // Epilogue modes (template): 0 = every exp2 on MUFU; 1 = all on the FMA pipe; 2 = one of
 // four columns on the FMA pipe; 3 = two of four (2 and 3 evaluate their FMA-pipe entries in
-// pairs, exp2_poly2); 8/9 = diagnostics (no exp / no TMEM read).
+// pairs, exp2_poly2); 8/9 = diagnostics (no exp / no TMEM read); 10/11 = no MMAs / no Q TMA;
+// 12 = fault injection (a pipeline stage never fills: tests the trap of mbar_wait_safe).
 template <int MODE>
 __device__ __forceinline__ float tc_exp2(float t, int e) {
   t = fminf(t, 0.f);
@@ -343,6 +359,49 @@ __device__ __forceinline__ void tc_epi_chunk(const uint32_t (&r)[32], const floa
         if (!MASK || 4 * g + e < lim) __stcs(kdst + (4 * g + e) * TC_M, kv[e]);  // evict-first
     }
   }
+}
+
+// ACCUM_F64 epilogue (FALKON_OPT_ACCUM_F64): k = exp2(min(t, 0)) in fp32 on the MUFU as above,
+// then acc[j & 3] += k * z_j by DFMA with fp64 z: the product of the fp32 kernel value and the
+// fp64 vector entry is exact and the sum is fp64 (no fp32 rounding of z, w or partial sums;
+// SURVEY.md §7 hard part 3).  KST: the fp32 k values are stored as in tc_epi_chunk.
+__device__ __forceinline__ void ld256_f64(double (&v)[4], const double *p) {  // LDG.E.256
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+      : "l"(p));
+}
+template <bool MASK, bool KST>
+__device__ __forceinline__ void tc_epi_chunk_d(const uint32_t (&r)[32], const double *__restrict__ z,
+                                               int lim, double (&acc)[4], float *kdst) {
+  // one 256-bit load per 4 columns, issued one group ahead of its use (the loads' L1 latency
+  // was the top stall: long scoreboard)
+  double zc[4], zn[4];
+  ld256_f64(zc, z);
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    if (g + 1 < 8) ld256_f64(zn, z + 4 * (g + 1));
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = 4 * g + e;
+      const double zv = (MASK && j >= lim) ? 0.0 : zc[e];
+      const float k = ex2_approx(fminf(__uint_as_float(r[j]), 0.f));
+      acc[e] = fma(k_to_f64(k), zv, acc[e]);
+      if (KST && (!MASK || j < lim)) __stcs(kdst + j * TC_M, k);
+    }
+    if (g + 1 < 8) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) zc[e] = zn[e];
+    }
+  }
+}
+
+// one 32-column chunk c of the single-vector epilogue, fp32 (tc_epi_chunk) or fp64 (ZD) z
+template <int MODE, bool MASK, bool KST, bool ZD>
+__device__ __forceinline__ void tc_epi_any(const uint32_t (&r)[32], const float *zt,
+                                           const double *ztd, int c, int lim, float2 (&acc)[2],
+                                           double (&accd)[4], float *kdst) {
+  if constexpr (ZD) tc_epi_chunk_d<MASK, KST>(r, ztd + c * 32, lim, accd, kdst);
+  else tc_epi_chunk<MODE, MASK, KST>(r, zt + c * 32, lim, acc, kdst);
 }
 
 // Multi-vector epilogue (Kv for V in R^{q x KV}): 32 accumulator columns,
@@ -396,7 +455,7 @@ __device__ __forceinline__ void tc_cp_128x256b(uint32_t tmem_dst, uint64_t sdesc
 // streamed operand; a stage is refilled only after BOTH CTAs' MMAs have released it (empty
 // barriers count CL arrivals, commits are multicast).
 template <int MODE, int NT, bool TS, bool STREAM = false, int EPIW = TC_EPI_WARPS, int KV = 1,
-          bool KST = false, int CL = 1>
+          bool KST = false, int CL = 1, bool ZD = false>
 __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     tc_kvp_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                   TcArgs a) {
@@ -492,6 +551,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
         if (elect_one()) {
           if (MODE == 11) {  // diagnostic: no Q loads
             mbar_arrive(&full[stage]);
+          } else if (MODE == 12) {  // fault injection: the stage never fills (mbar_wait_safe traps)
           } else if (STREAM) {
             uint8_t *st = sB + stage * BBOX;
             mbar_expect_tx(&full[stage], BBOX);
@@ -674,6 +734,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     const int64_t p = p0 + row;
     const int col0 = half * HALF;
     double acc64 = 0.0;
+    double accd[4] = {0.0, 0.0, 0.0, 0.0};  // ZD: fp64 DFMA chains over the whole split
     uint32_t rr[2][32];
     for (int t = 0; t < ntiles; ++t) {
       const int accb = t & 1;
@@ -682,7 +743,8 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       const int64_t q0 = qlo + (int64_t)t * NT;
       const int cnt = (int)lmin(NT, qhi - q0) - col0;  // valid columns of this half
       const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(accb * NT + col0);
-      const float *zt = a.z + q0 + col0;
+      const float *zt = ZD ? nullptr : a.z + q0 + col0;
+      const double *ztd = ZD ? a.z64 + q0 + col0 : nullptr;
       // KST: strip tile blockIdx.x, layout [tile][q][TC_M rows]; padding rows (p >= np) are
       // stored too (finite values; the GEMV weights them by w = 0)
       float *kd = KST ? a.kst + ((int64_t)blockIdx.x * a.ldk + q0 + col0) * TC_M + row : nullptr;
@@ -696,16 +758,16 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
             if (c + 1 < NCH) tmem_ld32(tb + (uint32_t)((c + 1) * 32), rr[(c + 1) & 1]);
-            if (kok) tc_epi_chunk<MODE, false, true>(rr[c & 1], zt + c * 32, 32, acc, kd + c * 32 * TC_M);
-            else tc_epi_chunk<MODE, false>(rr[c & 1], zt + c * 32, 32, acc);
+            if (kok) tc_epi_any<MODE, false, true, ZD>(rr[c & 1], zt, ztd, c, 32, acc, accd, kd + c * 32 * TC_M);
+            else tc_epi_any<MODE, false, false, ZD>(rr[c & 1], zt, ztd, c, 32, acc, accd, nullptr);
             if (c + 1 < NCH) tmem_wait_ld_regs(rr[(c + 1) & 1]);
           }
         } else {
           for (int c = 0; c * 32 < cw; ++c) {
             tmem_ld32(tb + (uint32_t)(c * 32), rr[0]);
             tmem_wait_ld_regs(rr[0]);
-            if (kok) tc_epi_chunk<MODE, true, true>(rr[0], zt + c * 32, cw - c * 32, acc, kd + c * 32 * TC_M);
-            else tc_epi_chunk<MODE, true>(rr[0], zt + c * 32, cw - c * 32, acc);
+            if (kok) tc_epi_any<MODE, true, true, ZD>(rr[0], zt, ztd, c, cw - c * 32, acc, accd, kd + c * 32 * TC_M);
+            else tc_epi_any<MODE, true, false, ZD>(rr[0], zt, ztd, c, cw - c * 32, acc, accd, nullptr);
           }
         }
       } else if (MODE == 9) {  // diagnostic: no TMEM traffic
@@ -719,21 +781,22 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           if (c + 1 < NCH) tmem_ld32(tb + (uint32_t)((c + 1) * 32), rr[(c + 1) & 1]);
-          tc_epi_chunk<MODE, false>(rr[c & 1], zt + c * 32, 32, acc);
+          tc_epi_any<MODE, false, false, ZD>(rr[c & 1], zt, ztd, c, 32, acc, accd, nullptr);
           if (c + 1 < NCH) tmem_wait_ld_regs(rr[(c + 1) & 1]);
         }
       } else {
         for (int c = 0; c * 32 < cnt; ++c) {
           tmem_ld32(tb + (uint32_t)(c * 32), rr[0]);
           tmem_wait_ld_regs(rr[0]);
-          tc_epi_chunk<MODE, true>(rr[0], zt + c * 32, cnt - c * 32, acc);
+          tc_epi_any<MODE, true, false, ZD>(rr[0], zt, ztd, c, cnt - c * 32, acc, accd, nullptr);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[accb]);
-      acc64 += (double)((acc[0].x + acc[0].y) + (acc[1].x + acc[1].y));
+      if (!ZD) acc64 += (double)((acc[0].x + acc[0].y) + (acc[1].x + acc[1].y));
     }
+    if (ZD) acc64 = (accd[0] + accd[1]) + (accd[2] + accd[3]);
     // combine the column groups of each row in a fixed order (deterministic)
     if (half > 0) red[(half - 1) * TC_M + row] = acc64;
     asm volatile("bar.sync 1, %0;" ::"n"(32 * EPIW) : "memory");
@@ -792,6 +855,23 @@ static int make_map(CUtensorMap *map, const __half *base, int64_t rows, int k_el
 
 static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
 
+// Device int of the fp16 range guard (in the WS_FLAGS slot); reset = zero it (stream-ordered).
+int tc_range_flag(falkon_ctx *ctx, int **flag, bool reset) {
+  void *p;
+  FK_TRY(ws_get(ctx, WS_FLAGS, 64, &p));
+  *flag = (int *)p;
+  if (reset) FK_CUDA(cudaMemsetAsync(p, 0, sizeof(int), ctx->stream));
+  return FALKON_OK;
+}
+int tc_range_check(falkon_ctx *ctx, bool *bad) {
+  int *flag, h = 0;
+  FK_TRY(tc_range_flag(ctx, &flag, false));
+  FK_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  *bad = h != 0;
+  return FALKON_OK;
+}
+
 int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const float *C, int64_t m,
                double sigma, const double *mu, Prepared *pp) {
   const int d16 = tc_seg(d);
@@ -803,18 +883,27 @@ int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const floa
   FK_TRY(ws_get(ctx, WS_XP, sizeof(__half) * n_pad * kp, &xp));
   FK_TRY(ws_get(ctx, WS_CP, sizeof(__half) * m_pad * kp, &cp));
   const int threads = 256;
+  int *flag;
+  FK_TRY(tc_range_flag(ctx, &flag, true));
   {
     LaunchScope ls(ctx, FALKON_T_PREP);
     const int64_t blocks = std::min<int64_t>(cdiv<int64_t>(m, threads / 32), 65535);
-    tc_pack_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(C, m, d, mu, g, d16, (__half *)cp);
+    tc_pack_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(C, m, d, mu, g, d16, (__half *)cp,
+                                                                   flag);
   }
   FK_LAUNCH_CHECK();
   if (n > 0 && X) {
     LaunchScope ls(ctx, FALKON_T_PREP);
     const int64_t blocks = std::min<int64_t>(cdiv<int64_t>(n, threads / 32), (int64_t)ctx->sm_count * 64);
-    tc_pack_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(X, n, d, mu, g, d16, (__half *)xp);
+    tc_pack_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(X, n, d, mu, g, d16, (__half *)xp,
+                                                                   flag);
     FK_LAUNCH_CHECK();
   }
+  // range guard (one stream synchronisation per prepare): out of fp16 range -> the caller
+  // re-prepares the operands for the fp32 SIMT path
+  bool bad = false;
+  FK_TRY(tc_range_check(ctx, &bad));
+  if (bad) return FALKON_TC_RANGE;
   pp->mu = mu;
   pp->g = g;
   pp->dq = d16;
@@ -825,10 +914,13 @@ int tc_prepare(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const floa
   CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(pp->tmaps);
   const bool st = tc_stream(d);
   FK_TRY(make_map(&maps[0], (const __half *)xp, n, kp, TC_M, st));  // X as P (pass A)
-  const int nt = (!st && tc_use_ts(d16)) ? TC_N_TS : TC_N;
-  FK_TRY(make_map(&maps[1], (const __half *)cp, m, kp, nt, st));  // C as Q (pass A)
+  FK_TRY(make_map(&maps[1], (const __half *)cp, m, kp, TC_N, st));  // C as Q (pass A)
   FK_TRY(make_map(&maps[2], (const __half *)cp, m, kp, TC_M, st));  // C as P (pass B)
-  FK_TRY(make_map(&maps[3], (const __half *)xp, n, kp, nt, st));  // X as Q (pass B)
+  FK_TRY(make_map(&maps[3], (const __half *)xp, n, kp, TC_N, st));  // X as Q (pass B)
+  if (!st && tc_use_ts(d16)) {  // TS kernel (opt-in): Q boxes of TC_N_TS rows
+    FK_TRY(make_map(&maps[4], (const __half *)cp, m, kp, TC_N_TS, st));
+    FK_TRY(make_map(&maps[5], (const __half *)xp, n, kp, TC_N_TS, st));
+  }
   return FALKON_OK;
 }
 
@@ -880,9 +972,10 @@ static int64_t tc_cluster_slots(falkon_ctx *ctx, const void *fn, int threads, si
 
 // One fused pass over P rows [p_begin, p_begin + p_count) (p_count < 0: all).  kst != null
 // (pass A, kv = 1): the k values are also stored row-major into kst[(p - p_begin) * ldk + q].
+// z64 != null: fp64 z and DFMA contractions (ACCUM_F64, kv 1, MODE 0); out64 is then required.
 static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z,
                      double *out64, float *out32, int kv, int64_t p_begin, int64_t p_count,
-                     float *kst, int64_t ldk) {
+                     float *kst, int64_t ldk, const double *z64 = nullptr) {
   const CUtensorMap *maps = reinterpret_cast<const CUtensorMap *>(pp.tmaps);
   const int d16 = pp.dq;
   const bool stream = tc_stream(pp.d);
@@ -891,7 +984,10 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
   const int64_t np = p_count >= 0 ? p_count : (passA ? pp.n : pp.m), nq = passA ? pp.m : pp.n;
   if (np <= 0) return FALKON_OK;
   if (kst && (!passA || kv != 1)) return fail(FALKON_EINVAL, "tc_launch: k strip needs pass A, kv 1");
-  const bool ts = kv == 1 && !stream && tc_use_ts(d16);
+  if (z64 && (kv != 1 || !out64)) return fail(FALKON_EINVAL, "tc_launch: fp64 z needs kv 1 and out64");
+  // TS (opt-in, single vector, resident P, MODE 0 two-pass only): the same decision selects
+  // the 192-row Q maps (maps[4], maps[5]) and the NT = 192 kernel
+  const bool ts = kv == 1 && !stream && !kst && !z64 && tc_use_ts(d16);
   const int nt = ts ? TC_N_TS : TC_N;
   // streaming: stages of 48 KB (P and Q boxes of both segments, 32 wide) — 4 fit
   const size_t sstage = (size_t)2 * (TC_M + TC_N) * TC_SBK * 2;
@@ -917,7 +1013,7 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
                           : tc_kvp_kernel<M, TC_N, false>);                        \
     break;
   switch (mode) {
-    FK_TC(1) FK_TC(2) FK_TC(3) FK_TC(8) FK_TC(9) FK_TC(10) FK_TC(11)
+    FK_TC(1) FK_TC(2) FK_TC(3) FK_TC(8) FK_TC(9) FK_TC(10) FK_TC(11) FK_TC(12)
     default:
       fn = ts ? tc_kvp_kernel<0, TC_N_TS, true>
               : (epiw == 16 ? tc_kvp_kernel<0, TC_N, false, false, 16>
@@ -927,7 +1023,7 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
 #undef FK_TC
   if (stream) fn = mode == 11 ? tc_kvp_kernel<11, TC_N, false, true> : tc_kvp_kernel<0, TC_N, false, true>;
   // 2-CTA clusters with Q multicast (FALKON_OPT_TC_CLUSTER): MODE 0, SS, single vector
-  const int cl = (ctx->opt.tc_cluster == 2 && kv == 1 && !ts && epiw == 16 &&
+  int cl = (ctx->opt.tc_cluster == 2 && kv == 1 && !ts && epiw == 16 &&
                   (mode <= 3 || kst)) || (ctx->opt.tc_cluster == 2 && kv == 1 && stream &&
                                           (mode == 0 || kst))
                      ? 2 : 1;
@@ -946,6 +1042,21 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
       fn = stream ? tc_kvp_kernel<0, TC_N, false, true, 8, 1, true>
                   : tc_kvp_kernel<0, TC_N, false, false, 16, 1, true>;
     epiw = stream ? 8 : 16;
+  }
+  if (z64) {  // ACCUM_F64 epilogue (MODE 0, exp on the MUFU; DFMA contraction)
+    const bool c2 = ctx->opt.tc_cluster == 2;
+    if (stream)
+      fn = kst ? (c2 ? tc_kvp_kernel<0, TC_N, false, true, 8, 1, true, 2, true>
+                     : tc_kvp_kernel<0, TC_N, false, true, 8, 1, true, 1, true>)
+               : (c2 ? tc_kvp_kernel<0, TC_N, false, true, 8, 1, false, 2, true>
+                     : tc_kvp_kernel<0, TC_N, false, true, 8, 1, false, 1, true>);
+    else
+      fn = kst ? (c2 ? tc_kvp_kernel<0, TC_N, false, false, 16, 1, true, 2, true>
+                     : tc_kvp_kernel<0, TC_N, false, false, 16, 1, true, 1, true>)
+               : (c2 ? tc_kvp_kernel<0, TC_N, false, false, 16, 1, false, 2, true>
+                     : tc_kvp_kernel<0, TC_N, false, false, 16, 1, false, 1, true>);
+    epiw = stream ? 8 : 16;
+    cl = c2 ? 2 : 1;
   }
   if (kv > 1) {  // multi-vector epilogue (8 epilogue warps: KV fp32 + KV fp64 sums per thread)
     epiw = 8;
@@ -984,6 +1095,7 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
   }
   TcArgs args;
   args.z = z;
+  args.z64 = z64;
   args.np = np;
   args.nq = nq;
   args.q_per_split = qps;
@@ -999,7 +1111,7 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
     LaunchScope ls(ctx, passA ? FALKON_T_PASS_A : FALKON_T_PASS_B);
     if (cl == 1) {
       fn<<<dim3((unsigned)gx, (unsigned)splits), threads, smem, ctx->stream>>>(
-          passA ? maps[0] : maps[2], passA ? maps[1] : maps[3], args);
+          passA ? maps[0] : maps[2], passA ? maps[ts ? 4 : 1] : maps[ts ? 5 : 3], args);
     } else {  // Q boxes of 128 rows (the P-shaped map of the Q operand), cluster launch
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)gx, (unsigned)splits);
@@ -1027,13 +1139,19 @@ int tc_pass(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z, dou
   return tc_launch(ctx, pp, passA, z, out64, out32, kv, 0, -1, nullptr, 0);
 }
 
+int tc_pass64(falkon_ctx *ctx, const Prepared &pp, bool passA, const double *z, double *out64) {
+  return tc_launch(ctx, pp, passA, nullptr, out64, nullptr, 1, 0, -1, nullptr, 0, z);
+}
+
 int tc_pack_rows(falkon_ctx *ctx, const Prepared &pp, const float *Xrows, int64_t r0, int64_t nr) {
   if (nr <= 0) return FALKON_OK;
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>(cdiv<int64_t>(nr, threads / 32), (int64_t)ctx->sm_count * 64);
   LaunchScope ls(ctx, FALKON_T_PREP);
+  int *flag;
+  FK_TRY(tc_range_flag(ctx, &flag, false));  // checked by the caller after the last chunk
   tc_pack_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(
-      Xrows, nr, pp.d, pp.mu, pp.g, pp.dq, (__half *)pp.Xp + r0 * (int64_t)(2 * pp.dq));
+      Xrows, nr, pp.d, pp.mu, pp.g, pp.dq, (__half *)pp.Xp + r0 * (int64_t)(2 * pp.dq), flag);
   FK_LAUNCH_CHECK();
   return FALKON_OK;
 }
@@ -1058,12 +1176,15 @@ constexpr int SE_WARPS = 8;
 constexpr int SE_CPW = 8;                     // centres per warp
 constexpr int SE_COLS = SE_WARPS * SE_CPW;    // centres per CTA
 constexpr int SE_FLUSH = 32;                  // tiles per fp32 partial (4 x 32 = 128 terms)
-template <bool WEIGHTED>
+// WD (ACCUM_F64): w is fp64 and the GEMV accumulates the exact products k * w by DFMA.
+template <bool WEIGHTED, bool WD = false>
 __global__ void __launch_bounds__(32 * SE_WARPS) se_gemv_kernel(const float *__restrict__ K, int64_t ldk,
-                                                                const float *__restrict__ w,
+                                                                const void *__restrict__ wv,
                                                                 const float *__restrict__ dw, int64_t rows,
                                                                 int64_t tiles_per_split, int64_t m,
                                                                 double *__restrict__ acc, int first) {
+  const float *w = reinterpret_cast<const float *>(wv);
+  const double *wd = reinterpret_cast<const double *>(wv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t jb = (int64_t)blockIdx.x * SE_COLS + warp * SE_CPW;
   if (jb >= m) return;
@@ -1079,6 +1200,34 @@ __global__ void __launch_bounds__(32 * SE_WARPS) se_gemv_kernel(const float *__r
   for (int c = 0; c < SE_CPW; ++c) a64[c] = 0.0, a32[c] = 0.f;
   for (int64_t t = t0; t < t1; ++t) {
     const int64_t r = t * TC_M + 4 * lane;
+    if (WD) {  // fp64 w (rows are zero-padded to the tile, as the strip)
+      double4 w4;
+      const double2 wa = __ldg(reinterpret_cast<const double2 *>(wd + r));
+      const double2 wb = __ldg(reinterpret_cast<const double2 *>(wd + r + 2));
+      w4.x = r < rows ? wa.x : 0.0;
+      w4.y = r + 1 < rows ? wa.y : 0.0;
+      w4.z = r + 2 < rows ? wb.x : 0.0;
+      w4.w = r + 3 < rows ? wb.y : 0.0;
+      if (WEIGHTED) {
+        w4.x *= r < rows ? (double)dw[r] : 0.0;
+        w4.y *= r + 1 < rows ? (double)dw[r + 1] : 0.0;
+        w4.z *= r + 2 < rows ? (double)dw[r + 2] : 0.0;
+        w4.w *= r + 3 < rows ? (double)dw[r + 3] : 0.0;
+      }
+      const float *kt = K + t * ldk * TC_M + 4 * lane;
+      float4 kq[SE_CPW];
+#pragma unroll
+      for (int c = 0; c < SE_CPW; ++c) kq[c] = __ldcs(reinterpret_cast<const float4 *>(kt + jc[c] * TC_M));
+#pragma unroll
+      for (int c = 0; c < SE_CPW; ++c) {
+        double s = a64[c];
+        s = fma(k_to_f64(kq[c].x), w4.x, s);
+        s = fma(k_to_f64(kq[c].y), w4.y, s);
+        s = fma(k_to_f64(kq[c].z), w4.z, s);
+        a64[c] = fma(k_to_f64(kq[c].w), w4.w, s);
+      }
+      continue;
+    }
     float4 wv;
     if (r + 3 < rows) {
       wv = __ldg(reinterpret_cast<const float4 *>(w + r));
@@ -1135,8 +1284,9 @@ bool tc_single_eval(const falkon_ctx *ctx, const Prepared &pp) {
   return tc_stream(pp.d);  // auto: d16 > 192 (TIMIT d = 440: 6 * 448 flops vs 8 B per entry)
 }
 
-int tc_product_single_eval(falkon_ctx *ctx, const Prepared &pp, const float *z, float *w32,
-                           double *u, const float *dw) {
+// z32/w32 (fp32 contractions) or z64/w64 (ACCUM_F64: DFMA contractions, fp64 w)
+static int single_eval_impl(falkon_ctx *ctx, const Prepared &pp, const float *z, const double *z64,
+                            float *w32, double *w64, double *u, const float *dw) {
   const int64_t n = pp.n, m = pp.m;
   const int64_t ldk = m;
   // rows per strip: a whole number of 128-row P tiles within the strip budget, which is capped
@@ -1167,21 +1317,40 @@ int tc_product_single_eval(falkon_ctx *ctx, const Prepared &pp, const float *z, 
   double *acc = (double *)ap;
   for (int64_t r0 = 0; r0 < n; r0 += rows) {
     const int64_t nr = std::min<int64_t>(rows, n - r0);
-    FK_TRY(tc_launch(ctx, pp, true, z, nullptr, w32 + r0, 1, r0, nr, K, ldk));
+    if (z64)
+      FK_TRY(tc_launch(ctx, pp, true, nullptr, w64 + r0, nullptr, 1, r0, nr, K, ldk, z64));
+    else
+      FK_TRY(tc_launch(ctx, pp, true, z, nullptr, w32 + r0, 1, r0, nr, K, ldk));
     LaunchScope ls(ctx, FALKON_T_PASS_B);
     const int64_t sp = cdiv<int64_t>(cdiv<int64_t>(nr, TC_M), tps);
-    if (dw)
-      se_gemv_kernel<true><<<dim3((unsigned)cb, (unsigned)sp), 32 * SE_WARPS, 0, ctx->stream>>>(
-          K, ldk, w32 + r0, dw + r0, nr, tps, m, acc, r0 == 0 ? 1 : 0);
-    else
-      se_gemv_kernel<false><<<dim3((unsigned)cb, (unsigned)sp), 32 * SE_WARPS, 0, ctx->stream>>>(
-          K, ldk, w32 + r0, nullptr, nr, tps, m, acc, r0 == 0 ? 1 : 0);
+    const dim3 grid((unsigned)cb, (unsigned)sp);
+    const int first = r0 == 0 ? 1 : 0;
+    if (z64) {
+      if (dw)
+        se_gemv_kernel<true, true><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w64 + r0, dw + r0, nr, tps, m, acc, first);
+      else
+        se_gemv_kernel<false, true><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w64 + r0, nullptr, nr, tps, m, acc, first);
+    } else if (dw) {
+      se_gemv_kernel<true><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w32 + r0, dw + r0, nr, tps, m, acc, first);
+    } else {
+      se_gemv_kernel<false><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w32 + r0, nullptr, nr, tps, m, acc, first);
+    }
     FK_LAUNCH_CHECK();
     if (r0 == 0 && sp < splits)  // later strips accumulate into every split row
       FK_CUDA(cudaMemsetAsync(acc + sp * m, 0, sizeof(double) * (size_t)(splits - sp) * m,
                               ctx->stream));
   }
   return reduce_partials(ctx, acc, splits, m, u, nullptr);
+}
+
+int tc_product_single_eval(falkon_ctx *ctx, const Prepared &pp, const float *z, float *w32,
+                           double *u, const float *dw) {
+  return single_eval_impl(ctx, pp, z, nullptr, w32, nullptr, u, dw);
+}
+
+int tc_product_single_eval64(falkon_ctx *ctx, const Prepared &pp, const double *z, double *w64,
+                             double *u, const float *dw) {
+  return single_eval_impl(ctx, pp, nullptr, z, nullptr, w64, u, dw);
 }
 
 }  // namespace falkon

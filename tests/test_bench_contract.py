@@ -76,3 +76,38 @@ def test_roofline_single_evaluation_strips():
     assert g["bound"] == "hbm" and abs(g["achieved"] - 4 * cfg.n * cfg.m * 2 / 140e-3 / 1e9) < 1e-6
     assert not bench.single_eval_active(argparse.Namespace(path="auto", single_eval=None),
                                         synth.CONFIGS["msd"].d)
+
+
+def test_gpus_flag_spawns_ranks_reference_arm():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself as 2 ranks
+    (torch.distributed.run on 127.0.0.1); the reference arm then prints exactly ONE line
+    (rank 0) reporting n_gpus = 2."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl",
+                        "reference", "--config", "tiny", "--steps", "1", "--warmup", "1",
+                        "--oracle-seconds", "0.2"], capture_output=True, text=True, timeout=300,
+                       env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+def test_product_roofline_fraction_i():
+    """frac_product (SURVEY.md §8(d) fraction (i)): the single-evaluation roofline is the
+    tensor fp32-class rate / 2d for MSD/TIMIT, the MUFU ex2 rate for HIGGS/TAXI (tensor cross
+    term not binding) and min(FP32/(d+3), MUFU) on the SIMT path."""
+    sys.path.insert(0, ROOT)
+    import argparse
+    import bench
+    import synth
+    peaks, _ = bench.measured_peaks()
+    f = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    a = argparse.Namespace(path="auto")
+    pk, _ = bench.product_roofline(a, synth.CONFIGS["timit"], 148)
+    assert abs(pk - float(peaks["bf16_tflops"]) / 3 * 1e12 / 880) < 1.0
+    pk, _ = bench.product_roofline(a, synth.CONFIGS["higgs"], 148)
+    assert abs(pk - 148 * 16 * f) < 1.0
+    pk, _ = bench.product_roofline(argparse.Namespace(path="simt"), synth.CONFIGS["taxi"], 148)
+    assert abs(pk - min(148 * 128 * f / 12, 148 * 16 * f)) < 1.0

@@ -198,3 +198,20 @@ def test_preconditioner_schedules_agree(lib, m, d):
                 (gemm_v, la, outer)
         else:
             ref[outer] = (T, A)
+
+
+def test_fit_nonfinite_target_reports_failed_iter(ctx):
+    """Reading c9: a NaN target makes the RHS and p^T A p non-finite in the first iteration;
+    the device-side breakdown test stops CG and the call returns ENONFINITE with
+    failed_iter = 1 (never a silently NaN alpha)."""
+    from paper_2006_10350_b200 import binding
+    cfg, X, y, C = synth.make_problem("tiny")
+    y = y.copy()
+    y[123] = np.nan
+    with pytest.raises(binding.FalkonError) as ei:
+        _fit_gpu(ctx, X, y, C, G, cfg.sigma, cfg.lam, cfg.iters)
+    assert ei.value.code == 3  # FALKON_ENONFINITE
+    assert ei.value.info["failed_iter"] == 1
+    # the context stays usable afterwards
+    alpha, info = _fit_gpu(ctx, X, np.nan_to_num(y), C, G, cfg.sigma, cfg.lam, 2)
+    assert np.all(np.isfinite(alpha)) and info["iters_run"] == 2

@@ -229,3 +229,108 @@ def test_exp_offload_modes_parity(ctx, mode):
             assert rel_l2(host(u), oracle.knm_t_knm_vec(X, C, v, G, sigma)) <= TOL, sigma
     finally:
         ctx.set_option(binding.OPT_EXP_OFFLOAD, 0)
+
+
+@pytest.mark.parametrize("accum_f64,tol", [(1, 1e-12), (0, 1e-7)])
+@pytest.mark.parametrize("d,sigma", [(90, 7.0), (9, 1.0), (8, 1.0)])
+def test_sequential_shards_sum_to_full_product(ctx, accum_f64, tol, d, sigma):
+    """the row-sharded product is the sum of per-shard products (run
+    here one after another on one device through the C ABI, as G ranks would).  With fp64
+    contractions (ACCUM_F64) the shard results differ from the unsharded product only in fp64
+    summation order (1e-12); the fp32 path's per-tile fp32 partial sums group the rows by
+    shard-relative tiles, so it agrees to fp32-partial-sum level."""
+    from paper_2006_10350_b200 import binding, parallel
+    X, C, v = _problem(20_011, 900, d, seed=31)
+    ctx.set_option(binding.OPT_ACCUM_F64, accum_f64)
+    try:
+        full = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, sigma, zeros(900)))
+        for world in (2, 3, 8):
+            acc = np.zeros(900)
+            for r in range(world):
+                lo, hi = parallel.shard_range(X.shape[0], world, r)
+                acc += host(ctx.knm_matvec(dev(X[lo:hi]), dev(C), dev(v), G, sigma, zeros(900)))
+            assert rel_l2(acc, full) <= tol, world
+    finally:
+        ctx.set_option(binding.OPT_ACCUM_F64, 0)
+
+
+def test_tensor_range_guard_falls_back_to_simt(ctx):
+    """coordinates or folded biases beyond the fp16 range of the tensor path's
+    hi/lo split would turn whole rows into NaN.  The packing kernel flags them and the product
+    runs on the fp32 SIMT kernels instead: finite, and bit-identical to the forced SIMT path."""
+    from paper_2006_10350_b200 import binding
+    X, C, v = _problem(3000, 400, 90, seed=32, scale=400.0)  # ||x~||^2 ~ 2e7 >> fp16 max
+    u = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 1.0, zeros(400)))
+    ctx.set_option(binding.OPT_PATH, binding.PATH_SIMT)
+    try:
+        us = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 1.0, zeros(400)))
+    finally:
+        ctx.set_option(binding.OPT_PATH, binding.PATH_AUTO)
+    assert np.all(np.isfinite(u))
+    assert np.array_equal(u, us)
+
+
+def test_ts_variant_with_multi_vector_and_strip(ctx):
+    """ADVICE r1: with FALKON_TC_TS=1 the 192-row TS tensor maps must only feed the TS kernel;
+    the multi-vector (kv = 16) and single-evaluation kernels keep 256-row Q boxes."""
+    import os
+    from paper_2006_10350_b200 import binding
+    X, C, v = _problem(4000, 600, 90, seed=33)
+    V = np.random.default_rng(3).standard_normal((600, 16))
+    ref_u = oracle.knm_t_knm_vec(X, C, v, G, 7.0)
+    os.environ["FALKON_TC_TS"] = "1"
+    try:
+        u = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 7.0, zeros(600)))
+        U = host(ctx.knm_matmat(dev(X), dev(C), dev(V), G, 7.0, zeros(600 * 16).reshape(600, 16)))
+        ctx.set_option(binding.OPT_SINGLE_EVAL, 1)
+        us = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, 7.0, zeros(600)))
+    finally:
+        del os.environ["FALKON_TC_TS"]
+        ctx.set_option(binding.OPT_SINGLE_EVAL, 2)
+    assert rel_l2(u, ref_u) <= TOL
+    assert rel_l2(us, ref_u) <= TOL
+    for c in (0, 7, 15):
+        assert rel_l2(U[:, c], oracle.knm_t_knm_vec(X, C, V[:, c], G, 7.0)) <= TOL
+
+
+def test_binding_rejects_wrong_sizes_and_devices(ctx):
+    """the C ABI trusts sizes, so the binding checks them (a short output would be
+    written past its end)."""
+    X, C, v = _problem(500, 50, 9, seed=34)
+    with pytest.raises(ValueError):
+        ctx.knm_matvec(dev(X), dev(C), dev(v), G, 1.0, zeros(49))
+    with pytest.raises(ValueError):
+        ctx.knm_matvec(dev(X), dev(C), dev(v[:40]), G, 1.0, zeros(50))
+    with pytest.raises(ValueError):
+        ctx.kernel_vec(dev(X), dev(C), dev(v), G, 1.0, np.zeros(499))
+    with pytest.raises(ValueError):
+        ctx.fit(dev(X), dev(np.zeros(499, np.float32)), dev(C), G, 1.0, 1e-3, 2, zeros(50))
+
+
+def test_stuck_pipeline_traps_and_reports_ecuda():
+    """A tcgen05 pipeline wait that never completes must not hang the GPU: mbar_wait_safe traps
+    after ~4 s of clock64 time, the kernel aborts, and the library call returns FALKON_ECUDA
+    (the CUDA context is then unusable - a sticky error - so this runs in a subprocess).
+    Fault injected with the diagnostic FALKON_TC_MODE=12 (a stage is never filled)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, ".")
+from paper_2006_10350_b200 import binding
+ctx = binding.Context(0)
+X = np.random.default_rng(0).standard_normal((2000, 90)).astype(np.float32)
+C = X[:300].copy()
+u = np.zeros(300)
+try:
+    ctx.knm_matvec(X, C, np.ones(300), binding.GAUSSIAN, 7.0, u)
+    print("NO-ERROR")
+except binding.FalkonError as e:
+    print("CODE", e.code, str(e)[:200])
+'''
+    env = dict(os.environ, FALKON_TC_MODE="12")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
+                       env=env, cwd=root)
+    assert "CODE 5" in r.stdout, (r.stdout, r.stderr[-1000:])
