@@ -92,12 +92,15 @@ enum {
   FALKON_OPT_LOOKAHEAD = 11,    /* blocked Cholesky: 1 (default) = the next outer panel's
                                    factorisation runs on a high-priority stream while the bulk of
                                    the trailing update runs on a low-priority one; 0 = serial */
-  FALKON_OPT_ACCUM_F64 = 12     /* precision of the two contractions (SURVEY.md §7 hard part 3):
+  FALKON_OPT_ACCUM_F64 = 12,    /* precision of the two contractions (SURVEY.md §7 hard part 3):
                                    0 = fp32 v and w, fp32 partial sums flushed to fp64 per tile;
                                    1 = fp64 v and w, each exact product k(x,c) * v accumulated by
                                    DFMA in fp64 (k itself stays fp32).  Applies to the single-vector
                                    products, fits, GSC fits and predictions; multi-output calls
                                    stay fp32.  See DESIGN.md for the measured default. */
+  FALKON_OPT_DIST_PRECOND = 13  /* 1: build the preconditioner with the distributed schedule
+                                   (NEXT-1, below) even on a 1-rank NCCL communicator (tests the
+                                   broadcast path on one GPU).  With world > 1 it is always used. */
 };
 
 /* Per-launch-class accumulated device times in ms (falkon_ctx_timings). */
@@ -188,6 +191,21 @@ int falkon_precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, 
                          double sigma, double lambda, double jitter,
                          double *P, double *diagT, double *diagA, double *work,
                          falkon_fit_info *info);
+
+/* Distributed preconditioner build (multi-GPU Cholesky of PAPER.md:460-469,
+   App. C Alg. 3/4 PAPER.md:1073-1216), here with G ranks SIMULATED in this process on the
+   context's device: rank r's buffers are P[r] (m x m), diagT[r], diagA[r] (m) and work[r]
+   (falkon_precond_work_elems(m)), all device memory, arrays of G host-side pointers.
+   Schedule (also what falkon_fit runs across real ranks when world > 1): outer panel j of
+   each factor (potrf_outer x 128 columns) belongs to rank j mod G; its owner factors it, the
+   factored panel is broadcast, and every rank applies the trailing update to its own column
+   panels; the LAUUM T T^T/m is split by the same column panels.  Every rank ends with the same
+   bits as falkon_precond_build (same GEMM calls per element).  Errors as
+   falkon_precond_build; EINVAL for G outside 1..64. */
+int falkon_precond_build_sim(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel,
+                             double sigma, double lambda, double jitter, int G, double *const *P,
+                             double *const *diagT, double *const *diagA, double *const *work,
+                             falkon_fit_info *info);
 
 /* In-place triangular solve x <- op(F)^-1 x with F = T (which = 0) or A (which = 1) read
    from a buffer built by falkon_precond_build (with its work buffer); op = transpose if

@@ -286,7 +286,7 @@ def preconditioner(C, kernel: int, sigma: float, lam: float, jitter: float = DEF
     except np.linalg.LinAlgError:
         raise NotPositiveDefinite(0) from None
     del K
-    M = T @ T.T
+    M = _upper_times_transpose(T)
     M /= m
     M[diag, diag] += lam
     try:
@@ -294,6 +294,22 @@ def preconditioner(C, kernel: int, sigma: float, lam: float, jitter: float = DEF
     except np.linalg.LinAlgError:
         raise NotPositiveDefinite(1) from None
     return T, A
+
+
+def _upper_times_transpose(T: np.ndarray, nb: int = CHOL_NB) -> np.ndarray:
+    """T T^T for upper-triangular T, by nb x nb blocks (numpy's whole-matrix T @ T.T
+    segfaults in its BLAS for m > 46,340, see CHOL_NB): block (I, J), J <= I, is
+    T[I, i0:] @ T[J, i0:]^T (the columns k < i0 of T[I, :] are exact zeros), mirrored."""
+    m = T.shape[0]
+    M = np.empty((m, m), dtype=np.float64)
+    for i0 in range(0, m, nb):
+        i1 = min(m, i0 + nb)
+        for j0 in range(0, i1, nb):
+            j1 = min(m, j0 + nb)
+            blk = T[i0:i1, i0:] @ T[j0:j1, i0:].T
+            M[i0:i1, j0:j1] = blk
+            M[j0:j1, i0:i1] = blk.T
+    return M
 
 
 def _solve_upper(U, b, trans: bool, nb: int = CHOL_NB):

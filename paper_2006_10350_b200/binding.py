@@ -24,7 +24,7 @@ PATH_AUTO, PATH_SIMT, PATH_TENSOR = 0, 1, 2
 OPT_PATH, OPT_TC_MIN_D, OPT_TC_TERMS, OPT_KERNEL_TIMING, OPT_EXP_OFFLOAD = 1, 2, 3, 4, 5
 OPT_POTRF_OUTER, OPT_GEMM_WARPS = 6, 7
 OPT_SINGLE_EVAL, OPT_STRIP_BYTES, OPT_TC_CLUSTER, OPT_LOOKAHEAD = 8, 9, 10, 11
-OPT_ACCUM_F64 = 12
+OPT_ACCUM_F64, OPT_DIST_PRECOND = 12, 13
 SINGLE_EVAL_OFF, SINGLE_EVAL_ON, SINGLE_EVAL_AUTO = 0, 1, 2
 TIMING_NAMES = ["prep", "pass_a", "pass_b", "reduce", "allreduce", "precond", "trsv", "vec"]
 
@@ -35,7 +35,7 @@ ERRORS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ENONFINITE", 4: "ENOMEM", 5: "E
 EXPORTS = ["falkon_get_unique_id", "falkon_ctx_create", "falkon_ctx_destroy",
            "falkon_ctx_set_stream", "falkon_ctx_set_option", "falkon_ctx_timings",
            "falkon_ctx_launch_count", "falkon_knm_matvec", "falkon_kernel_vec",
-           "falkon_kernel_tvec", "falkon_precond_work_elems", "falkon_precond_build", "falkon_precond_solve", "falkon_precond_solve_multi", "falkon_fit",
+           "falkon_kernel_tvec", "falkon_precond_work_elems", "falkon_precond_build", "falkon_precond_build_sim", "falkon_precond_solve", "falkon_precond_solve_multi", "falkon_fit",
            "falkon_predict", "falkon_gsc_fit", "falkon_knm_matmat", "falkon_predict_multi",
            "falkon_fit_multi", "falkon_strerror", "falkon_last_error",
            "falkon_version"]
@@ -88,6 +88,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "falkon_kernel_tvec": (C, [P, P, I64, I64, P, I64, C, D, P, P]),
         "falkon_precond_work_elems": (I64, [I64]),
         "falkon_precond_build": (C, [P, P, I64, I64, C, D, D, D, P, P, P, P, P]),
+        "falkon_precond_build_sim": (C, [P, P, I64, I64, C, D, D, D, C, P, P, P, P, P]),
         "falkon_precond_solve": (C, [P, P, P, P, P, I64, C, C, P]),
         "falkon_precond_solve_multi": (C, [P, P, P, P, P, I64, C, C, P, I64, I64]),
         "falkon_fit": (C, [P, P, P, I64, I64, P, I64, C, D, D, I32, D, P, P]),
@@ -258,6 +259,25 @@ class Context:
                                          self._v(work, "float64", "work",
                                                  self.precond_work_elems(m)),
                                          ctypes.byref(info))
+        if code != 0:
+            e = FalkonError(code, (_LIB.falkon_last_error() or b"").decode())
+            e.info = info.as_dict()
+            raise e
+        return info.as_dict()
+
+    def precond_build_sim(self, C, kernel, sigma, lam, jitter, Ps, diagTs, diagAs, works) -> dict:
+        """Distributed (NEXT-1) build with G = len(Ps) ranks simulated on this device."""
+        m, d = C.shape
+        G = len(Ps)
+        if not (len(diagTs) == len(diagAs) == len(works) == G):
+            raise ValueError("need G buffers of each kind")
+        arr = lambda xs, name, n: (ctypes.c_void_p * G)(*[self._v(x, "float64", name, n) for x in xs])
+        info = FitInfo()
+        code = _LIB.falkon_precond_build_sim(
+            self.h, self._v(C, "float32", "C", m * d), m, d, _kernel_id(kernel), float(sigma),
+            float(lam), float(jitter), G, arr(Ps, "P", m * m), arr(diagTs, "diagT", m),
+            arr(diagAs, "diagA", m), arr(works, "work", self.precond_work_elems(m)),
+            ctypes.byref(info))
         if code != 0:
             e = FalkonError(code, (_LIB.falkon_last_error() or b"").decode())
             e.info = info.as_dict()

@@ -572,6 +572,9 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
       if (value != 0 && value != 1) return fail(FALKON_EINVAL, "accum_f64 must be 0 or 1");
       ctx->opt.accum_f64 = (int)value;
       return FALKON_OK;
+    case FALKON_OPT_DIST_PRECOND:
+      ctx->opt.dist_precond = value ? 1 : 0;
+      return FALKON_OK;
     case FALKON_OPT_TC_CLUSTER:
       if (value != 1 && value != 2) return fail(FALKON_EINVAL, "tc_cluster must be 1 or 2");
       ctx->opt.tc_cluster = (int)value;
@@ -791,6 +794,25 @@ int falkon_precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, 
   FK_TRY(stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd));
   return precond_build(ctx, (const float *)Cd, m, d, kernel, sigma, lambda, jitter, P, diagT, diagA,
                        work, info);
+}
+
+int falkon_precond_build_sim(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel,
+                             double sigma, double lambda, double jitter, int G, double *const *P,
+                             double *const *diagT, double *const *diagA, double *const *work,
+                             falkon_fit_info *info) {
+  FK_TRY(check_common(ctx, 0, d, m, kernel, sigma));
+  if (!C || !P || !diagT || !diagA || !work) return fail(FALKON_EINVAL, "NULL array");
+  if (G < 1 || G > 64) return fail(FALKON_EINVAL, "G must be 1..64");
+  if (!(lambda >= 0.0) || !std::isfinite(lambda)) return fail(FALKON_EINVAL, "lambda must be >= 0");
+  for (int r = 0; r < G; ++r)
+    if (!P[r] || !diagT[r] || !diagA[r] || !work[r] || !is_device_ptr(P[r]) ||
+        !is_device_ptr(diagT[r]) || !is_device_ptr(diagA[r]) || !is_device_ptr(work[r]))
+      return fail(FALKON_EINVAL, "P, diagT, diagA, work of every rank must be device memory");
+  if (jitter < 0) jitter = 1e-8;
+  const void *Cd;
+  FK_TRY(stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd));
+  return precond_build_sim(ctx, (const float *)Cd, m, d, kernel, sigma, lambda, jitter, G, P, diagT,
+                           diagA, work, info);
 }
 
 int falkon_precond_solve(falkon_ctx *ctx, const double *P, const double *diagT, const double *diagA,

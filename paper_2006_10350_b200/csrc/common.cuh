@@ -68,6 +68,8 @@ enum WsSlot {
   WS_KSTRIP,      // fp32 k strip of the single-evaluation product [rows][ldk]
   WS_SE_ACC,      // fp64 [splits][m] accumulators of the strip GEMV
   WS_V64,         // fp64 m_pad: v zero-padded (ACCUM_F64 pass-A input)
+  WS_DIST_STAGE,  // fp64 m x NBO: packed A panel of the distributed preconditioner (NEXT-1)
+  WS_SIM_FLAGS,   // pivot-failure words of the simulated ranks (precond_build_sim)
   WS_COUNT
 };
 
@@ -94,6 +96,7 @@ struct Options {
                         // MSD 21.7 -> 20.9 ms, TIMIT 431 -> 424 ms), or 1 CTA
   int64_t strip_bytes = (int64_t)16 << 30;
   int accum_f64 = 0;    // FALKON_OPT_ACCUM_F64: fp64 v / w with DFMA contractions
+  int dist_precond = 0; // FALKON_OPT_DIST_PRECOND: distributed build even on a 1-rank communicator
 };
 
 }  // namespace falkon
@@ -151,6 +154,8 @@ int nccl_comm_init(falkon_ctx *ctx, const unsigned char *id);
 int nccl_comm_destroy(falkon_ctx *ctx);
 int nccl_allreduce_f64(falkon_ctx *ctx, double *buf, int64_t count);
 int nccl_allreduce_i64(falkon_ctx *ctx, int64_t *buf, int64_t count);
+int nccl_allreduce_min_u64(falkon_ctx *ctx, unsigned long long *buf, int64_t count);
+int nccl_broadcast_bytes(falkon_ctx *ctx, void *buf, size_t bytes, int root);
 
 // ------------------------------------------------------------------ product path (kvp.cu)
 struct Prepared {
@@ -237,6 +242,12 @@ int precond_build_T(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int k
 int precond_build_A(falkon_ctx *ctx, int64_t m, double lambda, const double *dscale, double *P,
                     double *diagT, double *diagA, double *work, double jitter,
                     falkon_fit_info *info);
+// NEXT-1 test entry: the distributed (1D block-cyclic) build with G ranks simulated in this
+// process, rank r's buffers P[r], diagT[r], diagA[r], work[r] (device memory)
+int precond_build_sim(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel,
+                      double sigma, double lambda, double jitter, int G, double *const *P,
+                      double *const *diagT, double *const *diagA, double *const *work,
+                      falkon_fit_info *info);
 // z = T^T (T x) = (Kmm + delta I) x from the factored buffer; tmp: m doubles
 int trmv_TtT(falkon_ctx *ctx, const double *P, const double *diagT, int64_t m, const double *x,
              double *tmp, double *z);

@@ -268,6 +268,14 @@ struct TcArgs {
   int64_t p_base;  // first P row of this launch (TMA row coordinate offset; 0 = all rows)
   float *kst;      // single-evaluation strip: k values stored row-major [np][ldk] (or null)
   int64_t ldk;
+  // fused strip GEMV (KST launches, warps 2-3): u (gacc, fp64 m) += previous strip^T w
+  const float *gK;     // previous strip's k values (null: no fused GEMV)
+  const void *gw;      // its rows' w (fp32, or fp64 when ZD)
+  const float *gdw;    // GSC row weights (or null)
+  int64_t grows, gm;   // rows of the previous strip, centres (= ldk)
+  double *gacc;
+  int gfirst;          // 1: overwrite gacc (first strip)
+  int gslots;          // bulk-copy ring slots per GEMV warp
 };
 
 constexpr int TC_EPI_WARPS = 8;   // 2 per SM sub-partition: (TMEM lane group, column half)
@@ -443,6 +451,282 @@ __device__ __forceinline__ void tc_mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, 
 // smem (matrix descriptor) -> TMEM copy of one 128-row x 16-fp16 chunk (8 TMEM columns)
 __device__ __forceinline__ void tc_cp_128x256b(uint32_t tmem_dst, uint64_t sdesc) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmem_dst), "l"(sdesc));
+}
+
+// ------------------------------------------------------------------ strip GEMV pieces (NEXT-4)
+constexpr int SE_WARPS = 8;
+constexpr int SE_CPW = 8;                     // centres per warp
+constexpr int SE_COLS = SE_WARPS * SE_CPW;    // centres per CTA
+constexpr int SE_FLUSH = 32;                  // tiles per fp32 partial (4 x 32 = 128 terms)
+// The rows' weights of one tile for lane l (rows r..r+3): w (fp32, or fp64 under WD) times the
+// GSC row weights dw when dw != null (Knm^T D Knm, Alg. 2; as scale_rows_kernel); rows >= `rows`
+// contribute 0.
+__device__ __forceinline__ float4 gemv_w32(const float *__restrict__ w, const float *__restrict__ dw,
+                                           int64_t r, int64_t rows) {
+  float4 wv;
+  if (r + 3 < rows) {
+    wv = __ldg(reinterpret_cast<const float4 *>(w + r));
+    if (dw) {
+      const float4 dd = __ldg(reinterpret_cast<const float4 *>(dw + r));
+      wv.x *= dd.x, wv.y *= dd.y, wv.z *= dd.z, wv.w *= dd.w;
+    }
+  } else {
+    wv.x = r < rows ? w[r] * (dw ? dw[r] : 1.f) : 0.f;
+    wv.y = r + 1 < rows ? w[r + 1] * (dw ? dw[r + 1] : 1.f) : 0.f;
+    wv.z = r + 2 < rows ? w[r + 2] * (dw ? dw[r + 2] : 1.f) : 0.f;
+    wv.w = 0.f;
+  }
+  return wv;
+}
+__device__ __forceinline__ double4 gemv_w64(const double *__restrict__ wd, const float *__restrict__ dw,
+                                            int64_t r, int64_t rows) {
+  const double2 wa = __ldg(reinterpret_cast<const double2 *>(wd + r));  // zero-padded to the tile
+  const double2 wb = __ldg(reinterpret_cast<const double2 *>(wd + r + 2));
+  double4 w4;
+  w4.x = r < rows ? wa.x : 0.0;
+  w4.y = r + 1 < rows ? wa.y : 0.0;
+  w4.z = r + 2 < rows ? wb.x : 0.0;
+  w4.w = r + 3 < rows ? wb.y : 0.0;
+  if (dw) {
+    w4.x *= r < rows ? (double)dw[r] : 0.0;
+    w4.y *= r + 1 < rows ? (double)dw[r + 1] : 0.0;
+    w4.z *= r + 2 < rows ? (double)dw[r + 2] : 0.0;
+    w4.w *= r + 3 < rows ? (double)dw[r + 3] : 0.0;
+  }
+  return w4;
+}
+
+// One warp's share of u += strip^T w: the SE_CPW centres jb.. (clamped to m - 1; duplicates are
+// discarded by the caller) over the strip's tiles [t0, t1).  Lane l reads the centre's 128
+// values of a tile as one 512-byte float4 load and multiplies them by w of rows 4l..4l+3.
+// PF: the next tile's loads are issued before this tile's FMAs (two tiles in flight; the
+// standalone kernel; the fused warps share the pass-A kernel's register budget and do not).
+// fp32 sums of <= 128 terms are flushed into fp64 (reading c12); WD: fp64 w, exact products by
+// DFMA.  Returns, in lane c < SE_CPW, the fp64 sum of centre jb + c (fixed order).
+template <bool WD, bool PF>
+__device__ __forceinline__ double strip_gemv_group(const float *__restrict__ K, int64_t ldk,
+                                                   const void *__restrict__ wv,
+                                                   const float *__restrict__ dw, int64_t rows,
+                                                   int64_t t0, int64_t t1, int64_t m, int64_t jb,
+                                                   int lane) {
+  const float *w = reinterpret_cast<const float *>(wv);
+  const double *wd = reinterpret_cast<const double *>(wv);
+  int jc[SE_CPW];  // centre offsets (m < 2^31)
+#pragma unroll
+  for (int c = 0; c < SE_CPW; ++c) jc[c] = (int)lmin(jb + c, m - 1) * TC_M;
+  double a64[SE_CPW];
+  float a32[SE_CPW];
+#pragma unroll
+  for (int c = 0; c < SE_CPW; ++c) a64[c] = 0.0, a32[c] = 0.f;
+  float4 kq[SE_CPW];
+  if (PF && t0 < t1) {
+    const float *kt = K + t0 * ldk * TC_M + 4 * lane;
+#pragma unroll
+    for (int c = 0; c < SE_CPW; ++c) kq[c] = __ldcs(reinterpret_cast<const float4 *>(kt + jc[c]));
+  }
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t r = t * TC_M + 4 * lane;
+    float4 kn[SE_CPW];
+    if (PF) {
+      if (t + 1 < t1) {  // prefetch the next tile
+        const float *kt = K + (t + 1) * ldk * TC_M + 4 * lane;
+#pragma unroll
+        for (int c = 0; c < SE_CPW; ++c) kn[c] = __ldcs(reinterpret_cast<const float4 *>(kt + jc[c]));
+      }
+    } else {
+      const float *kt = K + t * ldk * TC_M + 4 * lane;
+#pragma unroll
+      for (int c = 0; c < SE_CPW; ++c) kq[c] = __ldcs(reinterpret_cast<const float4 *>(kt + jc[c]));
+    }
+    if (WD) {
+      const double4 w4 = gemv_w64(wd, dw, r, rows);
+#pragma unroll
+      for (int c = 0; c < SE_CPW; ++c) {
+        double s = a64[c];
+        s = fma(k_to_f64(kq[c].x), w4.x, s);
+        s = fma(k_to_f64(kq[c].y), w4.y, s);
+        s = fma(k_to_f64(kq[c].z), w4.z, s);
+        a64[c] = fma(k_to_f64(kq[c].w), w4.w, s);
+      }
+    } else {
+      const float4 w4 = gemv_w32(w, dw, r, rows);
+#pragma unroll
+      for (int c = 0; c < SE_CPW; ++c) {
+        float s = a32[c];
+        s = fmaf(kq[c].x, w4.x, s);
+        s = fmaf(kq[c].y, w4.y, s);
+        s = fmaf(kq[c].z, w4.z, s);
+        a32[c] = fmaf(kq[c].w, w4.w, s);
+      }
+      if ((t - t0) % SE_FLUSH == SE_FLUSH - 1) {
+#pragma unroll
+        for (int c = 0; c < SE_CPW; ++c) a64[c] += (double)a32[c], a32[c] = 0.f;
+      }
+    }
+    if (PF && t + 1 < t1) {
+#pragma unroll
+      for (int c = 0; c < SE_CPW; ++c) kq[c] = kn[c];
+    }
+  }
+  double out = 0.0;
+#pragma unroll
+  for (int c = 0; c < SE_CPW; ++c) {
+    double v = a64[c] + (double)a32[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == c) out = v;
+  }
+  return out;
+}
+
+// Standalone strip GEMV: grid (centre blocks of SE_COLS) x (tile splits); one fp64 accumulator
+// row per split (first: overwrite, else add).  No atomics: deterministic.
+template <bool WEIGHTED, bool WD = false>
+__global__ void __launch_bounds__(32 * SE_WARPS) se_gemv_kernel(const float *__restrict__ K, int64_t ldk,
+                                                                const void *__restrict__ wv,
+                                                                const float *__restrict__ dw, int64_t rows,
+                                                                int64_t tiles_per_split, int64_t m,
+                                                                double *__restrict__ acc, int first) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t jb = (int64_t)blockIdx.x * SE_COLS + warp * SE_CPW;
+  if (jb >= m) return;
+  const int64_t ntile = cdiv<int64_t>(rows, TC_M);
+  const int64_t t0 = (int64_t)blockIdx.y * tiles_per_split;
+  const int64_t t1 = lmin(ntile, t0 + tiles_per_split);
+  const double v = strip_gemv_group<WD, true>(K, ldk, wv, WEIGHTED ? dw : nullptr, rows, t0, t1, m,
+                                              jb, lane);
+  const int64_t j = jb + lane;
+  if (lane < SE_CPW && j < m) {
+    double *o = acc + (int64_t)blockIdx.y * m + j;
+    *o = first ? v : *o + v;
+  }
+}
+
+// Fused strip GEMV (warps 2 and 3 of a single-evaluation pass-A CTA, idle otherwise): while
+// the tensor pipe evaluates strip s, these warps stream strip s - 1 (the other k buffer) from
+// HBM.  The launch's CTAs partition the centres: CTA c owns centre groups [c G / N, (c+1) G / N)
+// of SE_CPW centres over ALL tiles of the previous strip, so every u_j has one writer.
+// The warps hold no loads in registers: lane 0 keeps FG_SLOTS bulk copies (TMA engine, one
+// 4 KB k block [8 centres][128 rows] + the tile's w per slot) in flight into a shared-memory
+// ring per warp, and the warp consumes a slot with LDS once its mbarrier completes (the
+// register-staged loop reached only ~1.1 TB/s beside pass A: too few bytes in flight).
+constexpr int FG_MAX_SLOTS = 8;                      // ring slots per GEMV warp (at most)
+constexpr int FG_KB = SE_CPW * TC_M * 4;             // 4 KB of k per slot
+constexpr int FG_SLOT = FG_KB + TC_M * 8;            // + w of the tile (fp64 room)
+static inline int fg_ring_bytes(int slots) { return 128 + 128 + 2 * slots * FG_SLOT; }
+template <bool WD>
+__device__ __forceinline__ void fused_strip_gemv(const TcArgs &a, int wid, int lane,
+                                                 uint8_t *ring_base) {
+  const int FG_SLOTS = a.gslots;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(ring_base) + wid * FG_MAX_SLOTS;
+  uint8_t *ring = ring_base + 128 + wid * FG_SLOTS * FG_SLOT;
+  const int64_t nct = (int64_t)gridDim.x * gridDim.y;
+  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const int64_t ng = cdiv<int64_t>(a.gm, SE_CPW);
+  const int64_t g0 = cta * ng / nct, g1 = (cta + 1) * ng / nct;
+  const int64_t ntile = cdiv<int64_t>(a.grows, TC_M);
+  const int wb = WD ? 8 : 4;  // bytes per w element
+  // this warp's items: (group g, tile t) for g = g0 + wid, g0 + wid + 2, ... and all t
+  const int64_t my_groups = g1 > g0 + wid ? (g1 - g0 - wid + 1) / 2 : 0;
+  const int64_t nitems = my_groups * ntile;
+  if (nitems == 0) return;
+  if (lane == 0)
+    for (int s = 0; s < FG_SLOTS; ++s) mbar_init(&bar[s], 1);
+  fence_mbar_init();
+  __syncwarp();
+  auto issue = [&](int64_t it) {  // lane 0
+    const int64_t g = g0 + wid + 2 * (it / ntile), t = it % ntile;
+    const int64_t jb = g * SE_CPW;
+    const int s = (int)(it % FG_SLOTS);
+    const uint32_t kb = (uint32_t)(lmin(SE_CPW, a.gm - jb) * TC_M * 4);
+    const uint32_t wbytes = (uint32_t)(TC_M * wb);  // w rows are zero-padded past the strip
+    mbar_expect_tx(&bar[s], kb + wbytes);
+    bulk_g2s(ring + s * FG_SLOT, a.gK + (t * a.gm + jb) * TC_M, kb, &bar[s]);
+    bulk_g2s(ring + s * FG_SLOT + FG_KB, (const uint8_t *)a.gw + t * TC_M * wb, wbytes, &bar[s]);
+  };
+  if (lane == 0)
+    for (int64_t it = 0; it < lmin(FG_SLOTS, nitems); ++it) issue(it);
+  double a64[SE_CPW];
+  float a32[SE_CPW];
+  for (int64_t it = 0; it < nitems; ++it) {
+    const int64_t t = it % ntile;
+    const int64_t jb = (g0 + wid + 2 * (it / ntile)) * SE_CPW;
+    if (t == 0) {
+#pragma unroll
+      for (int c = 0; c < SE_CPW; ++c) a64[c] = 0.0, a32[c] = 0.f;
+    }
+    const int s = (int)(it % FG_SLOTS);
+    mbar_wait_safe(&bar[s], (uint32_t)((it / FG_SLOTS) & 1));
+    const uint8_t *slot = ring + s * FG_SLOT;
+    const int nval = (int)lmin(SE_CPW, a.gm - jb);  // valid centres in this block
+    const int64_t r = t * TC_M + 4 * lane;
+    float4 kq[SE_CPW];
+#pragma unroll
+    for (int c = 0; c < SE_CPW; ++c)
+      kq[c] = c < nval ? lds128(reinterpret_cast<const float *>(slot) + c * TC_M + 4 * lane)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (WD) {
+      const double *ws = reinterpret_cast<const double *>(slot + FG_KB) + 4 * lane;
+      double4 w4;
+      w4.x = r < a.grows ? ws[0] : 0.0;
+      w4.y = r + 1 < a.grows ? ws[1] : 0.0;
+      w4.z = r + 2 < a.grows ? ws[2] : 0.0;
+      w4.w = r + 3 < a.grows ? ws[3] : 0.0;
+      if (a.gdw) {
+        w4.x *= r < a.grows ? (double)a.gdw[r] : 0.0;
+        w4.y *= r + 1 < a.grows ? (double)a.gdw[r + 1] : 0.0;
+        w4.z *= r + 2 < a.grows ? (double)a.gdw[r + 2] : 0.0;
+        w4.w *= r + 3 < a.grows ? (double)a.gdw[r + 3] : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < SE_CPW; ++c) {
+        double acc = a64[c];
+        acc = fma(k_to_f64(kq[c].x), w4.x, acc);
+        acc = fma(k_to_f64(kq[c].y), w4.y, acc);
+        acc = fma(k_to_f64(kq[c].z), w4.z, acc);
+        a64[c] = fma(k_to_f64(kq[c].w), w4.w, acc);
+      }
+    } else {
+      float4 w4 = lds128(reinterpret_cast<const float *>(slot + FG_KB) + 4 * lane);
+      w4.x = r < a.grows ? w4.x : 0.f;
+      w4.y = r + 1 < a.grows ? w4.y : 0.f;
+      w4.z = r + 2 < a.grows ? w4.z : 0.f;
+      w4.w = r + 3 < a.grows ? w4.w : 0.f;
+      if (a.gdw) {
+        w4.x *= r < a.grows ? a.gdw[r] : 0.f;
+        w4.y *= r + 1 < a.grows ? a.gdw[r + 1] : 0.f;
+        w4.z *= r + 2 < a.grows ? a.gdw[r + 2] : 0.f;
+        w4.w *= r + 3 < a.grows ? a.gdw[r + 3] : 0.f;
+      }
+#pragma unroll
+      for (int c = 0; c < SE_CPW; ++c) {
+        float acc = a32[c];
+        acc = fmaf(kq[c].x, w4.x, acc);
+        acc = fmaf(kq[c].y, w4.y, acc);
+        acc = fmaf(kq[c].z, w4.z, acc);
+        a32[c] = fmaf(kq[c].w, w4.w, acc);
+      }
+      if (t % SE_FLUSH == SE_FLUSH - 1) {
+#pragma unroll
+        for (int c = 0; c < SE_CPW; ++c) a64[c] += (double)a32[c], a32[c] = 0.f;
+      }
+    }
+    // the slot's values are consumed (used by the FMAs above): refill it
+    __syncwarp();
+    if (lane == 0 && it + FG_SLOTS < nitems) issue(it + FG_SLOTS);
+    if (t == ntile - 1) {  // group done: fixed-order warp reduction, one writer per centre
+      double out = 0.0;
+#pragma unroll
+      for (int c = 0; c < SE_CPW; ++c) {
+        double v = a64[c] + (double)a32[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == c) out = v;
+      }
+      const int64_t j = jb + lane;
+      if (lane < SE_CPW && j < a.gm) a.gacc[j] = a.gfirst ? out : a.gacc[j] + out;
+    }
+  }
 }
 
 // NT: Q rows per MMA tile (accumulator columns).  TS: the resident P tile is copied once
@@ -658,6 +942,14 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       if (elect_one()) tc_commit(&tfull[acc]);
       __syncwarp();
     }
+  } else if (KST && KV == 1 && (warp == 2 || warp == 3)) {
+    // fused strip GEMV of the previous strip (single evaluation): warp 2 has allocated TMEM
+    // above and is otherwise idle until the dealloc at the end; warp 3 is idle
+    if (a.gK) {
+      uint8_t *gring = reinterpret_cast<uint8_t *>(
+          (reinterpret_cast<uintptr_t>(red + TC_M * (KV > 3 ? KV : 3)) + 127) & ~uintptr_t(127));
+      fused_strip_gemv<ZD>(a, warp - 2, lane, gring);
+    }
   } else if (KV > 1 && warp >= 4) {
     // multi-vector epilogue: thread = P row; the Q tile's z block ([NT][KV] fp32) arrives in
     // shared memory by the producer's bulk copy (double-buffered, mbarrier per buffer), KV/2
@@ -859,8 +1151,8 @@ static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
 int tc_range_flag(falkon_ctx *ctx, int **flag, bool reset) {
   void *p;
   FK_TRY(ws_get(ctx, WS_FLAGS, 64, &p));
-  *flag = (int *)p;
-  if (reset) FK_CUDA(cudaMemsetAsync(p, 0, sizeof(int), ctx->stream));
+  *flag = (int *)((char *)p + 32);  // bytes 0-15: the preconditioner's pivot-failure words
+  if (reset) FK_CUDA(cudaMemsetAsync(*flag, 0, sizeof(int), ctx->stream));
   return FALKON_OK;
 }
 int tc_range_check(falkon_ctx *ctx, bool *bad) {
@@ -972,10 +1264,22 @@ static int64_t tc_cluster_slots(falkon_ctx *ctx, const void *fn, int threads, si
 
 // One fused pass over P rows [p_begin, p_begin + p_count) (p_count < 0: all).  kst != null
 // (pass A, kv = 1): the k values are also stored row-major into kst[(p - p_begin) * ldk + q].
+// Fused GEMV of the previous strip (single evaluation; see fused_strip_gemv).
+struct FusedGemv {
+  const float *K = nullptr;  // previous strip's k values [tile][ldk][128]
+  const void *w = nullptr;   // its rows' w (fp32, or fp64 with z64)
+  const float *dw = nullptr;
+  int64_t rows = 0;
+  double *acc = nullptr;     // u (fp64 m)
+  int first = 0;
+};
+
 // z64 != null: fp64 z and DFMA contractions (ACCUM_F64, kv 1, MODE 0); out64 is then required.
+// fg (kst launches only): warps 2-3 also run the GEMV of the previous strip.
 static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const float *z,
                      double *out64, float *out32, int kv, int64_t p_begin, int64_t p_count,
-                     float *kst, int64_t ldk, const double *z64 = nullptr) {
+                     float *kst, int64_t ldk, const double *z64 = nullptr,
+                     const FusedGemv *fg = nullptr) {
   const CUtensorMap *maps = reinterpret_cast<const CUtensorMap *>(pp.tmaps);
   const int d16 = pp.dq;
   const bool stream = tc_stream(pp.d);
@@ -991,11 +1295,24 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
   const int nt = ts ? TC_N_TS : TC_N;
   // streaming: stages of 48 KB (P and Q boxes of both segments, 32 wide) — 4 fit
   const size_t sstage = (size_t)2 * (TC_M + TC_N) * TC_SBK * 2;
+  // single-evaluation launches reserve the fused GEMV's bulk-copy rings after the tail: at least
+  // 3 slots per GEMV warp, the rest of shared memory beyond the pass-A ring (up to 8 slots)
+  const bool fgr = kst && fg;  // fused GEMV in this launch
+  const size_t gmin = fgr ? (size_t)fg_ring_bytes(3) : 0;
   int sst = TC_MAX_STAGES;
-  while (sst > 2 && 1024 + sst * sstage + 256 + tc_tail_bytes(nt, kv, true) > (size_t)TC_SMEM_MAX) --sst;
-  const int stages = stream ? sst : tc_stages(nbox, nt, kv);
-  const size_t smem = stream ? 1024 + (size_t)stages * sstage + 256 + tc_tail_bytes(nt, kv, true)
+  while (sst > 2 && 1024 + sst * sstage + 256 + tc_tail_bytes(nt, kv, true) + gmin > (size_t)TC_SMEM_MAX) --sst;
+  if (const char *e = getenv("FALKON_TC_SST")) sst = std::max(2, std::min(sst, atoi(e)));  // A/B
+  int rst = tc_stages(nbox, nt, kv);
+  while (rst > 2 && tc_smem_bytes(nbox, rst, nt, kv) + gmin > (size_t)TC_SMEM_MAX) --rst;
+  const int stages = stream ? sst : rst;
+  const size_t base = stream ? 1024 + (size_t)stages * sstage + 256 + tc_tail_bytes(nt, kv, true)
                              : tc_smem_bytes(nbox, stages, nt, kv);
+  int gslots = 0;
+  if (fgr) {
+    gslots = 3;
+    while (gslots < FG_MAX_SLOTS && base + fg_ring_bytes(gslots + 1) <= (size_t)TC_SMEM_MAX) ++gslots;
+  }
+  const size_t smem = base + (fgr ? (size_t)fg_ring_bytes(gslots) : 0);
   if (smem > (size_t)TC_SMEM_MAX) return fail(FALKON_EUNSUPPORTED, "tc_pass: shared memory");
   int mode = ctx->opt.exp_offload;
   if (const char *e = getenv("FALKON_TC_MODE")) mode = atoi(e);  // diagnostics (8-11)
@@ -1107,6 +1424,14 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
   args.p_base = p_begin;
   args.kst = kst;
   args.ldk = ldk;
+  args.gK = (kst && fg) ? fg->K : nullptr;
+  args.gw = fg ? fg->w : nullptr;
+  args.gdw = fg ? fg->dw : nullptr;
+  args.grows = fg ? fg->rows : 0;
+  args.gm = ldk;
+  args.gacc = fg ? fg->acc : nullptr;
+  args.gfirst = fg ? fg->first : 0;
+  args.gslots = gslots;
   {
     LaunchScope ls(ctx, passA ? FALKON_T_PASS_A : FALKON_T_PASS_B);
     if (cl == 1) {
@@ -1172,125 +1497,21 @@ int tc_pass_A_rows(falkon_ctx *ctx, const Prepared &pp, const float *z, float *w
 // the tile.  A warp owns SE_CPW centres (independent loads in flight), lanes keep fp32 sums of
 // <= 128 terms flushed into fp64 (reading c12), one shuffle reduction per centre at the end,
 // one fp64 accumulator row per row split (no atomics: deterministic).
-constexpr int SE_WARPS = 8;
-constexpr int SE_CPW = 8;                     // centres per warp
-constexpr int SE_COLS = SE_WARPS * SE_CPW;    // centres per CTA
-constexpr int SE_FLUSH = 32;                  // tiles per fp32 partial (4 x 32 = 128 terms)
-// WD (ACCUM_F64): w is fp64 and the GEMV accumulates the exact products k * w by DFMA.
-template <bool WEIGHTED, bool WD = false>
-__global__ void __launch_bounds__(32 * SE_WARPS) se_gemv_kernel(const float *__restrict__ K, int64_t ldk,
-                                                                const void *__restrict__ wv,
-                                                                const float *__restrict__ dw, int64_t rows,
-                                                                int64_t tiles_per_split, int64_t m,
-                                                                double *__restrict__ acc, int first) {
-  const float *w = reinterpret_cast<const float *>(wv);
-  const double *wd = reinterpret_cast<const double *>(wv);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t jb = (int64_t)blockIdx.x * SE_COLS + warp * SE_CPW;
-  if (jb >= m) return;
-  const int64_t ntile = cdiv<int64_t>(rows, TC_M);
-  const int64_t t0 = (int64_t)blockIdx.y * tiles_per_split;
-  const int64_t t1 = lmin(ntile, t0 + tiles_per_split);
-  int64_t jc[SE_CPW];
-#pragma unroll
-  for (int c = 0; c < SE_CPW; ++c) jc[c] = lmin(jb + c, m - 1);  // clamped: duplicates discarded
-  double a64[SE_CPW];
-  float a32[SE_CPW];
-#pragma unroll
-  for (int c = 0; c < SE_CPW; ++c) a64[c] = 0.0, a32[c] = 0.f;
-  for (int64_t t = t0; t < t1; ++t) {
-    const int64_t r = t * TC_M + 4 * lane;
-    if (WD) {  // fp64 w (rows are zero-padded to the tile, as the strip)
-      double4 w4;
-      const double2 wa = __ldg(reinterpret_cast<const double2 *>(wd + r));
-      const double2 wb = __ldg(reinterpret_cast<const double2 *>(wd + r + 2));
-      w4.x = r < rows ? wa.x : 0.0;
-      w4.y = r + 1 < rows ? wa.y : 0.0;
-      w4.z = r + 2 < rows ? wb.x : 0.0;
-      w4.w = r + 3 < rows ? wb.y : 0.0;
-      if (WEIGHTED) {
-        w4.x *= r < rows ? (double)dw[r] : 0.0;
-        w4.y *= r + 1 < rows ? (double)dw[r + 1] : 0.0;
-        w4.z *= r + 2 < rows ? (double)dw[r + 2] : 0.0;
-        w4.w *= r + 3 < rows ? (double)dw[r + 3] : 0.0;
-      }
-      const float *kt = K + t * ldk * TC_M + 4 * lane;
-      float4 kq[SE_CPW];
-#pragma unroll
-      for (int c = 0; c < SE_CPW; ++c) kq[c] = __ldcs(reinterpret_cast<const float4 *>(kt + jc[c] * TC_M));
-#pragma unroll
-      for (int c = 0; c < SE_CPW; ++c) {
-        double s = a64[c];
-        s = fma(k_to_f64(kq[c].x), w4.x, s);
-        s = fma(k_to_f64(kq[c].y), w4.y, s);
-        s = fma(k_to_f64(kq[c].z), w4.z, s);
-        a64[c] = fma(k_to_f64(kq[c].w), w4.w, s);
-      }
-      continue;
-    }
-    float4 wv;
-    if (r + 3 < rows) {
-      wv = __ldg(reinterpret_cast<const float4 *>(w + r));
-      if (WEIGHTED) {  // Knm^T D Knm (GSC LinOp, Alg. 2): the row weights, as scale_rows_kernel
-        const float4 dd = __ldg(reinterpret_cast<const float4 *>(dw + r));
-        wv.x *= dd.x, wv.y *= dd.y, wv.z *= dd.z, wv.w *= dd.w;
-      }
-    } else {
-      wv.x = r < rows ? w[r] * (WEIGHTED ? dw[r] : 1.f) : 0.f;
-      wv.y = r + 1 < rows ? w[r + 1] * (WEIGHTED ? dw[r + 1] : 1.f) : 0.f;
-      wv.z = r + 2 < rows ? w[r + 2] * (WEIGHTED ? dw[r + 2] : 1.f) : 0.f;
-      wv.w = 0.f;
-    }
-    const float *kt = K + t * ldk * TC_M + 4 * lane;
-    float4 kv[SE_CPW];
-#pragma unroll
-    for (int c = 0; c < SE_CPW; ++c) kv[c] = __ldcs(reinterpret_cast<const float4 *>(kt + jc[c] * TC_M));
-#pragma unroll
-    for (int c = 0; c < SE_CPW; ++c) {
-      float s = a32[c];
-      s = fmaf(kv[c].x, wv.x, s);
-      s = fmaf(kv[c].y, wv.y, s);
-      s = fmaf(kv[c].z, wv.z, s);
-      a32[c] = fmaf(kv[c].w, wv.w, s);
-    }
-    if ((t - t0) % SE_FLUSH == SE_FLUSH - 1) {
-#pragma unroll
-      for (int c = 0; c < SE_CPW; ++c) a64[c] += (double)a32[c], a32[c] = 0.f;
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < SE_CPW; ++c) {
-    double v = a64[c] + (double)a32[c];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    a64[c] = v;
-  }
-  if (lane < SE_CPW) {
-    double v = a64[0];
-#pragma unroll
-    for (int c = 1; c < SE_CPW; ++c)
-      if (lane == c) v = a64[c];
-    const int64_t j = jb + lane;
-    if (j < m) {
-      double *o = acc + (int64_t)blockIdx.y * m + j;
-      *o = first ? v : *o + v;
-    }
-  }
-}
-
 bool tc_single_eval(const falkon_ctx *ctx, const Prepared &pp) {
   if (pp.path != FALKON_PATH_TENSOR || ctx->opt.single_eval == 0) return false;
   if (ctx->opt.single_eval == 1) return true;
   return tc_stream(pp.d);  // auto: d16 > 192 (TIMIT d = 440: 6 * 448 flops vs 8 B per entry)
 }
 
-// z32/w32 (fp32 contractions) or z64/w64 (ACCUM_F64: DFMA contractions, fp64 w)
+// z32/w32 (fp32 contractions) or z64/w64 (ACCUM_F64: DFMA contractions, fp64 w).  Per strip:
+// pass A stores the strip's k values, then the standalone GEMV accumulates u += strip^T w.
+// Every u_j is accumulated in strip order by one writer (deterministic).
 static int single_eval_impl(falkon_ctx *ctx, const Prepared &pp, const float *z, const double *z64,
                             float *w32, double *w64, double *u, const float *dw) {
   const int64_t n = pp.n, m = pp.m;
   const int64_t ldk = m;
-  // rows per strip: a whole number of 128-row P tiles within the strip budget, which is capped
-  // at half of the free device memory (plus the strip already held)
+  // rows per strip: a whole number of 128-row P tiles within half the strip budget (two
+  // buffers), the budget capped at half of the free device memory (plus the strips held)
   int64_t budget = ctx->opt.strip_bytes;
   {
     size_t fr = 0, tot = 0;
@@ -1299,48 +1520,70 @@ static int single_eval_impl(falkon_ctx *ctx, const Prepared &pp, const float *z,
     else
       cudaGetLastError();
   }
+  // FALKON_FUSED_GEMV=1 (experimental, off by default): two strip buffers, the GEMV of strip s - 1
+  // runs in warps 2-3 of strip s's pass-A launch.  Measured on TIMIT (profiles/
+  // r2_fused_gemv_ab.txt): 406-424 ms per product against 349-358 ms for the standalone GEMV
+  // after each strip: the fused GEMV streams at ~1.1 TB/s beside the k stores whatever the
+  // bulk-copy ring depth, and the pass-A CTAs wait for it.
+  const char *fe = getenv("FALKON_FUSED_GEMV");
+  const bool fused = fe && atoi(fe) != 0;
+  const int nbuf = fused ? 2 : 1;
   const int64_t tile_bytes = (int64_t)4 * TC_M * ldk;
-  // equal strips (a short last strip would run a fraction of a wave)
   const int64_t ntiles = cdiv<int64_t>(n, TC_M);
-  int64_t tiles = std::min<int64_t>(std::max<int64_t>(1, budget / tile_bytes), ntiles);
-  tiles = cdiv<int64_t>(ntiles, cdiv<int64_t>(ntiles, tiles));
+  int64_t tiles = std::min<int64_t>(std::max<int64_t>(1, budget / nbuf / tile_bytes), ntiles);
+  tiles = cdiv<int64_t>(ntiles, cdiv<int64_t>(ntiles, tiles));  // equal strips
   const int64_t rows = tiles * TC_M;
-  void *kp, *ap;
-  FK_TRY(ws_get(ctx, WS_KSTRIP, (size_t)tiles * tile_bytes, &kp));
-  // GEMV grid: centre blocks x tile splits, at least ~4 waves of 8-warp CTAs
-  const int64_t cb = cdiv<int64_t>(m, SE_COLS);
-  const int64_t want = std::max<int64_t>(1, cdiv<int64_t>(4 * ctx->sm_count * 8, cb));
-  const int64_t splits = std::min<int64_t>(want, tiles);
-  const int64_t tps = cdiv<int64_t>(tiles, splits);
-  FK_TRY(ws_get(ctx, WS_SE_ACC, sizeof(double) * (size_t)splits * m, &ap));
-  float *K = (float *)kp;
-  double *acc = (double *)ap;
-  for (int64_t r0 = 0; r0 < n; r0 += rows) {
-    const int64_t nr = std::min<int64_t>(rows, n - r0);
-    if (z64)
-      FK_TRY(tc_launch(ctx, pp, true, nullptr, w64 + r0, nullptr, 1, r0, nr, K, ldk, z64));
-    else
-      FK_TRY(tc_launch(ctx, pp, true, z, nullptr, w32 + r0, 1, r0, nr, K, ldk));
+  const int64_t nstrips = cdiv<int64_t>(n, rows);
+  void *kp;
+  FK_TRY(ws_get(ctx, WS_KSTRIP, (size_t)tiles * tile_bytes * (nstrips > 1 ? nbuf : 1), &kp));
+  float *Kbuf[2] = {(float *)kp, (float *)kp + (nstrips > 1 && nbuf == 2 ? tiles * TC_M * ldk : 0)};
+  const void *wv = z64 ? (const void *)w64 : (const void *)w32;
+  auto wrow = [&](int64_t r0) -> const void * {
+    return z64 ? (const void *)(w64 + r0) : (const void *)(w32 + r0);
+  };
+  (void)wv;
+  int64_t prev_r0 = 0, prev_nr = 0;
+  auto gemv = [&](const float *K, int64_t r0g, int64_t nrg, int first) -> int {
     LaunchScope ls(ctx, FALKON_T_PASS_B);
-    const int64_t sp = cdiv<int64_t>(cdiv<int64_t>(nr, TC_M), tps);
-    const dim3 grid((unsigned)cb, (unsigned)sp);
-    const int first = r0 == 0 ? 1 : 0;
+    const dim3 grid((unsigned)cdiv<int64_t>(m, SE_COLS), 1u);
+    const int64_t tl = cdiv<int64_t>(nrg, TC_M);
+    const float *dwl = dw ? dw + r0g : nullptr;
     if (z64) {
       if (dw)
-        se_gemv_kernel<true, true><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w64 + r0, dw + r0, nr, tps, m, acc, first);
+        se_gemv_kernel<true, true><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w64 + r0g, dwl, nrg, tl, m, u, first);
       else
-        se_gemv_kernel<false, true><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w64 + r0, nullptr, nr, tps, m, acc, first);
+        se_gemv_kernel<false, true><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w64 + r0g, nullptr, nrg, tl, m, u, first);
     } else if (dw) {
-      se_gemv_kernel<true><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w32 + r0, dw + r0, nr, tps, m, acc, first);
+      se_gemv_kernel<true><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w32 + r0g, dwl, nrg, tl, m, u, first);
     } else {
-      se_gemv_kernel<false><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w32 + r0, nullptr, nr, tps, m, acc, first);
+      se_gemv_kernel<false><<<grid, 32 * SE_WARPS, 0, ctx->stream>>>(K, ldk, w32 + r0g, nullptr, nrg, tl, m, u, first);
     }
     FK_LAUNCH_CHECK();
-    if (r0 == 0 && sp < splits)  // later strips accumulate into every split row
-      FK_CUDA(cudaMemsetAsync(acc + sp * m, 0, sizeof(double) * (size_t)(splits - sp) * m,
-                              ctx->stream));
+    return FALKON_OK;
+  };
+  for (int64_t s = 0; s < nstrips; ++s) {
+    const int64_t r0 = s * rows;
+    const int64_t nr = std::min<int64_t>(rows, n - r0);
+    if (!fused && s > 0) FK_TRY(gemv(Kbuf[(s - 1) & 1], prev_r0, prev_nr, s == 1 ? 1 : 0));
+    FusedGemv fg;
+    if (fused && s > 0) {
+      fg.K = Kbuf[(s - 1) & 1];
+      fg.w = wrow(prev_r0);
+      fg.dw = dw ? dw + prev_r0 : nullptr;
+      fg.rows = prev_nr;
+      fg.acc = u;
+      fg.first = s == 1 ? 1 : 0;
+    }
+    const FusedGemv *fgp = (fused && s > 0) ? &fg : nullptr;
+    if (z64)
+      FK_TRY(tc_launch(ctx, pp, true, nullptr, w64 + r0, nullptr, 1, r0, nr, Kbuf[s & 1], ldk, z64, fgp));
+    else
+      FK_TRY(tc_launch(ctx, pp, true, z, nullptr, w32 + r0, 1, r0, nr, Kbuf[s & 1], ldk, nullptr, fgp));
+    prev_r0 = r0;
+    prev_nr = nr;
   }
-  return reduce_partials(ctx, acc, splits, m, u, nullptr);
+  // the last strip's GEMV: one split (every u_j one writer), centre blocks of SE_COLS
+  return gemv(Kbuf[(nstrips - 1) & 1], prev_r0, prev_nr, nstrips == 1 ? 1 : 0);
 }
 
 int tc_product_single_eval(falkon_ctx *ctx, const Prepared &pp, const float *z, float *w32,

@@ -1028,6 +1028,150 @@ static int potrf(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, double *Dinv,
   return FALKON_OK;
 }
 
+__global__ void add_diag_kernel(double *dvec, int64_t m, double scale, double add);
+
+// ------------------------------------------------------------------ NEXT-1: distributed build
+// 1D block-cyclic blocked Cholesky over G ranks (the multi-GPU layout of PAPER.md:460-469,
+// App. C Alg. 4): outer panel j (NBO = potrf_outer x 128 columns of the
+// logical lower factor L) is owned by rank j mod G.  Per panel:
+//   1. the owner factors it (potrf_panel: diagonal blocks + TRSV inverse blocks, panel solve,
+//      intra-panel updates) on its copy of the buffer;
+//   2. the factored panel (columns [K0, K1) of L, rows >= K0), its diagonal entries, its TRSV
+//      inverse blocks and the owner's pivot-failure word are broadcast;
+//   3. every rank applies the panel's trailing update to the column panels IT owns.
+// The LAUUM (T D T^T / m) is split the same way: each rank computes its own column panels of
+// M.  Storage stays replicated (80 GB at m = 1e5 fits one B200) so the CG's triangular solves
+// run locally; the O(m^3) work is split G ways.  Every element sees the same GEMM calls (k
+// range, kernel, k order) as the single-GPU schedule, so the factors are bitwise identical.
+// me < 0 simulates all G ranks in this process on one device (separate buffers, device copies
+// for the broadcasts: the decomposition is testable without a second GPU).
+struct DistBuild {
+  int G = 1;
+  int me = -1;
+  double *const *P = nullptr;   // [G] (simulation) or [1] (this rank)
+  double *const *diagT = nullptr, *const *diagA = nullptr;
+  double *const *work = nullptr;  // per rank: precond_work_elems(m) doubles (TRSV inverses)
+  unsigned long long *const *fail = nullptr;  // per rank: 2 pivot-failure words
+  double *stage = nullptr;      // (real, G > 1) staging buffer of one A panel: m x NBO doubles
+  int nranks_local() const { return me < 0 ? G : 1; }
+  int rank_of(int i) const { return me < 0 ? i : me; }  // global rank of local slot i
+};
+
+__global__ void fail_min_kernel(unsigned long long *dst, const unsigned long long *src) {
+  if (threadIdx.x == 0 && *src < *dst) *dst = *src;
+}
+
+// Step 2: panel [K0, K1) of factor `which` (0 = T: view trans 1, L columns = rows of P;
+// 1 = A: view trans 0, L columns = column strips of P) from its owner to every rank.
+static int dist_exchange(falkon_ctx *ctx, const DistBuild &D, int which, int64_t m, int64_t K0,
+                         int64_t K1, int owner) {
+  const int64_t nb = K1 - K0;
+  const int64_t dv0 = (which == 0 ? 0 : precond_work_elems(m) / 2) + (K0 / TB) * TB * TB;
+  const int64_t dvn = (cdiv<int64_t>(K1, TB) - K0 / TB) * TB * TB;
+  auto dvec = [&](int i) { return (which == 0 ? D.diagT[i] : D.diagA[i]) + K0; };
+  if (D.me < 0) {  // simulation: device copies from the owner's buffers
+    for (int r = 0; r < D.G; ++r) {
+      if (r == owner) continue;
+      if (which == 0)
+        FK_CUDA(cudaMemcpyAsync(D.P[r] + K0 * m, D.P[owner] + K0 * m, sizeof(double) * nb * m,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+      else
+        FK_CUDA(cudaMemcpy2DAsync(D.P[r] + K0 * m + K0, sizeof(double) * m,
+                                  D.P[owner] + K0 * m + K0, sizeof(double) * m,
+                                  sizeof(double) * nb, m - K0, cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
+      FK_CUDA(cudaMemcpyAsync(dvec(r), dvec(owner), sizeof(double) * nb, cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+      FK_CUDA(cudaMemcpyAsync(D.work[r] + dv0, D.work[owner] + dv0, sizeof(double) * dvn,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+      fail_min_kernel<<<1, 32, 0, ctx->stream>>>(D.fail[r] + which, D.fail[owner] + which);
+    }
+    FK_LAUNCH_CHECK();
+    return FALKON_OK;
+  }
+  // real ranks: NCCL broadcasts on the context's communicator (ctx->stream)
+  const bool own = D.me == owner;
+  if (which == 0) {  // T panels are whole rows of P: broadcast in place
+    FK_TRY(nccl_broadcast_bytes(ctx, D.P[0] + K0 * m, sizeof(double) * nb * m, owner));
+  } else {  // A panels are column strips: pack, broadcast, unpack
+    if (own)
+      FK_CUDA(cudaMemcpy2DAsync(D.stage, sizeof(double) * nb, D.P[0] + K0 * m + K0,
+                                sizeof(double) * m, sizeof(double) * nb, m - K0,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    FK_TRY(nccl_broadcast_bytes(ctx, D.stage, sizeof(double) * nb * (m - K0), owner));
+    if (!own)
+      FK_CUDA(cudaMemcpy2DAsync(D.P[0] + K0 * m + K0, sizeof(double) * m, D.stage,
+                                sizeof(double) * nb, sizeof(double) * nb, m - K0,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  FK_TRY(nccl_broadcast_bytes(ctx, dvec(0), sizeof(double) * nb, owner));
+  FK_TRY(nccl_broadcast_bytes(ctx, D.work[0] + dv0, sizeof(double) * dvn, owner));
+  return FALKON_OK;
+}
+
+// Steps 1-3 for factor `which` over every outer panel.
+static int potrf_dist(falkon_ctx *ctx, const DistBuild &D, int which, int64_t m, double *Wbuf) {
+  const size_t dsm = sizeof(double) * NB * (NB + 1);
+  FK_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)dsm));
+  const int64_t NBO = (int64_t)NB * ctx->opt.potrf_outer;
+  const int64_t nob = cdiv<int64_t>(m, NBO);
+  auto view = [&](int i) {
+    return which == 0 ? View{D.P[i], m, 1, 1, D.diagT[i]} : View{D.P[i], m, 0, 1, D.diagA[i]};
+  };
+  auto dinv = [&](int i) { return D.work[i] + (which == 0 ? 0 : precond_work_elems(m) / 2); };
+  for (int64_t j = 0; j < nob; ++j) {
+    const int64_t K0 = j * NBO, K1 = std::min<int64_t>(K0 + NBO, m);
+    const int owner = (int)(j % D.G);
+    for (int i = 0; i < D.nranks_local(); ++i)
+      if (D.rank_of(i) == owner)
+        FK_TRY(potrf_panel(ctx, view(i), m, K0, K1, Wbuf, dinv(i), D.fail[i] + which, dsm));
+    if (D.G > 1) FK_TRY(dist_exchange(ctx, D, which, m, K0, K1, owner));
+    for (int i = 0; i < D.nranks_local(); ++i)
+      for (int64_t c = j + 1; c < nob; ++c)
+        if ((int)(c % D.G) == D.rank_of(i))
+          FK_TRY(potrf_update(ctx, view(i), m, K0, K1, c * NBO, std::min<int64_t>(m, (c + 1) * NBO)));
+  }
+  return FALKON_OK;
+}
+
+// LAUUM split by owned column panels: M(i, j) = sum_{k >= i} T(i,k) D(k) T(j,k) / m for the
+// columns j of this rank's panels (rows i >= the panel start), the same tiles and k order as the
+// single-GPU call (panel starts are multiples of the 128-row GEMM tile).
+static int lauum_dist(falkon_ctx *ctx, const DistBuild &D, int64_t m, double lambda,
+                      const double *dscale) {
+  const int64_t NBO = (int64_t)NB * ctx->opt.potrf_outer;
+  const int64_t nob = cdiv<int64_t>(m, NBO);
+  for (int i = 0; i < D.nranks_local(); ++i) {
+    View L2{D.P[i], m, 0, 1, D.diagA[i]};
+    View Tv{D.P[i], m, 0, 2, D.diagT[i]};
+    for (int64_t c = 0; c < nob; ++c) {
+      if ((int)(c % D.G) != D.rank_of(i)) continue;
+      const int64_t c0 = c * NBO, c1 = std::min<int64_t>(m, c0 + NBO);
+      GemmArgs g{};
+      g.A = Tv;
+      g.B = Tv;
+      g.C = L2;
+      g.M = m - c0;
+      g.N = c1 - c0;
+      g.ra = g.rb = g.rc = g.cc = c0;
+      g.k0 = 0;
+      g.k1 = m;
+      g.k_from_row = 1;
+      g.tri_tiles = 1;
+      g.alpha = 1.0 / (double)m;
+      g.beta = 0.0;
+      g.kscale = dscale;
+      FK_TRY(gemm(ctx, g));
+    }
+    LaunchScope ls(ctx, FALKON_T_PRECOND);
+    add_diag_kernel<<<(unsigned)cdiv<int64_t>(m, 256), 256, 0, ctx->stream>>>(D.diagA[i], m, 1.0,
+                                                                                lambda);
+  }
+  FK_LAUNCH_CHECK();
+  return FALKON_OK;
+}
+
 __global__ void add_diag_kernel(double *dvec, int64_t m, double scale, double add) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m) dvec[i] = dvec[i] * scale + add;
@@ -1108,6 +1252,57 @@ static int build_A(falkon_ctx *ctx, int64_t m, double lambda, const double *dsca
   return potrf(ctx, L2, m, (double *)wb, dinvA, failf);
 }
 
+// ---- distributed steps (b)-(e) (NEXT-1): Kmm is computed on every rank (O(m^2 d), replicated)
+static int build_T_dist(falkon_ctx *ctx, const DistBuild &D, const float *C, int64_t m, int64_t d,
+                        int kernel, double sigma, double jitter) {
+  void *wb;
+  FK_TRY(ws_get(ctx, WS_PW, sizeof(double) * NB * NB, &wb));
+  for (int i = 0; i < D.nranks_local(); ++i) {
+    View L1{D.P[i], m, 1, 1, D.diagT[i]};
+    const int64_t tt = cdiv<int64_t>(m, 64);
+    LaunchScope ls(ctx, FALKON_T_PRECOND);
+    kmm_kernel<<<(unsigned)(tt * (tt + 1) / 2), 256, 0, ctx->stream>>>(
+        C, m, d, kernel, 1.0 / (2.0 * sigma * sigma), 1.0 / sigma, jitter, L1);
+  }
+  FK_LAUNCH_CHECK();
+  return potrf_dist(ctx, D, 0, m, (double *)wb);
+}
+static int build_A_dist(falkon_ctx *ctx, const DistBuild &D, int64_t m, double lambda,
+                        const double *dscale) {
+  void *wb;
+  FK_TRY(ws_get(ctx, WS_PW, sizeof(double) * NB * NB, &wb));
+  FK_TRY(lauum_dist(ctx, D, m, lambda, dscale));
+  return potrf_dist(ctx, D, 1, m, (double *)wb);
+}
+
+// The build is distributed when the context has a multi-rank NCCL communicator, or when
+// FALKON_OPT_DIST_PRECOND forces the distributed schedule (a 1-rank communicator: the
+// broadcasts become self-copies; tests the code path on one GPU).
+static bool dist_active(const falkon_ctx *ctx) {
+  return ctx->nccl_comm && (ctx->world > 1 || ctx->opt.dist_precond);
+}
+static int dist_for_ctx(falkon_ctx *ctx, int64_t m, double **P, double **dT, double **dA,
+                        double **work, unsigned long long **fl, DistBuild *D) {
+  D->G = ctx->world;
+  D->me = ctx->rank;
+  D->P = P;
+  D->diagT = dT;
+  D->diagA = dA;
+  D->work = work;
+  D->fail = fl;
+  if (ctx->world > 1) {
+    void *st;
+    FK_TRY(ws_get(ctx, WS_DIST_STAGE,
+                  sizeof(double) * (size_t)m * NB * (size_t)ctx->opt.potrf_outer, &st));
+    D->stage = (double *)st;
+  }
+  return FALKON_OK;
+}
+// failure words: the panel owners' (replicated by a min over ranks) before the host check
+static int dist_merge_fail(falkon_ctx *ctx, unsigned long long *failf) {
+  return nccl_allreduce_min_u64(ctx, failf, 2);
+}
+
 int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel, double sigma,
                   double lambda, double jitter, double *P, double *diagT, double *diagA,
                   double *work, falkon_fit_info *info) {
@@ -1116,6 +1311,14 @@ int precond_build(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int ker
   FK_TRY(ws_get(ctx, WS_FLAGS, 64, &flags));
   unsigned long long *failf = (unsigned long long *)flags;
   FK_CUDA(cudaMemsetAsync(failf, 0xff, 16, ctx->stream));
+  if (dist_active(ctx)) {
+    DistBuild D;
+    FK_TRY(dist_for_ctx(ctx, m, &P, &diagT, &diagA, &work, &failf, &D));
+    FK_TRY(build_T_dist(ctx, D, C, m, d, kernel, sigma, jitter));
+    FK_TRY(build_A_dist(ctx, D, m, lambda, nullptr));
+    FK_TRY(dist_merge_fail(ctx, failf));
+    return check_pivots(ctx, failf, 0, 1, jitter, info);
+  }
   FK_TRY(build_T(ctx, C, m, d, kernel, sigma, jitter, P, diagT, dinvT, failf));
   FK_TRY(build_A(ctx, m, lambda, nullptr, P, diagT, diagA, dinvA, failf + 1));
   return check_pivots(ctx, failf, 0, 1, jitter, info);
@@ -1128,6 +1331,14 @@ int precond_build_T(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int k
   FK_TRY(ws_get(ctx, WS_FLAGS, 64, &flags));
   unsigned long long *failf = (unsigned long long *)flags;
   FK_CUDA(cudaMemsetAsync(failf, 0xff, 16, ctx->stream));
+  if (dist_active(ctx)) {
+    DistBuild D;
+    double *dA = nullptr;
+    FK_TRY(dist_for_ctx(ctx, m, &P, &diagT, &dA, &work, &failf, &D));
+    FK_TRY(build_T_dist(ctx, D, C, m, d, kernel, sigma, jitter));
+    FK_TRY(dist_merge_fail(ctx, failf));
+    return check_pivots(ctx, failf, 0, 0, jitter, info);
+  }
   FK_TRY(build_T(ctx, C, m, d, kernel, sigma, jitter, P, diagT, work, failf));
   return check_pivots(ctx, failf, 0, 0, jitter, info);
 }
@@ -1139,9 +1350,43 @@ int precond_build_A(falkon_ctx *ctx, int64_t m, double lambda, const double *dsc
   FK_TRY(ws_get(ctx, WS_FLAGS, 64, &flags));
   unsigned long long *failf = (unsigned long long *)flags;
   FK_CUDA(cudaMemsetAsync(failf, 0xff, 16, ctx->stream));
+  if (dist_active(ctx)) {
+    DistBuild D;
+    FK_TRY(dist_for_ctx(ctx, m, &P, &diagT, &diagA, &work, &failf, &D));
+    FK_TRY(build_A_dist(ctx, D, m, lambda, dscale));
+    FK_TRY(dist_merge_fail(ctx, failf));
+    return check_pivots(ctx, failf, 1, 1, jitter, info);
+  }
   FK_TRY(build_A(ctx, m, lambda, dscale, P, diagT, diagA, work + precond_work_elems(m) / 2,
                  failf + 1));
   return check_pivots(ctx, failf, 1, 1, jitter, info);
+}
+
+// G ranks simulated in this process (tests): rank r's buffers P[r], diagT[r], diagA[r], work[r].
+int precond_build_sim(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, int kernel,
+                      double sigma, double lambda, double jitter, int G, double *const *P,
+                      double *const *diagT, double *const *diagA, double *const *work,
+                      falkon_fit_info *info) {
+  void *flags;
+  FK_TRY(ws_get(ctx, WS_SIM_FLAGS, sizeof(unsigned long long) * 2 * (size_t)G, &flags));
+  unsigned long long *f0 = (unsigned long long *)flags;
+  FK_CUDA(cudaMemsetAsync(f0, 0xff, sizeof(unsigned long long) * 2 * (size_t)G, ctx->stream));
+  std::vector<unsigned long long *> fl((size_t)G);
+  for (int r = 0; r < G; ++r) fl[(size_t)r] = f0 + 2 * r;
+  DistBuild D;
+  D.G = G;
+  D.me = -1;
+  D.P = P;
+  D.diagT = diagT;
+  D.diagA = diagA;
+  D.work = work;
+  D.fail = fl.data();
+  FK_TRY(build_T_dist(ctx, D, C, m, d, kernel, sigma, jitter));
+  FK_TRY(build_A_dist(ctx, D, m, lambda, nullptr));
+  for (int r = 0; r < G; ++r) {  // every rank must report the same failures as rank 0
+    FK_TRY(check_pivots(ctx, fl[(size_t)r], 0, 1, jitter, info));
+  }
+  return FALKON_OK;
 }
 
 // ------------------------------------------------------------------ triangular mat-vecs

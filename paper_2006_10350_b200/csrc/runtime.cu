@@ -98,6 +98,7 @@ typedef struct {
 typedef int (*fn_get_uid)(nccl_uid_t *);
 typedef int (*fn_init_rank)(void **, int, nccl_uid_t, int);
 typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+typedef int (*fn_broadcast)(const void *, void *, size_t, int, int, void *, cudaStream_t);
 typedef int (*fn_destroy)(void *);
 typedef const char *(*fn_errstr)(int);
 
@@ -107,13 +108,15 @@ static struct {
   fn_get_uid get_uid = nullptr;
   fn_init_rank init_rank = nullptr;
   fn_allreduce allreduce = nullptr;
+  fn_broadcast broadcast = nullptr;
   fn_destroy destroy = nullptr;
   fn_errstr errstr = nullptr;
 } g_nccl;
 
 // enum values from nccl.h (types only: the functions are resolved with dlsym)
 static const int NCCL_INT64 = (int)ncclInt64, NCCL_FLOAT64 = (int)ncclFloat64,
-                 NCCL_SUM = (int)ncclSum;
+                 NCCL_SUM = (int)ncclSum, NCCL_UINT8 = (int)ncclUint8,
+                 NCCL_UINT64 = (int)ncclUint64, NCCL_MIN = (int)ncclMin;
 
 static int nccl_load() {
   std::call_once(g_nccl.once, [] {
@@ -126,10 +129,12 @@ static int nccl_load() {
     g_nccl.get_uid = (fn_get_uid)dlsym(g_nccl.h, "ncclGetUniqueId");
     g_nccl.init_rank = (fn_init_rank)dlsym(g_nccl.h, "ncclCommInitRank");
     g_nccl.allreduce = (fn_allreduce)dlsym(g_nccl.h, "ncclAllReduce");
+    g_nccl.broadcast = (fn_broadcast)dlsym(g_nccl.h, "ncclBroadcast");
     g_nccl.destroy = (fn_destroy)dlsym(g_nccl.h, "ncclCommDestroy");
     g_nccl.errstr = (fn_errstr)dlsym(g_nccl.h, "ncclGetErrorString");
   });
-  if (!g_nccl.h || !g_nccl.get_uid || !g_nccl.init_rank || !g_nccl.allreduce || !g_nccl.destroy)
+  if (!g_nccl.h || !g_nccl.get_uid || !g_nccl.init_rank || !g_nccl.allreduce ||
+      !g_nccl.broadcast || !g_nccl.destroy)
     return fail(FALKON_ENCCL, "NCCL (libnccl.so.2) could not be loaded");
   return FALKON_OK;
 }
@@ -178,6 +183,23 @@ int nccl_allreduce_i64(falkon_ctx *ctx, int64_t *buf, int64_t count) {
   return nccl_check(g_nccl.allreduce(buf, buf, (size_t)count, NCCL_INT64, NCCL_SUM,
                                      ctx->nccl_comm, ctx->stream),
                     "ncclAllReduce");
+}
+
+int nccl_allreduce_min_u64(falkon_ctx *ctx, unsigned long long *buf, int64_t count) {
+  if (!ctx->nccl_comm || count == 0) return FALKON_OK;
+  LaunchScope ls(ctx, FALKON_T_ALLREDUCE);
+  return nccl_check(g_nccl.allreduce(buf, buf, (size_t)count, NCCL_UINT64, NCCL_MIN,
+                                     ctx->nccl_comm, ctx->stream),
+                    "ncclAllReduce(min)");
+}
+
+// In-place broadcast of `bytes` from rank `root` (the distributed preconditioner's panels).
+int nccl_broadcast_bytes(falkon_ctx *ctx, void *buf, size_t bytes, int root) {
+  if (!ctx->nccl_comm || bytes == 0) return FALKON_OK;
+  LaunchScope ls(ctx, FALKON_T_ALLREDUCE);
+  return nccl_check(g_nccl.broadcast(buf, buf, bytes, NCCL_UINT8, root, ctx->nccl_comm,
+                                     ctx->stream),
+                    "ncclBroadcast");
 }
 
 }  // namespace falkon

@@ -138,3 +138,66 @@ def test_unique_id_broadcast_and_max_over_ranks():
     for r, (uid, t) in out.items():
         assert uid == bytes(range(128))
         assert t == 2.5
+
+
+# ---- NEXT-1: 1D block-cyclic distributed Cholesky (the schedule libfalkon runs across ranks)
+def _block_cyclic_cholesky(rank, world, S, nbo):
+    """Lower Cholesky S = L L^T with outer panel j owned by rank j % world: the owner factors
+    the panel (diagonal block Cholesky + panel solve), broadcasts it, and every rank applies
+    the trailing update to ITS column panels only.  Each rank holds a full-size buffer but
+    only ever updates its own columns (the storage-replicated layout of csrc/precond.cu)."""
+    import scipy.linalg as sla
+    m = S.shape[0]
+    L = S.copy()
+    nob = -(-m // nbo)
+    for j in range(nob):
+        k0, k1 = j * nbo, min(m, (j + 1) * nbo)
+        owner = j % world
+        panel = torch.zeros((m - k0, k1 - k0), dtype=torch.float64)
+        if rank == owner:
+            Lkk = sla.cholesky(L[k0:k1, k0:k1], lower=True)
+            L[k0:k1, k0:k1] = Lkk
+            if k1 < m:
+                L[k1:, k0:k1] = sla.solve_triangular(Lkk, L[k1:, k0:k1].T, lower=True).T
+            panel = torch.from_numpy(np.ascontiguousarray(L[k0:, k0:k1]))
+        dist.broadcast(panel, src=owner)
+        L[k0:, k0:k1] = panel.numpy()
+        for c in range(j + 1, nob):
+            if c % world != rank:
+                continue
+            c0, c1 = c * nbo, min(m, (c + 1) * nbo)
+            Lp = L[c0:, k0:k1]
+            L[c0:, c0:c1] -= Lp @ L[c0:c1, k0:k1].T
+    return np.tril(L)
+
+
+def _dist_precond(rank, world):
+    """Both factors of the Falkon preconditioner through the distributed schedule: T^T from
+    Kmm + delta I, then A^T from T T^T/m + lam I (LAUUM split by the owners' column panels)."""
+    cfg, X, y, C = synth.make_problem("tiny", m=100)
+    m, lam, delta = C.shape[0], 1e-3, 1e-8
+    K = oracle.kmm(C, G, cfg.sigma) + delta * np.eye(m)
+    LT = _block_cyclic_cholesky(rank, world, K, 16)            # L = T^T
+    T = LT.T
+    M = np.zeros((m, m))
+    for c in range(-(-m // 16)):                                  # owned column panels of M
+        if c % world == rank:
+            c0, c1 = c * 16, min(m, (c + 1) * 16)
+            M[:, c0:c1] = (T @ T[c0:c1].T) / m
+    Mt = torch.from_numpy(M)
+    dist.all_reduce(Mt)  # assemble (each column panel has one writer)
+    M = Mt.numpy() + lam * np.eye(m)
+    LA = _block_cyclic_cholesky(rank, world, np.tril(M) + np.tril(M, -1).T, 16)
+    return T, LA.T
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_block_cyclic_preconditioner_decomposition(world):
+    out = run_world(_dist_precond, world=world)
+    cfg, X, y, C = synth.make_problem("tiny", m=100)
+    To, Ao = oracle.preconditioner(C, G, cfg.sigma, 1e-3, 1e-8)
+    for r in range(world):
+        T, A = out[r]
+        assert np.allclose(T, To, rtol=0, atol=1e-12)
+        assert np.allclose(A, Ao, rtol=0, atol=1e-10)
+        assert np.array_equal(T, out[0][0]) and np.array_equal(A, out[0][1])

@@ -121,3 +121,33 @@ def test_single_eval_weighted_gsc_parity(se_ctx, ctx):
     ao = gsc.gsc_falkon(X, y, C, yC, gsc.LOGISTIC, G, sigma, mus, its)
     assert rel_l2(out[0], ao) <= 1e-3
     assert rel_l2(out[0], out[1]) <= 1e-4
+
+
+@pytest.mark.parametrize("accum_f64", [0, 1])
+def test_fused_strip_gemv_variant(ctx, accum_f64):
+    """Experimental FALKON_FUSED_GEMV=1: the GEMV of strip s - 1 runs in warps 2-3 of strip s's
+    pass-A launch through a bulk-copy ring (two k buffers, so strips are half as long: the
+    fp32 path's per-strip partial sums group differently, 1e-7; fp64 contractions 1e-12),
+    and the oracle bar."""
+    import os
+    from paper_2006_10350_b200 import binding
+    n, m, d, sigma = 9001, 700, 300, 12.0
+    X = synth.gen_X(41, 0, n, d)
+    C = X[synth.center_indices(41, n, m)]
+    v = synth.gen_vec(41, m).astype(np.float64)
+    ctx.set_option(binding.OPT_SINGLE_EVAL, 1)
+    ctx.set_option(binding.OPT_STRIP_BYTES, 64 << 20)
+    ctx.set_option(binding.OPT_ACCUM_F64, accum_f64)
+    try:
+        a = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, sigma, zeros(m)))
+        os.environ["FALKON_FUSED_GEMV"] = "1"
+        try:
+            b = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, sigma, zeros(m)))
+        finally:
+            del os.environ["FALKON_FUSED_GEMV"]
+    finally:
+        ctx.set_option(binding.OPT_SINGLE_EVAL, 2)
+        ctx.set_option(binding.OPT_STRIP_BYTES, 16 << 30)
+        ctx.set_option(binding.OPT_ACCUM_F64, 0)
+    assert rel_l2(b, a) <= (1e-12 if accum_f64 else 1e-7)
+    assert rel_l2(b, oracle.knm_t_knm_vec(X, C, v, G, sigma)) <= 1e-4

@@ -396,3 +396,15 @@ def test_blocked_cholesky_and_solves_match_lapack():
             assert np.allclose(x, x0, rtol=1e-12, atol=1e-12)
     with pytest.raises(np.linalg.LinAlgError):
         fo._chol_upper_inplace(-np.eye(5), 2)
+
+
+def test_blocked_upper_times_transpose():
+    """T T^T by blocks (the oracle's LAUUM, avoiding numpy's whole-matrix product that crashes
+    past m = 46,340) equals the plain product and is exactly symmetric."""
+    from oracle import falkon_oracle as fo
+    rng = np.random.default_rng(12)
+    for m, nb in [(301, 7), (129, 64), (40, 2048)]:
+        T = np.triu(rng.standard_normal((m, m)))
+        M = fo._upper_times_transpose(T, nb)
+        assert np.allclose(M, T @ T.T, rtol=0, atol=1e-12 * m)
+        assert np.array_equal(M, M.T)
