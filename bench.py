@@ -180,10 +180,10 @@ def oracle_rate(cfg, n_global, m, seconds: float, rank_workers: int):
 
 def kt_path_tensor(args, d):
     """Mirror of libfalkon's path choice (tc_supported): tensor cores for the Gaussian kernel
-    when d > 8 (measured crossover), unless --path forces one."""
+    when d > 4 (measured crossover, profiles/r2_crossover.jsonl), unless --path forces one."""
     if args.path == "simt":
         return False
-    return args.path == "tensor" or d > 8
+    return args.path == "tensor" or d > 4
 
 
 # The paper's whole-fit times on the real datasets (BASELINE.md; context, not the target).

@@ -80,7 +80,7 @@ struct TimedEvent {
 
 struct Options {
   int path = FALKON_PATH_AUTO;
-  int tc_min_d = 8;   // measured SIMT/tensor crossover
+  int tc_min_d = 4;   // measured SIMT/tensor crossover (profiles/r2_crossover.jsonl)
   int tc_terms = 3;
   int kernel_timing = 0;
   int exp_offload = 0;  // tensor path: share of exp2 evaluated on the FMA pipe (0..3)
