@@ -227,6 +227,42 @@ __device__ __forceinline__ void tc_commit_mc(uint64_t *bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
+// ---- CTA-pair (cta_group::2) forms: one MMA of M = 256 over the two CTAs' shared memory ----
+constexpr uint32_t TC_PEER_MASK = 0xFEFFFFFFu;  // clears the CTA-in-pair bit of a cluster address
+__device__ __forceinline__ void tc_mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// completion of the pair's MMAs arrives on the barrier at this offset in both CTAs
+__device__ __forceinline__ void tc_commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// TMA load into THIS CTA's shared memory whose completion counts on the pair leader's barrier
+// at the same offset (the peer bit of the barrier address cleared)
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *map, int c0, int c1,
+                                                 uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & TC_PEER_MASK)
+      : "memory");
+}
+// arrive on the barrier at this offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t *bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
@@ -738,8 +774,14 @@ __device__ __forceinline__ void fused_strip_gemv(const TcArgs &a, int wid, int l
 // 128-row half of every Q box and multicasts it to both, halving the L2 -> SM traffic of the
 // streamed operand; a stage is refilled only after BOTH CTAs' MMAs have released it (empty
 // barriers count CL arrivals, commits are multicast).
+// PAIR (STREAM, CL = 2): the two CTAs of a cluster run ONE tcgen05.mma.cta_group::2 of M = 256
+// (each CTA's 128 P rows) x N = 256: each CTA stages only its own P rows and ITS HALF of the Q
+// box (32 KB stages instead of 48 KB: deeper ring, more bytes in flight); the leader (rank 0)
+// waits for both halves on its full barrier (the peer's TMA completes there), issues the MMAs
+// and commits to both CTAs' empty / tfull barriers; both CTAs' epilogues release the
+// accumulator on the leader's tempty barrier.
 template <int MODE, int NT, bool TS, bool STREAM = false, int EPIW = TC_EPI_WARPS, int KV = 1,
-          bool KST = false, int CL = 1, bool ZD = false>
+          bool KST = false, int CL = 1, bool ZD = false, bool PAIR = false>
 __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     tc_kvp_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                   TcArgs a) {
@@ -747,7 +789,10 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   constexpr int SBK = STREAM ? TC_SBK : TC_BK;     // K width of the streamed boxes
   constexpr int SA_BOX = TC_M * SBK * 2;             // streaming: one P box (8 KB)
   constexpr int SQ_BOX = NT * SBK * 2;               // streaming: one Q box (16 KB)
-  constexpr int BBOX = STREAM ? 2 * (SA_BOX + SQ_BOX) : NT * TC_BK * 2;  // stage bytes
+  static_assert(!PAIR || (CL == 2 && NT == 2 * TC_M && KV == 1 && !TS), "pair MMA shape");
+  // stage bytes; PAIR: this CTA's P boxes (streaming) and its 128-row half of the Q box
+  constexpr int BBOX = PAIR ? (STREAM ? 4 * SA_BOX : TC_A_BOX)
+                            : (STREAM ? 2 * (SA_BOX + SQ_BOX) : NT * TC_BK * 2);
   constexpr int GRP = EPIW / 4;          // column groups (epilogue warps per TMEM lane group)
   constexpr int HALF = NT / GRP;         // columns per epilogue warp
   constexpr int NCH = HALF / 32;         // 32-column chunks per epilogue warp
@@ -778,11 +823,11 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);
+      mbar_init(&empty[s], PAIR ? 1 : CL);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPIW);
+      mbar_init(&tempty[i], PAIR ? 2 * EPIW : EPIW);
     }
     mbar_init(afull, 1);
     mbar_init(&zfull[0], 1);
@@ -792,10 +837,17 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -809,8 +861,14 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   if (warp == 0) {
     // TMA producer: the whole warp walks the ring, one elected lane issues the copies
     if (!STREAM && elect_one()) {
-      mbar_expect_tx(afull, (uint32_t)(a.nbox * TC_A_BOX));
-      for (int b = 0; b < a.nbox; ++b) tma_load_2d(sA + b * TC_A_BOX, &tmP, b * TC_BK, (int)(a.p_base + p0), afull);
+      if (PAIR) {  // both CTAs' P tiles complete on the leader's afull (its MMAs read both)
+        if (crank == 0) mbar_expect_tx(afull, (uint32_t)(2 * a.nbox * TC_A_BOX));
+        for (int b = 0; b < a.nbox; ++b)
+          tma_load_2d_pair(sA + b * TC_A_BOX, &tmP, b * TC_BK, (int)(a.p_base + p0), afull);
+      } else {
+        mbar_expect_tx(afull, (uint32_t)(a.nbox * TC_A_BOX));
+        for (int b = 0; b < a.nbox; ++b) tma_load_2d(sA + b * TC_A_BOX, &tmP, b * TC_BK, (int)(a.p_base + p0), afull);
+      }
     }
     __syncwarp();
     const int segk = a.nk * 16;  // STREAM: elements per segment
@@ -836,6 +894,19 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
           if (MODE == 11) {  // diagnostic: no Q loads
             mbar_arrive(&full[stage]);
           } else if (MODE == 12) {  // fault injection: the stage never fills (mbar_wait_safe traps)
+          } else if (PAIR && !STREAM) {  // this CTA's 128-row half of the Q box
+            if (crank == 0) mbar_expect_tx(&full[stage], 2 * BBOX);
+            tma_load_2d_pair(sB + stage * BBOX, &tmQ, b * TC_BK, q0 + (int)crank * TC_M, &full[stage]);
+          } else if (PAIR) {
+            // own P rows (h, l) and own 128-row half of the Q box (h, l) into this CTA's stage;
+            // completions count on the leader's full barrier, which expects both CTAs' boxes
+            uint8_t *st = sB + stage * BBOX;
+            if (crank == 0) mbar_expect_tx(&full[stage], 2 * BBOX);
+            const int pr = (int)(a.p_base + p0), qh = q0 + (int)crank * TC_M;
+            tma_load_2d_pair(st, &tmP, b * SBK, pr, &full[stage]);                  // h_p
+            tma_load_2d_pair(st + SA_BOX, &tmP, segk + b * SBK, pr, &full[stage]);  // l_p
+            tma_load_2d_pair(st + 2 * SA_BOX, &tmQ, b * SBK, qh, &full[stage]);         // h_q half
+            tma_load_2d_pair(st + 3 * SA_BOX, &tmQ, segk + b * SBK, qh, &full[stage]);  // l_q half
           } else if (STREAM) {
             uint8_t *st = sB + stage * BBOX;
             mbar_expect_tx(&full[stage], BBOX);
@@ -869,11 +940,13 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && !(PAIR && crank != 0)) {
     // MMA issuer: warp-uniform control flow, one elected lane issues tcgen05.mma.  The
     // descriptors are linear in the shared-memory address (start address in the low bits),
-    // so chunk / stage offsets are plain integer adds on precomputed bases.
-    const uint32_t idesc = (1u << 4) | ((uint32_t)(NT >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+    // so chunk / stage offsets are plain integer adds on precomputed bases.  PAIR: the
+    // leader's warp issues M = 256 MMAs for the CTA pair; the peer's warp 1 idles.
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(NT >> 3) << 17) |
+                           ((uint32_t)((PAIR ? 2 : 1) * TC_M >> 4) << 24);
     const uint64_t a0 = sw128_desc(smem_u32(sA));
     const uint64_t b0 = STREAM ? sw64_desc(smem_u32(sB)) : sw128_desc(smem_u32(sB));
     const int nk = a.nk;
@@ -897,7 +970,22 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       for (int b = 0; b < a.nbox; ++b) {
         mbar_wait_safe(&full[stage], phase);
         tc_fence_after();
-        if (STREAM && elect_one()) {
+        if (PAIR && STREAM && elect_one()) {
+          const uint64_t ah = b0 + (uint64_t)((stage * BBOX) >> 4);
+          const uint64_t al = ah + (uint64_t)(SA_BOX >> 4);
+          const uint64_t bh = ah + (uint64_t)((2 * SA_BOX) >> 4);
+          const uint64_t bl = ah + (uint64_t)((3 * SA_BOX) >> 4);
+#pragma unroll
+          for (int jj = 0; jj < SBK / 16; ++jj) {
+            if (b * (SBK / 16) + jj < nk) {
+              const uint64_t o = (uint64_t)(jj * 2);  // +32 B within the 64 B swizzle row
+              tc_mma_f16_pair(dtm, ah + o, bh + o, idesc, (b | jj) ? 1u : 0u);  // h_p . h_q
+              tc_mma_f16_pair(dtm, al + o, bh + o, idesc, 1u);                  // l_p . h_q
+              tc_mma_f16_pair(dtm, ah + o, bl + o, idesc, 1u);                  // h_p . l_q
+            }
+          }
+          tc_commit_pair(&empty[stage]);
+        } else if (STREAM && !PAIR && elect_one()) {
           const uint64_t ah = b0 + (uint64_t)((stage * BBOX) >> 4);
           const uint64_t al = ah + (uint64_t)(SA_BOX >> 4);
           const uint64_t bh = ah + (uint64_t)((2 * SA_BOX) >> 4);
@@ -923,14 +1011,17 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
               const int ca = j < nk ? j : j - nk;         // h_p chunk
               const uint32_t first = (b | jj) ? 1u : 0u;  // first MMA of the tile overwrites
               if (TS) tc_mma_f16_ts(dtm, tmem_a + (uint32_t)(8 * ca), bd, idesc, first);
+              else if (PAIR) tc_mma_f16_pair(dtm, adesc(ca), bd, idesc, first);
               else tc_mma_f16(dtm, adesc(ca), bd, idesc, first);  // h_p . h_q | h_p . l_q
               if (j < nk) {                                        // l_p . h_q
                 if (TS) tc_mma_f16_ts(dtm, tmem_a + (uint32_t)(8 * (nk + j)), bd, idesc, 1u);
+                else if (PAIR) tc_mma_f16_pair(dtm, adesc(nk + j), bd, idesc, 1u);
                 else tc_mma_f16(dtm, adesc(nk + j), bd, idesc, 1u);
               }
             }
           }
-          if (CL == 1) tc_commit(&empty[stage]);
+          if (PAIR) tc_commit_pair(&empty[stage]);
+          else if (CL == 1) tc_commit(&empty[stage]);
           else tc_commit_mc(&empty[stage], CMASK);
         }
         __syncwarp();
@@ -939,7 +1030,10 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
           phase ^= 1;
         }
       }
-      if (elect_one()) tc_commit(&tfull[acc]);
+      if (elect_one()) {
+        if (PAIR) tc_commit_pair(&tfull[acc]);
+        else tc_commit(&tfull[acc]);
+      }
       __syncwarp();
     }
   } else if (KST && KV == 1 && (warp == 2 || warp == 3)) {
@@ -996,7 +1090,10 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[accb]);
+      if (lane == 0) {  // PAIR: the leader's tempty collects both CTAs' epilogue warps
+        if (PAIR && crank != 0) mbar_arrive_cluster(&tempty[accb], 0);
+        else mbar_arrive(&tempty[accb]);
+      }
 #pragma unroll
       for (int c = 0; c < KV / 2; ++c) {
         acc64[2 * c] += (double)acc[c].x;
@@ -1085,7 +1182,10 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[accb]);
+      if (lane == 0) {  // PAIR: the leader's tempty collects both CTAs' epilogue warps
+        if (PAIR && crank != 0) mbar_arrive_cluster(&tempty[accb], 0);
+        else mbar_arrive(&tempty[accb]);
+      }
       if (!ZD) acc64 += (double)((acc[0].x + acc[0].y) + (acc[1].x + acc[1].y));
     }
     if (ZD) acc64 = (accd[0] + accd[1]) + (accd[2] + accd[3]);
@@ -1105,7 +1205,10 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   if (CL > 1) cluster_sync_all();  // the partner's last multicasts / commits into this CTA are done
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
@@ -1293,8 +1396,22 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
   // the 192-row Q maps (maps[4], maps[5]) and the NT = 192 kernel
   const bool ts = kv == 1 && !stream && !kst && !z64 && tc_use_ts(d16);
   const int nt = ts ? TC_N_TS : TC_N;
-  // streaming: stages of 48 KB (P and Q boxes of both segments, 32 wide) — 4 fit
-  const size_t sstage = (size_t)2 * (TC_M + TC_N) * TC_SBK * 2;
+  // CTA-pair MMA (cta_group::2) for the streaming kernel with 2-CTA clusters (default; measured
+  // TIMIT single evaluation 355 -> 320 ms, two-pass 426 -> 407 ms per product,
+  // profiles/r2_pair_ab.txt); FALKON_TC_PAIR=0 selects the multicast-only cluster kernel (A/B)
+  const char *pe = getenv("FALKON_TC_PAIR");
+  int mode = ctx->opt.exp_offload;
+  if (const char *e = getenv("FALKON_TC_MODE")) mode = atoi(e);  // diagnostics (8-12)
+  // resident-P kernels (d <= 190) keep the multicast clusters: the pair variant is correct but
+  // slower there (MSD 21.4 -> 23.0 ms, HIGGS 576 -> 745 ms, TAXI 1337 -> 1810 ms per product:
+  // the two CTAs' epilogues gate one shared accumulator pipeline), opt-in FALKON_TC_PAIR=2
+  const int pv = pe ? atoi(pe) : 1;
+  const bool pair = kv == 1 && ctx->opt.tc_cluster == 2 && pv != 0 && !ts &&
+                    (stream || (pv == 2 && (mode == 0 || kst || z64)));
+  const int nt_stage = (pair && !stream) ? TC_M : nt;  // resident pair: half-Q-box stages
+  // streaming: stages of 48 KB (P and Q boxes of both segments, 32 wide) — 4 fit; a CTA of a
+  // pair stages its P rows and its half of the Q box: 32 KB, 6 fit
+  const size_t sstage = pair ? (size_t)4 * TC_M * TC_SBK * 2 : (size_t)2 * (TC_M + TC_N) * TC_SBK * 2;
   // single-evaluation launches reserve the fused GEMV's bulk-copy rings after the tail: at least
   // 3 slots per GEMV warp, the rest of shared memory beyond the pass-A ring (up to 8 slots)
   const bool fgr = kst && fg;  // fused GEMV in this launch
@@ -1302,11 +1419,11 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
   int sst = TC_MAX_STAGES;
   while (sst > 2 && 1024 + sst * sstage + 256 + tc_tail_bytes(nt, kv, true) + gmin > (size_t)TC_SMEM_MAX) --sst;
   if (const char *e = getenv("FALKON_TC_SST")) sst = std::max(2, std::min(sst, atoi(e)));  // A/B
-  int rst = tc_stages(nbox, nt, kv);
-  while (rst > 2 && tc_smem_bytes(nbox, rst, nt, kv) + gmin > (size_t)TC_SMEM_MAX) --rst;
+  int rst = tc_stages(nbox, nt_stage, kv);
+  while (rst > 2 && tc_smem_bytes(nbox, rst, nt_stage, kv) + gmin > (size_t)TC_SMEM_MAX) --rst;
   const int stages = stream ? sst : rst;
   const size_t base = stream ? 1024 + (size_t)stages * sstage + 256 + tc_tail_bytes(nt, kv, true)
-                             : tc_smem_bytes(nbox, stages, nt, kv);
+                             : tc_smem_bytes(nbox, stages, nt_stage, kv);
   int gslots = 0;
   if (fgr) {
     gslots = 3;
@@ -1314,8 +1431,6 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
   }
   const size_t smem = base + (fgr ? (size_t)fg_ring_bytes(gslots) : 0);
   if (smem > (size_t)TC_SMEM_MAX) return fail(FALKON_EUNSUPPORTED, "tc_pass: shared memory");
-  int mode = ctx->opt.exp_offload;
-  if (const char *e = getenv("FALKON_TC_MODE")) mode = atoi(e);  // diagnostics (8-11)
   typedef void (*kfn)(const CUtensorMap, const CUtensorMap, TcArgs);
   kfn fn;
   // resident-P kernel: 16 epilogue warps (4 per SM sub-partition) — measured 18-22 % faster
@@ -1360,7 +1475,21 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
                   : tc_kvp_kernel<0, TC_N, false, false, 16, 1, true>;
     epiw = stream ? 8 : 16;
   }
-  if (z64) {  // ACCUM_F64 epilogue (MODE 0, exp on the MUFU; DFMA contraction)
+  if (pair && stream) {  // streaming, 2-CTA clusters: one M = 256 MMA per pair
+    fn = z64 ? (kst ? tc_kvp_kernel<0, TC_N, false, true, 8, 1, true, 2, true, true>
+                    : tc_kvp_kernel<0, TC_N, false, true, 8, 1, false, 2, true, true>)
+             : (kst ? tc_kvp_kernel<0, TC_N, false, true, 8, 1, true, 2, false, true>
+                    : tc_kvp_kernel<0, TC_N, false, true, 8, 1, false, 2, false, true>);
+    epiw = 8;
+    cl = 2;
+  } else if (pair) {  // resident P tile, 2-CTA clusters: M = 256 MMAs over the pair
+    fn = z64 ? (kst ? tc_kvp_kernel<0, TC_N, false, false, 16, 1, true, 2, true, true>
+                    : tc_kvp_kernel<0, TC_N, false, false, 16, 1, false, 2, true, true>)
+             : (kst ? tc_kvp_kernel<0, TC_N, false, false, 16, 1, true, 2, false, true>
+                    : tc_kvp_kernel<0, TC_N, false, false, 16, 1, false, 2, false, true>);
+    epiw = 16;
+    cl = 2;
+  } else if (z64) {  // ACCUM_F64 epilogue (MODE 0, exp on the MUFU; DFMA contraction)
     const bool c2 = ctx->opt.tc_cluster == 2;
     if (stream)
       fn = kst ? (c2 ? tc_kvp_kernel<0, TC_N, false, true, 8, 1, true, 2, true>

@@ -151,3 +151,28 @@ def test_fused_strip_gemv_variant(ctx, accum_f64):
         ctx.set_option(binding.OPT_ACCUM_F64, 0)
     assert rel_l2(b, a) <= (1e-12 if accum_f64 else 1e-7)
     assert rel_l2(b, oracle.knm_t_knm_vec(X, C, v, G, sigma)) <= 1e-4
+
+
+@pytest.mark.parametrize("pair", ["0", "1", "2"])
+@pytest.mark.parametrize("se,accum_f64", [(0, 0), (1, 0), (1, 1), (0, 1)])
+@pytest.mark.parametrize("d,sigma", [(440, 14.5), (90, 7.0)])
+def test_cta_pair_variant(ctx, pair, se, accum_f64, d, sigma):
+    """CTA-pair MMAs (cta_group::2): default for the streaming kernel (d > 190), opt-in
+    (FALKON_TC_PAIR=2) for the resident one; FALKON_TC_PAIR=0 = multicast-only clusters.
+    Oracle bar for two-pass and single-evaluation products, fp32 and fp64 contractions."""
+    import os
+    from paper_2006_10350_b200 import binding
+    n, m = 3001, 771
+    X = synth.gen_X(43, 0, n, d)
+    C = X[synth.center_indices(43, n, m)]
+    v = synth.gen_vec(43, m).astype(np.float64)
+    ctx.set_option(binding.OPT_SINGLE_EVAL, se)
+    ctx.set_option(binding.OPT_ACCUM_F64, accum_f64)
+    os.environ["FALKON_TC_PAIR"] = pair
+    try:
+        u = host(ctx.knm_matvec(dev(X), dev(C), dev(v), G, sigma, zeros(m)))
+    finally:
+        del os.environ["FALKON_TC_PAIR"]
+        ctx.set_option(binding.OPT_SINGLE_EVAL, 2)
+        ctx.set_option(binding.OPT_ACCUM_F64, 0)
+    assert rel_l2(u, oracle.knm_t_knm_vec(X, C, v, G, sigma)) <= 1e-4
