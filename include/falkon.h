@@ -99,6 +99,11 @@ enum {
                                    DFMA in fp64 (k itself stays fp32).  Applies to the single-vector
                                    products, fits, GSC fits and predictions; multi-output calls
                                    stay fp32.  See DESIGN.md for the measured default. */
+  FALKON_OPT_FIT_PRECISE = 14,  /* 1 (default): a Gaussian fit (falkon_fit, falkon_gsc_fit) whose
+                                   AUTO path is the tensor kernel runs on the SIMT kernels when
+                                   d <= 32 and the mean scaled centre norm ||c~||^2/2 exceeds 4
+                                   (the tensor cores' truncating accumulation biases K there;
+                                   DESIGN.md reading d3); 0 = always the AUTO path */
   FALKON_OPT_DIST_PRECOND = 13  /* 1: build the preconditioner with the distributed schedule
                                    (NEXT-1, below) even on a 1-rank NCCL communicator (tests the
                                    broadcast path on one GPU).  With world > 1 it is always used. */
@@ -127,6 +132,7 @@ typedef struct {
   double t_rhs_s;
   double t_cg_s;
   double t_total_s;
+  int32_t product_path;    /* FALKON_PATH_SIMT / _TENSOR: the product kernels the fit used */
 } falkon_fit_info;
 
 /* ---- context ------------------------------------------------------------------------- */

@@ -24,7 +24,7 @@ PATH_AUTO, PATH_SIMT, PATH_TENSOR = 0, 1, 2
 OPT_PATH, OPT_TC_MIN_D, OPT_TC_TERMS, OPT_KERNEL_TIMING, OPT_EXP_OFFLOAD = 1, 2, 3, 4, 5
 OPT_POTRF_OUTER, OPT_GEMM_WARPS = 6, 7
 OPT_SINGLE_EVAL, OPT_STRIP_BYTES, OPT_TC_CLUSTER, OPT_LOOKAHEAD = 8, 9, 10, 11
-OPT_ACCUM_F64, OPT_DIST_PRECOND = 12, 13
+OPT_ACCUM_F64, OPT_DIST_PRECOND, OPT_FIT_PRECISE = 12, 13, 14
 SINGLE_EVAL_OFF, SINGLE_EVAL_ON, SINGLE_EVAL_AUTO = 0, 1, 2
 TIMING_NAMES = ["prep", "pass_a", "pass_b", "reduce", "allreduce", "precond", "trsv", "vec"]
 
@@ -55,7 +55,7 @@ class FitInfo(ctypes.Structure):
                 ("failed_column", ctypes.c_int64), ("iters_run", ctypes.c_int32),
                 ("failed_iter", ctypes.c_int32), ("t_precond_s", ctypes.c_double),
                 ("t_rhs_s", ctypes.c_double), ("t_cg_s", ctypes.c_double),
-                ("t_total_s", ctypes.c_double)]
+                ("t_total_s", ctypes.c_double), ("product_path", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

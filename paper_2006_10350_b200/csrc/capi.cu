@@ -204,6 +204,38 @@ __global__ void gsc_rhs_kernel(double *__restrict__ r, const double *__restrict_
     r[i] = -fma(s, zt[i], r[i]);
 }
 
+// ------------------------------------------------------------------ fit-time product path
+// DESIGN.md reading d3: the tensor cores accumulate fp32 by truncation, so the folded-bias
+// fp16x3 cross term carries a bias of ~ulp(|partial sums|)/2 toward zero; its scale is the
+// magnitude of the biases a_p = -||x~_p||^2/2.  Measured (profiles/r2_fit_golden_*): on TAXI-
+// shaped data (d 9, sigma 1: mean ||c~||^2/2 = 6.5) the fit's alpha error is 7x the SIMT
+// path's (1.8e-3 vs 2.4e-4 at m = 2e4, n = 2e5), on HIGGS / MSD-shaped data (1.3-1.4) the
+// tensor path is as accurate or better.  So a Gaussian FIT whose AUTO path would be the tensor
+// kernel runs on the SIMT kernels when d <= 32 (the packed FP32 kernel) and the mean scaled
+// centre norm exceeds FIT_BIAS_MAX; products outside fits keep the tensor path.
+constexpr double FIT_BIAS_MAX = 4.0;
+struct FitPathScope {  // restores the context's path option at scope exit
+  falkon_ctx *ctx;
+  int saved;
+  int chosen = FALKON_PATH_AUTO;
+  explicit FitPathScope(falkon_ctx *c) : ctx(c), saved(c->opt.path) {}
+  ~FitPathScope() { ctx->opt.path = saved; }
+  int choose(const float *Cd, int64_t m, int64_t d, int kernel, double sigma) {
+    chosen = tc_supported(ctx, kernel, d) ? FALKON_PATH_TENSOR : FALKON_PATH_SIMT;
+    if (!ctx->opt.fit_precise || ctx->opt.path != FALKON_PATH_AUTO || chosen != FALKON_PATH_TENSOR ||
+        d > 32)
+      return FALKON_OK;
+    double msq = 0.0;
+    FK_TRY(center_spread(ctx, Cd, m, d, &msq));
+    const double bias = 0.5 * msq * 1.4426950408889634 / (sigma * sigma);  // mean |b_j|
+    if (bias > FIT_BIAS_MAX) {
+      ctx->opt.path = FALKON_PATH_SIMT;
+      chosen = FALKON_PATH_SIMT;
+    }
+    return FALKON_OK;
+  }
+};
+
 // ------------------------------------------------------------------ product pieces
 struct Fit {
   Prepared pp;
@@ -572,6 +604,9 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
       if (value != 0 && value != 1) return fail(FALKON_EINVAL, "accum_f64 must be 0 or 1");
       ctx->opt.accum_f64 = (int)value;
       return FALKON_OK;
+    case FALKON_OPT_FIT_PRECISE:
+      ctx->opt.fit_precise = value ? 1 : 0;
+      return FALKON_OK;
     case FALKON_OPT_DIST_PRECOND:
       ctx->opt.dist_precond = value ? 1 : 0;
       return FALKON_OK;
@@ -904,6 +939,7 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
     for (auto &ee : ev) cudaEventDestroy(ee);
   };
   Fit F;
+  FitPathScope fps(ctx);
   do {
     if (iters == 0) break;
     const void *Xd, *yd, *Cd;
@@ -914,6 +950,8 @@ int falkon_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_local,
                             pw, &loc)))
       break;
     cudaEventRecord(ev[1], ctx->stream);
+    if ((rc = fps.choose((const float *)Cd, m, d, kernel, sigma))) break;
+    loc.product_path = fps.chosen;
     // (2) RHS  R = A^-T T^-T Knm^T y   (Alg. 1 line 9)
     if ((rc = prepare_operands(ctx, (const float *)Xd, n_local, d, (const float *)Cd, m, kernel,
                                sigma, &F.pp)))
@@ -1037,12 +1075,15 @@ int falkon_gsc_fit(falkon_ctx *ctx, const float *X, const float *y, int64_t n_lo
   };
   int rc = FALKON_OK;
   Fit F;
+  FitPathScope fps(ctx);
   do {
     const void *Xd, *yd, *Cd, *yCd;
     if ((rc = stage_in(ctx, WS_STAGE_X, X, sizeof(float) * n_local * d, &Xd))) break;
     if ((rc = stage_in(ctx, WS_STAGE_Y, y, sizeof(float) * n_local, &yd))) break;
     if ((rc = stage_in(ctx, WS_STAGE_C, C, sizeof(float) * m * d, &Cd))) break;
     if ((rc = stage_in(ctx, WS_STAGE_V, yC, sizeof(float) * m, &yCd))) break;
+    if ((rc = fps.choose((const float *)Cd, m, d, kernel, sigma))) break;
+    loc.product_path = fps.chosen;
     if ((rc = prepare_operands(ctx, (const float *)Xd, n_local, d, (const float *)Cd, m, kernel,
                                sigma, &F.pp)))
       break;

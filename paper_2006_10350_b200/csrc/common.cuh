@@ -97,6 +97,7 @@ struct Options {
   int64_t strip_bytes = (int64_t)16 << 30;
   int accum_f64 = 0;    // FALKON_OPT_ACCUM_F64: fp64 v / w with DFMA contractions
   int dist_precond = 0; // FALKON_OPT_DIST_PRECOND: distributed build even on a 1-rank communicator
+  int fit_precise = 1;  // FALKON_OPT_FIT_PRECISE: fits on small-d, large-norm data take the SIMT path
 };
 
 }  // namespace falkon
@@ -184,6 +185,8 @@ int pass_A(falkon_ctx *ctx, const Prepared &pp, const float *z, double *w64, flo
 // u = Knm^T w (pass B) on this rank (no collective).  w: fp32 n (padded).  u: fp64 m.
 int pass_B(falkon_ctx *ctx, const Prepared &pp, const float *w, double *u);
 int f64_to_f32(falkon_ctx *ctx, const double *src, float *dst, int64_t n, int64_t n_pad);
+// mean over the centres of ||c_j - mean(C)||^2 (host result; synchronises the stream)
+int center_spread(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, double *mean_sq);
 // FALKON_OPT_ACCUM_F64 passes: z fp64 (zero-padded to a multiple of 128), contraction by DFMA of
 // the exact fp32 kernel value, fp64 output (w64: n, u: m).
 int pass_A64(falkon_ctx *ctx, const Prepared &pp, const double *z, double *w64);

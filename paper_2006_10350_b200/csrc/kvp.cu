@@ -79,6 +79,43 @@ int center_mean(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, double **
   return FALKON_OK;
 }
 
+// mean over the centres of ||c_j - mu||^2 (one CTA, fixed order: identical on every rank)
+__global__ void center_spread_kernel(const float *__restrict__ C, int64_t m, int64_t d,
+                                     const double *__restrict__ mu, double *__restrict__ out) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
+    double r = 0.0;
+    for (int64_t k = 0; k < d; ++k) {
+      const double x = (double)C[j * d + k] - mu[k];
+      r += x * x;
+    }
+    acc += r;
+  }
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0] / (double)m;
+}
+
+int center_spread(falkon_ctx *ctx, const float *C, int64_t m, int64_t d, double *mean_sq) {
+  double *mu;
+  FK_TRY(center_mean(ctx, C, m, d, &mu));
+  void *p;
+  FK_TRY(ws_get(ctx, WS_SCALARS, 64, &p));
+  {
+    LaunchScope ls(ctx, FALKON_T_PREP);
+    center_spread_kernel<<<1, 256, 0, ctx->stream>>>(C, m, d, mu, (double *)p);
+  }
+  FK_LAUNCH_CHECK();
+  FK_CUDA(cudaMemcpyAsync(mean_sq, p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  FK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FALKON_OK;
+}
+
 // ------------------------------------------------------------------ packing (SIMT layout)
 // One warp per row: out[r, k] = (in[r, k] - mu[k]) * g  (k < d), 0 for d <= k < dq;
 // bias[r] = -0.5 * ||out[r, :]||^2 computed in fp64 from the ROUNDED fp32 coordinates, so

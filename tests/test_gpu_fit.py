@@ -215,3 +215,23 @@ def test_fit_nonfinite_target_reports_failed_iter(ctx):
     # the context stays usable afterwards
     alpha, info = _fit_gpu(ctx, X, np.nan_to_num(y), C, G, cfg.sigma, cfg.lam, 2)
     assert np.all(np.isfinite(alpha)) and info["iters_run"] == 2
+
+
+@pytest.mark.parametrize("name,n,m,expect", [("taxi", 8000, 600, 1), ("tiny", None, None, 1),
+                                             ("higgs", 8000, 600, 2), ("msd", 4000, 500, 2)])
+def test_fit_precise_path_choice(ctx, name, n, m, expect):
+    """Reading d3 (FALKON_OPT_FIT_PRECISE): Gaussian fits whose mean scaled centre norm
+    ||c~||^2/2 exceeds 4 at d <= 32 (TAXI: 6.5, tiny: 5.8) run on the SIMT kernels; HIGGS
+    (1.4) and MSD (d = 90) keep the tensor kernel.  Reported in falkon_fit_info.product_path."""
+    from paper_2006_10350_b200 import binding
+    cfg, X, y, C = synth.make_problem(name, n=n, m=m)
+    ref = oracle.fit(X, y, C, G, cfg.sigma, cfg.lam, cfg.iters)
+    alpha, info = _fit_gpu(ctx, X, y, C, G, cfg.sigma, cfg.lam, cfg.iters)
+    assert info["product_path"] == expect
+    assert rel_l2(alpha, ref) <= 1e-3
+    ctx.set_option(binding.OPT_FIT_PRECISE, 0)
+    try:
+        _, info0 = _fit_gpu(ctx, X, y, C, G, cfg.sigma, cfg.lam, cfg.iters)
+    finally:
+        ctx.set_option(binding.OPT_FIT_PRECISE, 1)
+    assert info0["product_path"] == 2
