@@ -41,11 +41,18 @@ def main():
     ap.add_argument("--m", type=int)
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--workers", type=int, default=len(os.sched_getaffinity(0)))
+    ap.add_argument("--direct-max-d", type=int, default=None,
+                    help="oracle: direct differences only up to this d (default: the oracle's "
+                         "DIRECT_DIFF_MAX_D = 32); above it the fp64 norm expansion (error ~1e-13 "
+                         "relative on the squared distance, SURVEY.md E4), ~10x faster at d = 28")
     a = ap.parse_args()
     cfg = synth.CONFIGS[a.config]
     n, m = a.n or cfg.n, a.m or cfg.m
     out = golden_path(a.config, n, m, a.kernel)
     os.makedirs(os.path.dirname(out), exist_ok=True)
+    if a.direct_max_d is not None:
+        from oracle import falkon_oracle as fo
+        fo.DIRECT_DIFF_MAX_D = a.direct_max_d  # forked product workers inherit it
     t0 = time.time()
     _, X, y, C = synth.make_problem(a.config, n=n, m=m)
     Xs = synth.gen_X(cfg.seed, 0, N_TEST, cfg.d, stream=synth.STREAM_XTEST)
@@ -59,6 +66,7 @@ def main():
             "iters_run": info["iters_run"], "n_test": N_TEST, "test_stream": synth.STREAM_XTEST,
             "oracle_fit_s": round(t2 - t1, 1), "gen_s": round(t1 - t0, 1),
             "workers": a.workers, "host_cores": os.cpu_count(),
+            "direct_diff_max_d": a.direct_max_d if a.direct_max_d is not None else 32,
             "writer": "scripts/oracle_golden.py (oracle/ only)"}
     del info
     np.savez(out, alpha=alpha, pred=pred, meta=json.dumps(meta))
