@@ -104,9 +104,16 @@ enum {
                                    d <= 32 and the mean scaled centre norm ||c~||^2/2 exceeds 4
                                    (the tensor cores' truncating accumulation biases K there;
                                    DESIGN.md reading d3); 0 = always the AUTO path */
-  FALKON_OPT_DIST_PRECOND = 13  /* 1: build the preconditioner with the distributed schedule
+  FALKON_OPT_DIST_PRECOND = 13, /* 1: build the preconditioner with the distributed schedule
                                    (NEXT-1, below) even on a 1-rank NCCL communicator (tests the
                                    broadcast path on one GPU).  With world > 1 it is always used. */
+  FALKON_OPT_SE_GEMV_SMS = 15   /* single evaluation schedule: G > 0 = split SMs (two strip
+                                   buffers; the GEMV of strip s runs as a persistent grid of G CTAs
+                                   on a highest-priority stream while pass A of strip s + 1 takes
+                                   the other SMs; the last strip's GEMV uses the whole GPU);
+                                   0 (default) = serial (pass A of a strip, then its GEMV on all
+                                   SMs): measured faster on TIMIT (314 vs 352-389 ms per product,
+                                   DESIGN.md §7).  0 <= G < SM count, else FALKON_EINVAL. */
 };
 
 /* Per-launch-class accumulated device times in ms (falkon_ctx_timings). */

@@ -545,6 +545,9 @@ int falkon_ctx_destroy(falkon_ctx *ctx) {
   if (ctx->hi_stream) cudaStreamDestroy(ctx->hi_stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->lo_stream) cudaStreamDestroy(ctx->lo_stream);
+  if (ctx->se_stream) cudaStreamDestroy(ctx->se_stream);
+  for (auto &e : ctx->se_ev)
+    if (e) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return FALKON_OK;
@@ -592,6 +595,11 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
     case FALKON_OPT_SINGLE_EVAL:
       if (value < 0 || value > 2) return fail(FALKON_EINVAL, "single_eval must be 0, 1 or 2");
       ctx->opt.single_eval = (int)value;
+      return FALKON_OK;
+    case FALKON_OPT_SE_GEMV_SMS:
+      if (value < 0 || value >= ctx->sm_count)
+        return fail(FALKON_EINVAL, "se_gemv_sms must be in [0, SM count)");
+      ctx->opt.se_gemv_sms = (int)value;
       return FALKON_OK;
     case FALKON_OPT_STRIP_BYTES:
       if (value < ((int64_t)64 << 20)) return fail(FALKON_EINVAL, "strip bytes must be >= 64 MiB");

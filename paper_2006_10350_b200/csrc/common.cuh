@@ -97,6 +97,7 @@ struct Options {
   int64_t strip_bytes = (int64_t)16 << 30;
   int accum_f64 = 0;    // FALKON_OPT_ACCUM_F64: fp64 v / w with DFMA contractions
   int dist_precond = 0; // FALKON_OPT_DIST_PRECOND: distributed build even on a 1-rank communicator
+  int se_gemv_sms = 0;  // FALKON_OPT_SE_GEMV_SMS: split-SM single evaluation (0 = serial)
   int fit_precise = 1;  // FALKON_OPT_FIT_PRECISE: fits on small-d, large-norm data take the SIMT path
 };
 
@@ -122,6 +123,10 @@ struct falkon_ctx {
   // priority for the bulk trailing update; created on first use
   cudaStream_t hi_stream = nullptr, lo_stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // host-X pipeline of falkon_knm_matvec
+  // split-SM single evaluation (kvp_tc.cu): highest-priority stream of the strip GEMV and the
+  // events ordering pass A (strip buffer b written) / GEMV (buffer b read); created on first use
+  cudaStream_t se_stream = nullptr;
+  cudaEvent_t se_ev[4] = {};
   // co-resident CTAs of cluster launches, per kernel (kvp_tc.cu tc_cluster_slots)
   static constexpr int NSLOTCACHE = 8;
   const void *slot_fn[NSLOTCACHE] = {};

@@ -46,7 +46,13 @@ constexpr int TC_M = 128;
 constexpr int TC_N = 256;                         // Q rows per tile, shared-memory A (SS)
 constexpr int TC_N_TS = 192;                      // Q rows per tile, A in TMEM (TS)
 constexpr int TC_BK = 64;                          // fp16 per K box (128 B = one swizzle row)
-constexpr int TC_SBK = 32;  // streaming kernel: fp16 per K box (64 B rows, SWIZZLE_64B), 48 KB stages
+#ifndef FALKON_SBK
+#define FALKON_SBK 32
+#endif
+// streaming kernel: fp16 per K box (32: 64 B rows, SWIZZLE_64B, 48 KB stages; 64: 128 B rows,
+// SWIZZLE_128B, half the TMA row requests per byte)
+constexpr int TC_SBK = FALKON_SBK;
+static_assert(TC_SBK == 32 || TC_SBK == 64, "streaming K box");
 constexpr int TC_THREADS = 128 + 32 * 8;          // 4 control warps + 8 epilogue warps
 constexpr int TC_SMEM_MAX = 227 * 1024;
 constexpr int TC_A_BOX = TC_M * TC_BK * 2;         // 16 KB
@@ -638,6 +644,34 @@ __global__ void __launch_bounds__(32 * SE_WARPS) se_gemv_kernel(const float *__r
   }
 }
 
+// Split-SM strip GEMV (opt-in FALKON_OPT_SE_GEMV_SMS = G): a persistent grid of G CTAs streams
+// strip s while pass A of strip s + 1 runs on the other SMs (second stream, highest priority, so
+// the GEMV's CTAs take the first SMs pass A's CTAs release).  One 768-thread CTA per SM (its
+// shared-memory claim keeps pass-A CTAs off the SM); every warp loops over centre groups of
+// SE_CPW (strip_gemv_group: one writer per u_j, fixed order) with one tile's loads in flight per
+// lane (8 x 16 B), 96 KB per SM.  Measured alone: 95 GB/s per SM on 16 SMs (the standalone GEMV
+// is HBM-bound at 44 GB/s per SM on 148); beside pass A the schedule loses to the serial one
+// (TIMIT 352-389 ms vs 314 ms per product, profiles/r2_split_sm_gemv.jsonl): the GEMV on G SMs
+// drops to ~72 GB/s per SM and pass A loses more than its share of SMs.
+constexpr int BL_WARPS = 24;
+constexpr int BL_SMEM = 160 * 1024;
+template <bool WEIGHTED, bool WD>
+__global__ void __launch_bounds__(32 * BL_WARPS, 1)
+    se_gemv_ldg_kernel(const float *__restrict__ K, int64_t m, const void *__restrict__ wv,
+                       const float *__restrict__ dw, int64_t rows, double *__restrict__ acc,
+                       int first) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntile = cdiv<int64_t>(rows, TC_M);
+  const int64_t ng = cdiv<int64_t>(m, SE_CPW);
+  for (int64_t g = (int64_t)blockIdx.x * BL_WARPS + wid; g < ng; g += (int64_t)gridDim.x * BL_WARPS) {
+    const int64_t jb = g * SE_CPW;
+    const double v = strip_gemv_group<WD, false>(K, m, wv, WEIGHTED ? dw : nullptr, rows, 0, ntile,
+                                                 m, jb, lane);
+    const int64_t j = jb + lane;
+    if (lane < SE_CPW && j < m) acc[j] = first ? v : acc[j] + v;
+  }
+}
+
 // Fused strip GEMV (warps 2 and 3 of a single-evaluation pass-A CTA, idle otherwise): while
 // the tensor pipe evaluates strip s, these warps stream strip s - 1 (the other k buffer) from
 // HBM.  The launch's CTAs partition the centres: CTA c owns centre groups [c G / N, (c+1) G / N)
@@ -948,7 +982,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     const uint32_t idesc = (1u << 4) | ((uint32_t)(NT >> 3) << 17) |
                            ((uint32_t)((PAIR ? 2 : 1) * TC_M >> 4) << 24);
     const uint64_t a0 = sw128_desc(smem_u32(sA));
-    const uint64_t b0 = STREAM ? sw64_desc(smem_u32(sB)) : sw128_desc(smem_u32(sB));
+    const uint64_t b0 = (STREAM && TC_SBK == 32) ? sw64_desc(smem_u32(sB)) : sw128_desc(smem_u32(sB));
     const int nk = a.nk;
     auto adesc = [&](int c) -> uint64_t {
       return a0 + (uint64_t)(((c >> 2) * TC_A_BOX + (c & 3) * 32) >> 4);
@@ -1242,7 +1276,7 @@ static int make_map(CUtensorMap *map, const __half *base, int64_t rows, int k_el
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void *)base, dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   stream ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   (stream && TC_SBK == 32) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FALKON_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return FALKON_OK;
@@ -1531,6 +1565,18 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
     }
     if (ctas >= 8 * slots && eff > 0.9) break;
   }
+  // L2-resident Q ranges: when the P tiles need several waves, every wave streams the same Q
+  // range; a range larger than L2 is then re-read from HBM once per wave (MSD pass B: 2.7x the
+  // algorithmic bytes, profiles/ncu_traffic.json).  Split Q so one range (packed rows of
+  // 4 * d16 B) fits in FALKON_TC_L2Q_MB (default 40 MB of the 126 MB L2; 0 = off).
+  {
+    int64_t l2q = (int64_t)40 << 20;
+    if (const char *e = getenv("FALKON_TC_L2Q_MB")) l2q = (int64_t)atoi(e) << 20;
+    if (l2q > 0 && gx > slots) {
+      const int64_t need = cdiv<int64_t>(nq * (int64_t)4 * d16, l2q);
+      if (need > best_s && qt / need >= 4) best_s = need;
+    }
+  }
   int64_t qps = round_up<int64_t>(cdiv<int64_t>(nq, best_s), nt);
   const int64_t splits = std::max<int64_t>(1, cdiv<int64_t>(nq, qps));
   double *part = out64;
@@ -1656,7 +1702,13 @@ static int single_eval_impl(falkon_ctx *ctx, const Prepared &pp, const float *z,
   // bulk-copy ring depth, and the pass-A CTAs wait for it.
   const char *fe = getenv("FALKON_FUSED_GEMV");
   const bool fused = fe && atoi(fe) != 0;
-  const int nbuf = fused ? 2 : 1;
+  // split-SM schedule (FALKON_OPT_SE_GEMV_SMS = G > 0): the GEMV of strip s runs as a
+  // persistent grid of G CTAs on the highest-priority stream while pass A of strip s + 1 runs
+  // on the remaining SMs; buffer b = s & 1 is rewritten by pass A(s + 2) only after GEMV(s)
+  int gsm = fused ? 0 : ctx->opt.se_gemv_sms;
+  if (const char *e = getenv("FALKON_SE_GEMV_SMS")) gsm = fused ? 0 : atoi(e);  // A/B
+  gsm = std::max(0, std::min(gsm, ctx->sm_count - 1));
+  const int nbuf = (fused || gsm > 0) ? 2 : 1;
   const int64_t tile_bytes = (int64_t)4 * TC_M * ldk;
   const int64_t ntiles = cdiv<int64_t>(n, TC_M);
   int64_t tiles = std::min<int64_t>(std::max<int64_t>(1, budget / nbuf / tile_bytes), ntiles);
@@ -1690,6 +1742,50 @@ static int single_eval_impl(falkon_ctx *ctx, const Prepared &pp, const float *z,
     FK_LAUNCH_CHECK();
     return FALKON_OK;
   };
+  if (gsm > 0 && nstrips > 1) {
+    auto bulk = [&](const float *K, int64_t r0g, int64_t nrg, int first) -> int {
+      LaunchScope ls(ctx, FALKON_T_PASS_B);
+      const float *dwl = dw ? dw + r0g : nullptr;
+      const void *wr = wrow(r0g);
+      auto fn = z64 ? (dw ? se_gemv_ldg_kernel<true, true> : se_gemv_ldg_kernel<false, true>)
+                    : (dw ? se_gemv_ldg_kernel<true, false> : se_gemv_ldg_kernel<false, false>);
+      FK_CUDA(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, BL_SMEM));
+      fn<<<(unsigned)gsm, 32 * BL_WARPS, BL_SMEM, ctx->stream>>>(K, m, wr, dwl, nrg, u, first);
+      FK_LAUNCH_CHECK();
+      return FALKON_OK;
+    };
+    if (!ctx->se_stream) {
+      int least = 0, greatest = 0;
+      FK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      FK_CUDA(cudaStreamCreateWithPriority(&ctx->se_stream, cudaStreamNonBlocking, greatest));
+      for (auto &e : ctx->se_ev) FK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaStream_t base = ctx->stream, side = ctx->se_stream;
+    cudaEvent_t *evA = ctx->se_ev, *evG = ctx->se_ev + 2;  // buffer b written / read
+    for (int64_t s = 0; s < nstrips; ++s) {
+      const int b = (int)(s & 1);
+      const int64_t r0 = s * rows;
+      const int64_t nr = std::min<int64_t>(rows, n - r0);
+      if (s >= 2) FK_CUDA(cudaStreamWaitEvent(base, evG[b], 0));  // GEMV(s - 2) done with buffer b
+      if (z64)
+        FK_TRY(tc_launch(ctx, pp, true, nullptr, w64 + r0, nullptr, 1, r0, nr, Kbuf[b], ldk, z64));
+      else
+        FK_TRY(tc_launch(ctx, pp, true, z, nullptr, w32 + r0, 1, r0, nr, Kbuf[b], ldk));
+      if (s + 1 < nstrips) {
+        FK_CUDA(cudaEventRecord(evA[b], base));
+        FK_CUDA(cudaStreamWaitEvent(side, evA[b], 0));
+        ctx->stream = side;
+        const int rc = bulk(Kbuf[b], r0, nr, s == 0 ? 1 : 0);
+        ctx->stream = base;
+        FK_TRY(rc);
+        FK_CUDA(cudaEventRecord(evG[b], side));
+      } else {  // the last strip's GEMV on the whole GPU, after GEMV(s - 1) (both write u)
+        FK_CUDA(cudaStreamWaitEvent(base, evG[b ^ 1], 0));
+        FK_TRY(gemv(Kbuf[b], r0, nr, 0));
+      }
+    }
+    return FALKON_OK;
+  }
   for (int64_t s = 0; s < nstrips; ++s) {
     const int64_t r0 = s * rows;
     const int64_t nr = std::min<int64_t>(rows, n - r0);

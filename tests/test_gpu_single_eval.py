@@ -176,3 +176,43 @@ def test_cta_pair_variant(ctx, pair, se, accum_f64, d, sigma):
         ctx.set_option(binding.OPT_SINGLE_EVAL, 2)
         ctx.set_option(binding.OPT_ACCUM_F64, 0)
     assert rel_l2(u, oracle.knm_t_knm_vec(X, C, v, G, sigma)) <= 1e-4
+
+
+@pytest.mark.parametrize("accum_f64", [0, 1])
+@pytest.mark.parametrize("gsm", [1, 16, 147])
+def test_split_sm_gemv_variant(ctx, accum_f64, gsm):
+    """FALKON_OPT_SE_GEMV_SMS = G > 0: the GEMV of strip s as a persistent grid of G CTAs
+    (se_gemv_ldg_kernel, one 768-thread CTA per SM) on a second stream beside pass A of strip s + 1, two
+    strip buffers, the last strip's GEMV on the whole GPU.  Deterministic, the serial schedule
+    to fp32 regrouping (fp64 contractions: 1e-12) and the oracle bar; 5 strips + ragged tail,
+    m not a multiple of the 8-centre groups."""
+    from paper_2006_10350_b200 import binding
+    n, m, d, sigma = 40001, 1030, 300, 12.0
+    X = synth.gen_X(47, 0, n, d)
+    C = X[synth.center_indices(47, n, m)]
+    v = synth.gen_vec(47, m).astype(np.float64)
+    dX, dC, dv = dev(X), dev(C), dev(v)
+    ctx.set_option(binding.OPT_SINGLE_EVAL, 1)
+    ctx.set_option(binding.OPT_STRIP_BYTES, 64 << 20)
+    ctx.set_option(binding.OPT_ACCUM_F64, accum_f64)
+    try:
+        a = host(ctx.knm_matvec(dX, dC, dv, G, sigma, zeros(m)))
+        ctx.set_option(binding.OPT_SE_GEMV_SMS, gsm)
+        b1 = host(ctx.knm_matvec(dX, dC, dv, G, sigma, zeros(m)))
+        b2 = host(ctx.knm_matvec(dX, dC, dv, G, sigma, zeros(m)))
+    finally:
+        ctx.set_option(binding.OPT_SE_GEMV_SMS, 0)
+        ctx.set_option(binding.OPT_SINGLE_EVAL, 2)
+        ctx.set_option(binding.OPT_STRIP_BYTES, 16 << 30)
+        ctx.set_option(binding.OPT_ACCUM_F64, 0)
+    assert np.array_equal(b1, b2)
+    assert rel_l2(b1, a) <= (1e-12 if accum_f64 else 1e-7)
+    assert rel_l2(b1, oracle.knm_t_knm_vec(X, C, v, G, sigma)) <= 1e-4
+
+
+def test_split_sm_gemv_option_range(ctx):
+    from paper_2006_10350_b200 import binding
+    with pytest.raises(binding.FalkonError):
+        ctx.set_option(binding.OPT_SE_GEMV_SMS, -1)
+    with pytest.raises(binding.FalkonError):
+        ctx.set_option(binding.OPT_SE_GEMV_SMS, 100000)
