@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--gsc-n", type=int, default=None, help="override the GSC workload's n")
     ap.add_argument("--single-eval", type=int, default=None, choices=[0, 1, 2],
                     help="products: 0 two passes, 1 single evaluation (k strip), 2 auto")
+    ap.add_argument("--strip-mb", type=int, default=None,
+                    help="single evaluation: k strip budget in MiB (FALKON_OPT_STRIP_BYTES)")
     ap.add_argument("--tc-cluster", type=int, default=None, choices=[1, 2],
                     help="tensor path: 1 CTA or 2-CTA clusters multicasting the Q boxes")
     ap.add_argument("--multi-k", type=int, default=0,
@@ -404,6 +406,8 @@ def main():
         ctx.set_option(binding.OPT_EXP_OFFLOAD, args.exp_offload)
     if args.single_eval is not None:
         ctx.set_option(binding.OPT_SINGLE_EVAL, args.single_eval)
+    if args.strip_mb is not None:
+        ctx.set_option(binding.OPT_STRIP_BYTES, args.strip_mb << 20)
     if args.accum_f64 is not None:
         ctx.set_option(binding.OPT_ACCUM_F64, args.accum_f64)
     if args.tc_cluster is not None:

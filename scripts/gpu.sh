@@ -12,6 +12,7 @@
 #   sweeps                     SIMT/tensor crossover, Fig. mvm_impl n- and d-sweeps
 #   sanitize                   compute-sanitizer memcheck / racecheck / synccheck
 #   reference [CFG]            the oracle arm (bench.py --impl reference)
+#   probes                     L2 / HBM bandwidth and pipe-rate microbenchmarks
 #   configscale                the -m gpu slow config-scale fit parity against tests/golden/fits
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"; mkdir -p gpurun_out
 task=$1; shift
@@ -65,6 +66,10 @@ sanitize)
 reference)
   timeout 900 python bench.py --impl reference --config ${1:-timit} --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
   tail -c 800 gpurun_out/bench_ref.json ;;
+probes)
+  for p in l2_bw pipe_rates; do
+    nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/$p scripts/probes/$p.cu && /tmp/$p | tee gpurun_out/probe_$p.txt
+  done ;;
 configscale)
   timeout 3000 python -m pytest tests/test_gpu_fit_configscale.py -m gpu -q -rA > gpurun_out/configscale.txt 2>&1
   tail -15 gpurun_out/configscale.txt ;;
