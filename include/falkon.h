@@ -60,7 +60,12 @@ enum {
 };
 
 /* Product-path selection (falkon_ctx_set_option FALKON_OPT_PATH). */
-enum { FALKON_PATH_AUTO = 0, FALKON_PATH_SIMT = 1, FALKON_PATH_TENSOR = 2 };
+enum { FALKON_PATH_AUTO = 0, FALKON_PATH_SIMT = 1, FALKON_PATH_TENSOR = 2,
+       /* fp64 throughout (reading d4): coordinates (x - mu) g in fp64 from the fp32
+          inputs, fp64 exponent and exp2, fp64 contractions (~1e-15 relative kernel values; the
+          FP64 pipe binds, ~4e11 n*m/s at d = 28).  Single-vector products and fits only
+          (multi-output calls return FALKON_EUNSUPPORTED). */
+       FALKON_PATH_F64 = 3 };
 
 /* Options (falkon_ctx_set_option). */
 enum {
@@ -99,14 +104,24 @@ enum {
                                    DFMA in fp64 (k itself stays fp32).  Applies to the single-vector
                                    products, fits, GSC fits and predictions; multi-output calls
                                    stay fp32.  See DESIGN.md for the measured default. */
-  FALKON_OPT_FIT_PRECISE = 14,  /* 1 (default): a Gaussian fit (falkon_fit, falkon_gsc_fit) whose
-                                   AUTO path is the tensor kernel runs on the SIMT kernels when
-                                   d <= 32 and the mean scaled centre norm ||c~||^2/2 exceeds 4
-                                   (the tensor cores' truncating accumulation biases K there;
-                                   DESIGN.md reading d3); 0 = always the AUTO path */
+  FALKON_OPT_FIT_PRECISE = 14,  /* 1 (default): fits (falkon_fit, falkon_gsc_fit) on the AUTO path
+                                   take (a) FALKON_PATH_F64 when d <= 32 and m > 25,000 (fp32
+                                   kernel values put alpha past the 1e-3 bar there, DESIGN.md
+                                   reading d4), else (b) the SIMT kernels when the AUTO path is
+                                   the tensor kernel, d <= 32 and the mean scaled centre norm
+                                   ||c~||^2/2 exceeds 4 (the tensor cores' truncating accumulation
+                                   biases K, reading d3); 0 = always the AUTO path */
   FALKON_OPT_DIST_PRECOND = 13, /* 1: build the preconditioner with the distributed schedule
                                    (NEXT-1, below) even on a 1-rank NCCL communicator (tests the
                                    broadcast path on one GPU).  With world > 1 it is always used. */
+  FALKON_OPT_OZAKI = 16,        /* 1 (default): the preconditioner's large fp64 GEMMs (Cholesky
+                                   trailing updates with k range >= 256, the LAUUM T D T^T in k
+                                   chunks of 1024) run on the int8 tensor cores by the
+                                   Ozaki scheme (error-free split into 8 signed 7-bit slices per
+                                   row-scaled operand, 36 exact int32 slice products, fp64
+                                   recombination; ~1e-15 relative, deterministic, not bitwise equal
+                                   to the DMMA GEMM); 0 = fp64 DMMA.  Measured: m = 5e4 build
+                                   4.10 -> 3.06 s. */
   FALKON_OPT_SE_GEMV_SMS = 15   /* single evaluation schedule: G > 0 = split SMs (two strip
                                    buffers; the GEMV of strip s runs as a persistent grid of G CTAs
                                    on a highest-priority stream while pass A of strip s + 1 takes
@@ -139,7 +154,7 @@ typedef struct {
   double t_rhs_s;
   double t_cg_s;
   double t_total_s;
-  int32_t product_path;    /* FALKON_PATH_SIMT / _TENSOR: the product kernels the fit used */
+  int32_t product_path;    /* FALKON_PATH_SIMT / _TENSOR / _F64: the product kernels the fit used */
 } falkon_fit_info;
 
 /* ---- context ------------------------------------------------------------------------- */

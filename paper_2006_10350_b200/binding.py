@@ -20,12 +20,12 @@ GAUSSIAN = 0
 LAPLACIAN = 1
 KERNELS = {"gaussian": GAUSSIAN, "laplacian": LAPLACIAN}
 
-PATH_AUTO, PATH_SIMT, PATH_TENSOR = 0, 1, 2
+PATH_AUTO, PATH_SIMT, PATH_TENSOR, PATH_F64 = 0, 1, 2, 3
 OPT_PATH, OPT_TC_MIN_D, OPT_TC_TERMS, OPT_KERNEL_TIMING, OPT_EXP_OFFLOAD = 1, 2, 3, 4, 5
 OPT_POTRF_OUTER, OPT_GEMM_WARPS = 6, 7
 OPT_SINGLE_EVAL, OPT_STRIP_BYTES, OPT_TC_CLUSTER, OPT_LOOKAHEAD = 8, 9, 10, 11
 OPT_ACCUM_F64, OPT_DIST_PRECOND, OPT_FIT_PRECISE = 12, 13, 14
-OPT_SE_GEMV_SMS = 15
+OPT_SE_GEMV_SMS, OPT_OZAKI = 15, 16
 SINGLE_EVAL_OFF, SINGLE_EVAL_ON, SINGLE_EVAL_AUTO = 0, 1, 2
 TIMING_NAMES = ["prep", "pass_a", "pass_b", "reduce", "allreduce", "precond", "trsv", "vec"]
 

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 OUT = os.path.join(HERE, "libfalkon.so")
 BUILD = os.path.join(HERE, "build")
-SOURCES = ["runtime.cu", "kvp.cu", "kvp_tc.cu", "precond.cu", "capi.cu"]
+SOURCES = ["runtime.cu", "kvp.cu", "kvp_tc.cu", "precond.cu", "ozaki.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
               "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
@@ -31,7 +31,9 @@ def nvcc() -> str:
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(BUILD, src.replace(".cu", ".o"))
     srcp = os.path.join(CSRC, src)
-    deps = [srcp, os.path.join(CSRC, "common.cuh"), os.path.join(INCLUDE, "falkon.h")]
+    deps = [srcp, os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "tcgen05.cuh"),
+            os.path.join(CSRC, "precond.cuh"),
+            os.path.join(INCLUDE, "falkon.h")]
     if os.path.exists(obj) and all(os.path.getmtime(obj) >= os.path.getmtime(d) for d in deps):
         return obj
     cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", srcp, "-o", obj]

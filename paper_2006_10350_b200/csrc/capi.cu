@@ -214,6 +214,8 @@ __global__ void gsc_rhs_kernel(double *__restrict__ r, const double *__restrict_
 // kernel runs on the SIMT kernels when d <= 32 (the packed FP32 kernel) and the mean scaled
 // centre norm exceeds FIT_BIAS_MAX; products outside fits keep the tensor path.
 constexpr double FIT_BIAS_MAX = 4.0;
+// reading d4: fits with d <= 32 and more centres than this run on FALKON_PATH_F64
+constexpr int64_t FIT_F64_MIN_M = 25000;
 struct FitPathScope {  // restores the context's path option at scope exit
   falkon_ctx *ctx;
   int saved;
@@ -221,10 +223,20 @@ struct FitPathScope {  // restores the context's path option at scope exit
   explicit FitPathScope(falkon_ctx *c) : ctx(c), saved(c->opt.path) {}
   ~FitPathScope() { ctx->opt.path = saved; }
   int choose(const float *Cd, int64_t m, int64_t d, int kernel, double sigma) {
-    chosen = tc_supported(ctx, kernel, d) ? FALKON_PATH_TENSOR : FALKON_PATH_SIMT;
-    if (!ctx->opt.fit_precise || ctx->opt.path != FALKON_PATH_AUTO || chosen != FALKON_PATH_TENSOR ||
-        d > 32)
+    if (ctx->opt.path == FALKON_PATH_F64) {
+      chosen = FALKON_PATH_F64;
       return FALKON_OK;
+    }
+    chosen = tc_supported(ctx, kernel, d) ? FALKON_PATH_TENSOR : FALKON_PATH_SIMT;
+    if (!ctx->opt.fit_precise || ctx->opt.path != FALKON_PATH_AUTO || d > 32) return FALKON_OK;
+    // reading d4: small-d fits at large m need fp64 kernel values for the alpha bar (measured:
+    // HIGGS-shaped n = 1.05M, m = 5e4: alpha 1.4e-3 on fp32-class kernels of either pipe)
+    if (m > FIT_F64_MIN_M) {
+      ctx->opt.path = FALKON_PATH_F64;
+      chosen = FALKON_PATH_F64;
+      return FALKON_OK;
+    }
+    if (chosen != FALKON_PATH_TENSOR) return FALKON_OK;
     double msq = 0.0;
     FK_TRY(center_spread(ctx, Cd, m, d, &msq));
     const double bias = 0.5 * msq * 1.4426950408889634 / (sigma * sigma);  // mean |b_j|
@@ -438,7 +450,7 @@ static int alloc_fit_vectors(falkon_ctx *ctx, Fit &F) {
   FK_TRY(ws_get(ctx, WS_W32, sizeof(float) * pad128(F.pp.n), &b));
   F.v32 = (float *)a;
   F.w32 = (float *)b;
-  F.f64 = ctx->opt.accum_f64 != 0;
+  F.f64 = ctx->opt.accum_f64 != 0 || F.pp.path == FALKON_PATH_F64;
   if (F.f64) {
     FK_TRY(ws_get(ctx, WS_V64, sizeof(double) * pad128(F.pp.m), &a));
     FK_TRY(ws_get(ctx, WS_W64, sizeof(double) * pad128(F.pp.n), &b));
@@ -563,7 +575,7 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
   if (!ctx) return fail(FALKON_EINVAL, "ctx is NULL");
   switch (option) {
     case FALKON_OPT_PATH:
-      if (value < 0 || value > 2) return fail(FALKON_EINVAL, "bad path");
+      if (value < 0 || value > 3) return fail(FALKON_EINVAL, "bad path");
       ctx->opt.path = (int)value;
       return FALKON_OK;
     case FALKON_OPT_TC_MIN_D:
@@ -595,6 +607,10 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
     case FALKON_OPT_SINGLE_EVAL:
       if (value < 0 || value > 2) return fail(FALKON_EINVAL, "single_eval must be 0, 1 or 2");
       ctx->opt.single_eval = (int)value;
+      return FALKON_OK;
+    case FALKON_OPT_OZAKI:
+      if (value < 0 || value > 1) return fail(FALKON_EINVAL, "ozaki must be 0 or 1");
+      ctx->opt.ozaki = (int)value;
       return FALKON_OK;
     case FALKON_OPT_SE_GEMV_SMS:
       if (value < 0 || value >= ctx->sm_count)

@@ -461,6 +461,123 @@ __global__ void __launch_bounds__(KVP_THREADS)
   }
 }
 
+// ------------------------------------------------------------------ fp64 path (FALKON_PATH_F64)
+// For fits whose alpha must match an fp64 reference where fp32 kernel values cannot (small d,
+// large m: the CG iterate amplifies the ~1e-7 relative error of fp32 k; reading d4):
+// coordinates (x - mu) g computed in fp64 from the fp32 inputs (exact upcast), the exponent
+// and the exp2 (CUDA's exp2(double), ~1 ulp) in fp64, fp64 contractions.  Same primitive and
+// tiling as kvp_generic_kernel (one P point per thread, TQ64 Q points per shared-memory tile,
+// bulk-copy ring); the FP64 pipe (~60 DFMA/clk/SM on B200) binds.
+constexpr int KVP64_TQ = 16;
+__global__ void pack_rows64_kernel(const float *__restrict__ in, int64_t rows, int64_t rows_pad,
+                                   int64_t d, const double *__restrict__ mu, double g, int dq,
+                                   double *__restrict__ out, double *__restrict__ bias) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); r < rows_pad;
+       r += (int64_t)gridDim.x * wpb) {
+    double ss = 0.0;
+    for (int k = lane; k < dq; k += 32) {
+      const double v = (r < rows && k < d) ? ((double)in[r * d + k] - mu[k]) * g : 0.0;
+      out[r * dq + k] = v;
+      ss = fma(v, v, ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (bias && lane == 0) bias[r] = -0.5 * ss;
+  }
+}
+
+template <int KER>
+__global__ void __launch_bounds__(KVP_THREADS)
+    kvp64_kernel(const double *__restrict__ P, const double *__restrict__ pa, int64_t np,
+                 const double *__restrict__ Q, const double *__restrict__ qb,
+                 const double *__restrict__ z, int64_t nq, int64_t q_per_split, int dq,
+                 double *__restrict__ out64) {
+  constexpr int TQ = KVP64_TQ;
+  extern __shared__ __align__(128) double smem_d[];
+  const int QF = TQ * dq;
+  double *const SB = smem_d + 2 * QF;
+  double *const SZ = SB + 2 * TQ;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(SZ + 2 * TQ);
+  const int tid = threadIdx.x;
+  const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
+  const int64_t qhi = min(nq, qlo + q_per_split);
+  const int ntiles = qhi > qlo ? (int)cdiv<int64_t>(qhi - qlo, TQ) : 0;
+  auto issue = [&](int t) {  // Q rows, biases and z are zero-padded to a multiple of 128
+    const int64_t q0 = qlo + (int64_t)t * TQ;
+    const int cnt2 = ((int)lmin(TQ, qhi - q0) + 1) & ~1;  // 16-byte multiples
+    const int s = t & 1;
+    const uint32_t bq = (uint32_t)cnt2 * dq * 8, bs = (uint32_t)cnt2 * 8;
+    mbar_expect_tx(&bar[s], bq + (KER == FALKON_GAUSSIAN ? bs : 0) + bs);
+    bulk_g2s(smem_d + s * QF, Q + q0 * dq, bq, &bar[s]);
+    if (KER == FALKON_GAUSSIAN) bulk_g2s(SB + s * TQ, qb + q0, bs, &bar[s]);
+    bulk_g2s(SZ + s * TQ, z + q0, bs, &bar[s]);
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (ntiles > 0) issue(0);
+    if (ntiles > 1) issue(1);
+  }
+  const int64_t p_raw = (int64_t)blockIdx.x * KVP_THREADS + tid;
+  const int64_t p = min(p_raw, np - 1);
+  const double *prow = P + p * dq;
+  const double pav = (KER == FALKON_GAUSSIAN) ? pa[p] : 0.0;
+  double acc = 0.0;
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t & 1;
+    mbar_wait(&bar[s], (t >> 1) & 1);
+    const int cnt = (int)lmin(TQ, qhi - (qlo + (int64_t)t * TQ));
+    const double *sqs = smem_d + s * QF;
+    double e[TQ];
+#pragma unroll
+    for (int j = 0; j < TQ; ++j) e[j] = (KER == FALKON_GAUSSIAN) ? pav + SB[s * TQ + j] : 0.0;
+    for (int k0 = 0; k0 < dq; k0 += 16) {
+      double pch[16];
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) {
+        double2 v2 = make_double2(0.0, 0.0);
+        if (k0 + 2 * k2 < dq) v2 = __ldg(reinterpret_cast<const double2 *>(prow + k0) + k2);
+        pch[2 * k2] = v2.x;
+        pch[2 * k2 + 1] = v2.y;
+      }
+#pragma unroll
+      for (int j = 0; j < TQ; ++j) {
+        const double2 *qrow = reinterpret_cast<const double2 *>(sqs + j * dq + k0);
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+          if (k0 + 2 * k2 < dq) {
+            const double2 q2 = qrow[k2];
+            if (KER == FALKON_GAUSSIAN) {
+              e[j] = fma(pch[2 * k2], q2.x, e[j]);
+              e[j] = fma(pch[2 * k2 + 1], q2.y, e[j]);
+            } else {
+              double df = pch[2 * k2] - q2.x;
+              e[j] = fma(df, df, e[j]);
+              df = pch[2 * k2 + 1] - q2.y;
+              e[j] = fma(df, df, e[j]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < TQ; ++j)
+      if (j < cnt) {
+        const double kv = (KER == FALKON_GAUSSIAN) ? exp2(fmin(e[j], 0.0)) : exp2(-sqrt(e[j]));
+        acc = fma(kv, SZ[s * TQ + j], acc);
+      }
+    __syncthreads();
+    if (tid == 0 && t + 2 < ntiles) issue(t + 2);
+  }
+  if (p_raw < np) out64[(int64_t)blockIdx.y * np + p_raw] = acc;
+}
+
 // ------------------------------------------------------------------ reductions / conversions
 __global__ void reduce_splits_kernel(const double *__restrict__ part, int splits, int64_t np,
                                      double *__restrict__ out64, float *__restrict__ out32) {
@@ -627,6 +744,51 @@ static int kvp_launch(falkon_ctx *ctx, int kernel, int64_t d, int dq, const floa
   return FALKON_OK;
 }
 
+// fp64 path launch: out64[p] = sum_q k(P_p, Q_q) z_q (+ the deterministic split reduction)
+static int kvp64_launch(falkon_ctx *ctx, int kernel, int dq, const double *P, const double *pa,
+                        int64_t np, const double *Q, const double *qb, const double *z,
+                        int64_t nq, int cls, double *out64) {
+  if (np <= 0) return FALKON_OK;
+  constexpr int TQ = KVP64_TQ;
+  const void *fn = kernel == FALKON_GAUSSIAN ? (const void *)kvp64_kernel<FALKON_GAUSSIAN>
+                                             : (const void *)kvp64_kernel<FALKON_LAPLACIAN>;
+  const size_t smem = (size_t)(2 * TQ * dq + 4 * TQ) * 8 + 16;
+  if (smem > 227 * 1024) return fail(FALKON_EUNSUPPORTED, "fp64 path: d too large");
+  FK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t gx = cdiv<int64_t>(np, KVP_THREADS);
+  const int64_t capacity = (int64_t)ctx->sm_count * occupancy(fn, KVP_THREADS, smem);
+  int64_t splits = 1;
+  if (gx < capacity) {
+    splits = std::max<int64_t>(1, capacity / gx);
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, nq / (4 * TQ)));
+    splits = std::min<int64_t>(splits, 65535);
+  }
+  const int64_t qps = round_up<int64_t>(cdiv<int64_t>(nq, splits), TQ);
+  splits = std::max<int64_t>(1, cdiv<int64_t>(nq, qps));
+  if (gx > 0x7fffffffLL) return fail(FALKON_EINVAL, "too many rows for one launch");
+  double *part = out64;
+  if (splits > 1) {
+    void *pp;
+    FK_TRY(ws_get(ctx, WS_PART, sizeof(double) * splits * np, &pp));
+    part = (double *)pp;
+  }
+  {
+    LaunchScope ls(ctx, cls);
+    typedef void (*f64_fn)(const double *, const double *, int64_t, const double *, const double *,
+                           const double *, int64_t, int64_t, int, double *);
+    ((f64_fn)fn)<<<dim3((unsigned)gx, (unsigned)splits), KVP_THREADS, smem, ctx->stream>>>(
+        P, pa, np, Q, qb, z, nq, qps, dq, part);
+  }
+  FK_LAUNCH_CHECK();
+  if (splits > 1) {
+    LaunchScope ls(ctx, FALKON_T_REDUCE);
+    reduce_splits_kernel<<<(unsigned)cdiv<int64_t>(np, 256), 256, 0, ctx->stream>>>(
+        part, (int)splits, np, out64, nullptr);
+    FK_LAUNCH_CHECK();
+  }
+  return FALKON_OK;
+}
+
 // ------------------------------------------------------------------ public-ish entry points
 int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, const float *C,
                      int64_t m, int kernel, double sigma, Prepared *pp) {
@@ -636,6 +798,35 @@ int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, cons
   pp->kernel = kernel;
   double *mu;
   FK_TRY(center_mean(ctx, C, m, d, &mu));
+  if (ctx->opt.path == FALKON_PATH_F64) {  // fp64 coordinates and biases, row-major [rows][dq]
+    pp->path = FALKON_PATH_F64;
+    const int dq = (int)round_up<int64_t>(d, 2);
+    pp->dq = dq;
+    const double g = kernel == FALKON_GAUSSIAN ? std::sqrt(LOG2E) / sigma : LOG2E / sigma;
+    const int64_t n_pad = round_up<int64_t>(std::max<int64_t>(n, 1), 128);
+    const int64_t m_pad = round_up<int64_t>(m, 128);
+    void *xp, *xa, *cp, *cb;
+    FK_TRY(ws_get(ctx, WS_XP, sizeof(double) * n_pad * dq, &xp));
+    FK_TRY(ws_get(ctx, WS_XA, sizeof(double) * n_pad, &xa));
+    FK_TRY(ws_get(ctx, WS_CP, sizeof(double) * m_pad * dq, &cp));
+    FK_TRY(ws_get(ctx, WS_CB, sizeof(double) * m_pad, &cb));
+    const bool gauss = kernel == FALKON_GAUSSIAN;
+    {
+      LaunchScope ls(ctx, FALKON_T_PREP);
+      pack_rows64_kernel<<<(unsigned)std::min<int64_t>(cdiv<int64_t>(m_pad, 8), 65535), 256, 0,
+                           ctx->stream>>>(C, m, m_pad, d, mu, g, dq, (double *)cp,
+                                          gauss ? (double *)cb : nullptr);
+      pack_rows64_kernel<<<(unsigned)std::min<int64_t>(cdiv<int64_t>(n_pad, 8), (int64_t)ctx->sm_count * 64),
+                           256, 0, ctx->stream>>>(X, n, n_pad, d, mu, g, dq, (double *)xp,
+                                                  gauss ? (double *)xa : nullptr);
+    }
+    FK_LAUNCH_CHECK();
+    pp->Xp = xp;
+    pp->xa = (const float *)xa;  // fp64 biases (reinterpreted by the fp64 passes)
+    pp->Cp = cp;
+    pp->cb = (const float *)cb;
+    return FALKON_OK;
+  }
   const bool use_tc = tc_supported(ctx, kernel, d);
   if (use_tc) {
     pp->path = FALKON_PATH_TENSOR;
@@ -701,8 +892,13 @@ int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, cons
   return FALKON_OK;
 }
 
+static int f64_needs_f64() {
+  return fail(FALKON_EUNSUPPORTED, "FALKON_PATH_F64 products run on fp64 vectors only");
+}
+
 int pass_A(falkon_ctx *ctx, const Prepared &pp, const float *z, double *w64, float *w32) {
   if (pp.n <= 0) return FALKON_OK;
+  if (pp.path == FALKON_PATH_F64) return f64_needs_f64();
   if (pp.path == FALKON_PATH_TENSOR) return tc_pass(ctx, pp, true, z, w64, w32);
   return kvp_launch(ctx, pp.kernel, pp.d, pp.dq, (const float *)pp.Xp, pp.xa, pp.n,
                     (const float *)pp.Cp, pp.cb, z, pp.m, FALKON_T_PASS_A, w64, w32);
@@ -713,6 +909,7 @@ int pass_B(falkon_ctx *ctx, const Prepared &pp, const float *w, double *u) {
     FK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * pp.m, ctx->stream));
     return FALKON_OK;
   }
+  if (pp.path == FALKON_PATH_F64) return f64_needs_f64();
   if (pp.path == FALKON_PATH_TENSOR) return tc_pass(ctx, pp, false, w, u, nullptr);
   return kvp_launch(ctx, pp.kernel, pp.d, pp.dq, (const float *)pp.Cp, pp.cb, pp.m,
                     (const float *)pp.Xp, pp.xa, w, pp.n, FALKON_T_PASS_B, u, nullptr);
@@ -720,6 +917,9 @@ int pass_B(falkon_ctx *ctx, const Prepared &pp, const float *w, double *u) {
 
 int pass_A64(falkon_ctx *ctx, const Prepared &pp, const double *z, double *w64) {
   if (pp.n <= 0) return FALKON_OK;
+  if (pp.path == FALKON_PATH_F64)
+    return kvp64_launch(ctx, pp.kernel, pp.dq, (const double *)pp.Xp, (const double *)pp.xa, pp.n,
+                        (const double *)pp.Cp, (const double *)pp.cb, z, pp.m, FALKON_T_PASS_A, w64);
   if (pp.path == FALKON_PATH_TENSOR) return tc_pass64(ctx, pp, true, z, w64);
   return kvp_launch(ctx, pp.kernel, pp.d, pp.dq, (const float *)pp.Xp, pp.xa, pp.n,
                     (const float *)pp.Cp, pp.cb, z, pp.m, FALKON_T_PASS_A, w64, nullptr, true);
@@ -730,6 +930,9 @@ int pass_B64(falkon_ctx *ctx, const Prepared &pp, const double *w, double *u) {
     FK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * pp.m, ctx->stream));
     return FALKON_OK;
   }
+  if (pp.path == FALKON_PATH_F64)
+    return kvp64_launch(ctx, pp.kernel, pp.dq, (const double *)pp.Cp, (const double *)pp.cb, pp.m,
+                        (const double *)pp.Xp, (const double *)pp.xa, w, pp.n, FALKON_T_PASS_B, u);
   if (pp.path == FALKON_PATH_TENSOR) return tc_pass64(ctx, pp, false, w, u);
   return kvp_launch(ctx, pp.kernel, pp.d, pp.dq, (const float *)pp.Cp, pp.cb, pp.m,
                     (const float *)pp.Xp, pp.xa, w, pp.n, FALKON_T_PASS_B, u, nullptr, true);
@@ -823,12 +1026,14 @@ static int simt_multi(falkon_ctx *ctx, const Prepared &pp, bool passA, const flo
 int pass_A_multi(falkon_ctx *ctx, const Prepared &pp, const float *z, int kv, double *w64,
                  float *w32) {
   if (pp.n <= 0) return FALKON_OK;
+  if (pp.path == FALKON_PATH_F64) return f64_needs_f64();
   if (kv == 1) return pass_A(ctx, pp, z, w64, w32);
   if (pp.path == FALKON_PATH_TENSOR) return tc_pass(ctx, pp, true, z, w64, w32, kv);
   return simt_multi(ctx, pp, true, z, kv, w64, w32);
 }
 
 int pass_B_multi(falkon_ctx *ctx, const Prepared &pp, const float *w, int kv, double *u) {
+  if (pp.path == FALKON_PATH_F64) return f64_needs_f64();
   if (pp.n <= 0) {
     FK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * pp.m * kv, ctx->stream));
     return FALKON_OK;

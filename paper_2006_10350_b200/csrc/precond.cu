@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "precond.cuh"
 
 namespace falkon {
 
@@ -56,47 +57,7 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// ------------------------------------------------------------------ views
-// Logical matrix element (r, c) of a view.  tri: 0 = dense; 1 = lower (r > c from
-// storage, r == c from dvec, r < c is zero); 2 = upper (c > r from storage, diag from
-// dvec, c < r is zero).
-struct View {
-  double *base;
-  int64_t ld;
-  int trans;
-  int tri;
-  double *dvec;
-};
-
-__device__ __forceinline__ int64_t vidx(const View &v, int64_t r, int64_t c) {
-  return v.trans ? c * v.ld + r : r * v.ld + c;
-}
-__device__ __forceinline__ double vget(const View &v, int64_t r, int64_t c) {
-  if (v.tri == 1) {
-    if (r < c) return 0.0;
-    if (r == c) return v.dvec[r];
-  } else if (v.tri == 2) {
-    if (c < r) return 0.0;
-    if (r == c) return v.dvec[r];
-  }
-  return v.base[vidx(v, r, c)];
-}
-__device__ __forceinline__ void vset(const View &v, int64_t r, int64_t c, double x) {
-  if (v.tri == 1) {
-    if (r < c) return;
-    if (r == c) {
-      v.dvec[r] = x;
-      return;
-    }
-  } else if (v.tri == 2) {
-    if (c < r) return;
-    if (r == c) {
-      v.dvec[r] = x;
-      return;
-    }
-  }
-  v.base[vidx(v, r, c)] = x;
-}
+// views: precond.cuh
 
 // ------------------------------------------------------------------ Kmm (step b)
 // Logical lower triangle of S = Kmm + delta I written through view `S` (+ its diagonal).
@@ -253,19 +214,7 @@ __global__ void __launch_bounds__(512) potrf_diag_kernel(View S, int64_t k0, int
 }
 
 // ------------------------------------------------------------------ fp64 GEMM through views
-// C(i, j) = alpha * sum_{k in [kb, k1)} A(ra + i, k) * B(rb + j, k) + beta * C(rc + i, cc + j)
-// for 0 <= i < M, 0 <= j < N.  tri_tiles: only tiles with ti >= tj (square lower region).
-// k_from_row: kb = max(k0, ra + ti*GT) (LAUUM: sum over k >= row block).
-struct GemmArgs {
-  View A, B, C;
-  int64_t M, N;
-  int64_t ra, rb, rc, cc;
-  int64_t k0, k1;
-  int k_from_row;
-  int tri_tiles;
-  double alpha, beta;
-  const double *kscale;  // optional: B(j, k) is multiplied by kscale[k] (weighted LAUUM, Alg. 2)
-};
+// GemmArgs (precond.cuh): C = alpha A B^T + beta C through views.
 
 // Asynchronous (cp.async, LDGSTS) staging of a GT x GK chunk of a view into shared memory:
 // masked elements are zero-filled (src-size 0), diagonal elements read from the view's dvec.
@@ -797,6 +746,10 @@ static int gemm_launch(falkon_ctx *ctx, const GemmArgs &a) {
 
 static int gemm(falkon_ctx *ctx, const GemmArgs &a) {
   if (a.M <= 0 || a.N <= 0) return FALKON_OK;
+  {  // FALKON_OPT_OZAKI: int8 tensor-core emulation (ozaki.cu) where it applies
+    const int rc = oz_gemm(ctx, a);
+    if (rc != OZ_DECLINED) return rc;
+  }
   if (ctx->opt.gemm_warps == 5) {  // TMA-fed warp-specialised kernel where it applies
     int rc;
     if (gemm_launch_tma(ctx, a, &rc)) return rc;

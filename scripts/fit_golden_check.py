@@ -9,7 +9,9 @@ import synth
 from paper_2006_10350_b200 import binding
 
 pat = sys.argv[1] if len(sys.argv) > 1 else "*"
-variants = [("fp32", 0, 0), ("f64", 1, 0), ("fp32_simt", 0, 1)]
+# (name, fp64 contractions, SIMT path, exp on the FMA pipe (tensor path), Ozaki preconditioner)
+variants = [("fp32", 0, 0, 0, 0), ("f64", 1, 0, 0, 0), ("fp32_simt", 0, 1, 0, 0),
+            ("expoly", 0, 0, 1, 0), ("f64_expoly", 1, 0, 1, 0), ("ozaki", 0, 0, 0, 1)]
 if len(sys.argv) > 2:
     variants = [v for v in variants if v[0] in sys.argv[2].split(",")]
 ctx = binding.Context(0)
@@ -21,10 +23,12 @@ for f in sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "fits", pat + ".
     _, X, y, C = synth.make_problem(meta["config"], n=meta["n"], m=meta["m"])
     Xs = synth.gen_X(cfg.seed, 0, meta["n_test"], cfg.d, stream=synth.STREAM_XTEST)
     Xd, yd, Cd, Xsd = (torch.from_numpy(a).cuda() for a in (X, y, C, Xs))
-    for name, acc, simt in variants:
+    for name, acc, simt, expo, oz in variants:
         if simt and meta["kernel"] == 1:
             continue
         ctx.set_option(binding.OPT_ACCUM_F64, acc)
+        ctx.set_option(binding.OPT_EXP_OFFLOAD, expo)
+        ctx.set_option(binding.OPT_OZAKI, oz)
         ctx.set_option(binding.OPT_PATH, binding.PATH_SIMT if simt else binding.PATH_AUTO)
         alpha = torch.zeros(meta["m"], dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()

@@ -82,9 +82,9 @@ def test_binding_enum_values_match_the_header():
              "OPT_EXP_OFFLOAD": "FALKON_OPT_EXP_OFFLOAD", "OPT_POTRF_OUTER": "FALKON_OPT_POTRF_OUTER",
              "OPT_GEMM_WARPS": "FALKON_OPT_GEMM_WARPS", "OPT_SINGLE_EVAL": "FALKON_OPT_SINGLE_EVAL",
              "OPT_STRIP_BYTES": "FALKON_OPT_STRIP_BYTES", "OPT_TC_CLUSTER": "FALKON_OPT_TC_CLUSTER",
-             "OPT_LOOKAHEAD": "FALKON_OPT_LOOKAHEAD", "OPT_ACCUM_F64": "FALKON_OPT_ACCUM_F64", "OPT_DIST_PRECOND": "FALKON_OPT_DIST_PRECOND", "OPT_FIT_PRECISE": "FALKON_OPT_FIT_PRECISE", "OPT_SE_GEMV_SMS": "FALKON_OPT_SE_GEMV_SMS",
+             "OPT_LOOKAHEAD": "FALKON_OPT_LOOKAHEAD", "OPT_ACCUM_F64": "FALKON_OPT_ACCUM_F64", "OPT_DIST_PRECOND": "FALKON_OPT_DIST_PRECOND", "OPT_FIT_PRECISE": "FALKON_OPT_FIT_PRECISE", "OPT_SE_GEMV_SMS": "FALKON_OPT_SE_GEMV_SMS", "OPT_OZAKI": "FALKON_OPT_OZAKI",
              "PATH_AUTO": "FALKON_PATH_AUTO",
-             "PATH_SIMT": "FALKON_PATH_SIMT", "PATH_TENSOR": "FALKON_PATH_TENSOR",
+             "PATH_SIMT": "FALKON_PATH_SIMT", "PATH_TENSOR": "FALKON_PATH_TENSOR", "PATH_F64": "FALKON_PATH_F64",
              "GAUSSIAN": "FALKON_GAUSSIAN", "LAPLACIAN": "FALKON_LAPLACIAN"}
     for py, c in pairs.items():
         assert getattr(binding, py) == enums[c], (py, c)
