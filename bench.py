@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-fit", action="store_true", help="skip the full falkon_fit timing")
     ap.add_argument("--fit-iters", type=int, default=None)
-    ap.add_argument("--path", default="auto", choices=["auto", "simt", "tensor"])
+    ap.add_argument("--path", default="auto", choices=["auto", "simt", "tensor", "f64"])
     ap.add_argument("--n", type=int, default=None, help="override global n (debug)")
     ap.add_argument("--m", type=int, default=None, help="override m (debug)")
     ap.add_argument("--oracle-seconds", type=float, default=15.0)
@@ -271,6 +271,14 @@ def roofline(args, cfg, kt, ms_total, n_local, m, sms):
                 "peak_source": f"{peak_src} sm_max_mhz {f_hz/1e6:.0f} MHz x {sms} SM x 16 MUFU ex2"
                                " per clk (tensor cross term not binding at this d)",
                 **extra, **common}
+    if args.path == "f64":  # FALKON_PATH_F64: the FP64 pipe (64 DFMA lanes/clk/SM on B200)
+        peak = sms * 64 * f_hz / (d + 2)
+        ach = evals / (dom_ms * 1e-3)
+        return {"bound": "alu", "pipe": "fp64", "achieved": ach / 1e9, "peak": peak / 1e9,
+                "unit": "G kernel-evals/s", "frac": ach / peak,
+                "peak_source": f"sm_max_mhz {f_hz/1e6:.0f} MHz x {sms} SM x 64 DFMA lanes / "
+                               "(d + 2) per clk (d cross-term DFMA + bias + contraction; the "
+                               "fp64 exp2 counted as extra work)", **common}
     fp32 = sms * 128 * f_hz / (d + 2)
     mufu = sms * 16 * f_hz
     peak, pipe = min((fp32, "fp32"), (mufu, "mufu"))
@@ -296,6 +304,9 @@ def product_roofline(args, cfg, sms):
         pk = min(tc, mufu)
         return pk, (f"min(tensor {peaks['bf16_tflops']} TF/s / 3 / 2d = {tc:.3g}, MUFU "
                     f"{sms} SM x 16 x {f_hz/1e6:.0f} MHz = {mufu:.3g}) evals/s ({src} peaks)")
+    if args.path == "f64":
+        pk = sms * 64 * f_hz / (d + 2)
+        return pk, f"FP64 {sms} SM x 64 DFMA lanes x {f_hz/1e6:.0f} MHz / (d + 2) evals/s"
     fp32 = sms * 128 * f_hz / (d + 3)
     pk = min(fp32, mufu)
     return pk, (f"min(FP32 {sms} SM x 128 x {f_hz/1e6:.0f} MHz / (d+3) = {fp32:.3g}, MUFU "
@@ -401,7 +412,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     ctx = parallel.make_context(local, world, rank, stream=stream)
-    ctx.set_option(binding.OPT_PATH, {"auto": 0, "simt": 1, "tensor": 2}[args.path])
+    ctx.set_option(binding.OPT_PATH, {"auto": 0, "simt": 1, "tensor": 2, "f64": 3}[args.path])
     if args.exp_offload is not None:
         ctx.set_option(binding.OPT_EXP_OFFLOAD, args.exp_offload)
     if args.single_eval is not None:

@@ -48,6 +48,7 @@ constexpr int OZ_BN = OZ_BN_OVR;         // C tile columns; 8 level accumulators
 constexpr int OZ_BK = 32;          // int8 per K box = one MMA's K (32 B rows, SWIZZLE_32B)
 constexpr int OZ_KMAX = 1024;      // 8 * 1024 * 127^2 < 2^31: level sums exact in int32
 constexpr int OZ_STAGES = 4;
+constexpr int64_t OZ_MIN_LD = 512;  // preconditioners of m < 512 stay on DMMA (launch-bound)
 constexpr int OZ_ASL = OZ_BM * OZ_BK;                   // 4 KB per A slice box
 constexpr int OZ_BSL = OZ_BN * OZ_BK;                   // 2 KB per B slice box
 constexpr int OZ_STAGE = OZ_S * (OZ_ASL + OZ_BSL);      // 48 KB
@@ -446,8 +447,10 @@ int oz_gemm(falkon_ctx *ctx, const GemmArgs &a) {
     // the LAUUM  C(i, j) = alpha sum_{k >= i} T(i, k) [D(k)] T(j, k) + beta C  (T upper, C lower,
     // i >= j): C scaled by beta once, then k chunks of OZ_KMAX accumulate (beta = 1), chunk
     // [kc, kc + OZ_KMAX) only over the rows i < kc + OZ_KMAX it reaches (T(i, k) = 0 for k < i)
+    // the decision depends on the buffer (ld = m), never on a call's M / N: the distributed
+    // schedule's per-panel calls then take the same path as the single-GPU build's one call
     if (!(a.tri_tiles && a.ra == a.rb && a.rc == a.ra && a.cc == a.rb && a.N <= a.M &&
-          a.C.tri == 1 && a.M >= 2 * OZ_BM && a.N >= 2 * OZ_BN))
+          a.C.tri == 1 && a.C.ld >= OZ_MIN_LD))
       return OZ_DECLINED;
     {
       LaunchScope ls(ctx, FALKON_T_PRECOND);
@@ -455,23 +458,28 @@ int oz_gemm(falkon_ctx *ctx, const GemmArgs &a) {
           a.C, a.rc, a.cc, a.M, a.N, a.beta);
     }
     FK_LAUNCH_CHECK();
-    for (int64_t kc = std::max(a.k0, a.ra); kc < a.k1; kc += OZ_KMAX) {
+    // chunk boundaries at absolute multiples of OZ_KMAX: every element sees the same k chunks
+    // (hence the same slices, exponents and integer sums) whatever the row range of the call,
+    // so the distributed schedule's per-panel calls reproduce the single-GPU build bitwise
+    for (int64_t kc = std::max(a.k0, a.ra), ke; kc < a.k1; kc = ke) {
+      ke = std::min<int64_t>(a.k1, (kc / OZ_KMAX + 1) * OZ_KMAX);
       GemmArgs s = a;
       s.k_from_row = 0;
       s.k0 = kc;
-      s.k1 = std::min<int64_t>(kc + OZ_KMAX, a.k1);
+      s.k1 = ke;
       s.beta = 1.0;
-      s.M = std::min<int64_t>(a.M, kc + OZ_KMAX - a.ra);
-      s.N = std::min<int64_t>(a.N, kc + OZ_KMAX - a.rb);
+      s.M = std::min<int64_t>(a.M, ke - a.ra);
+      s.N = std::min<int64_t>(a.N, ke - a.rb);
       if (s.M <= 0 || s.N <= 0) continue;
       FK_TRY(oz_gemm_core(ctx, s));
     }
     return FALKON_OK;
   }
   const int64_t K = a.k1 - a.k0;
-  // small GEMMs (panel solves, the intra-panel updates with k = 128) stay on DMMA: the trailing
-  // updates (k = potrf_outer x 128 = 1024) carry almost all of the flops
-  if (a.kscale || K < 256 || K > OZ_KMAX || a.M < 2 * OZ_BM || a.N < 2 * OZ_BN) return OZ_DECLINED;
+  // the panel solves and the intra-panel updates (k = 128) stay on DMMA: the trailing updates
+  // (k = potrf_outer x 128 = 1024 by default) carry almost all of the flops.  As above the
+  // decision uses the k range and the buffer size only (schedule-independent results).
+  if (a.kscale || K < 256 || K > OZ_KMAX || a.C.ld < OZ_MIN_LD) return OZ_DECLINED;
   return oz_gemm_core(ctx, a);
 }
 
