@@ -578,6 +578,168 @@ __global__ void __launch_bounds__(KVP_THREADS)
   if (p_raw < np) out64[(int64_t)blockIdx.y * np + p_raw] = acc;
 }
 
+// fp64 path, d <= 64 (the fits that reading d4 routes here): register-blocked.  Both operands
+// in the tile-transposed fp64 layout [tile of 128 points][k][128]; a CTA keeps its P tile in
+// shared memory and streams Q tiles of 128 points (bulk copies, 2-stage ring); thread (tp, tq)
+// owns 8 P rows x 8 Q columns (pairs 2tp + 32i, 2tq + 32j: conflict-free LDS.128), so per
+// coordinate 8 LDS.128 feed 64 DFMA.  exp2 by range reduction and a degree-11 polynomial
+// (relative error < 1e-14).  Q columns past the split's range get z = 0 (the padding of z
+// is not guaranteed: pass B's z is pass A's output).
+// The per-row sums of the 16 tq threads are reduced in a fixed order (deterministic).
+constexpr int K64_T = 128;
+constexpr int K64_DMAX = 64;
+__device__ __forceinline__ double exp2_f64(double t) {  // t <= 0
+  t = fmax(t, -1070.0);
+  const double n = (t + 6755399441055744.0) - 6755399441055744.0;  // rint (|t| < 2^51)
+  const double y = (t - n) * 0.6931471805599453;                    // |y| <= 0.347
+  double p = 2.505210838544172e-08;                                 // 1/11!
+  p = fma(p, y, 2.755731922398589e-07);
+  p = fma(p, y, 2.7557319223985893e-06);
+  p = fma(p, y, 2.48015873015873e-05);
+  p = fma(p, y, 1.984126984126984e-04);
+  p = fma(p, y, 1.388888888888889e-03);
+  p = fma(p, y, 8.333333333333333e-03);
+  p = fma(p, y, 4.1666666666666664e-02);
+  p = fma(p, y, 0.16666666666666666);
+  p = fma(p, y, 0.5);
+  p = fma(p, y, 1.0);
+  p = fma(p, y, 1.0);
+  const int ni = (int)n;  // in [-1070, 0]
+  if (ni >= -1022) return p * __longlong_as_double((long long)(ni + 1023) << 52);
+  return p * __longlong_as_double((long long)(ni + 1023 + 64) << 52) * 5.421010862427522e-20;  // 2^-64
+}
+__global__ void pack_rows64_tt_kernel(const float *__restrict__ in, int64_t rows, int64_t rows_pad,
+                                      int64_t d, const double *__restrict__ mu, double g, int dq,
+                                      double *__restrict__ out, double *__restrict__ bias) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows_pad) return;
+  double *o = out + (r / K64_T) * dq * K64_T + (r % K64_T);
+  double ss = 0.0;
+  for (int k = 0; k < dq; ++k) {
+    const double v = (r < rows && k < d) ? ((double)in[r * d + k] - mu[k]) * g : 0.0;
+    o[(int64_t)k * K64_T] = v;
+    ss = fma(v, v, ss);
+  }
+  if (bias) bias[r] = -0.5 * ss;
+}
+__device__ __forceinline__ double2 lds_d2(const double *p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+template <int KER>
+__global__ void __launch_bounds__(256, 1)
+    kvp64t_kernel(const double *__restrict__ P, const double *__restrict__ pa, int64_t np,
+                  const double *__restrict__ Q, const double *__restrict__ qb,
+                  const double *__restrict__ z, int64_t nq, int64_t q_per_split, int dq,
+                  double *__restrict__ out64) {
+  extern __shared__ __align__(128) double sm64[];
+  const int TB = dq * K64_T;  // doubles per tile
+  // [3 mbarriers, padded to 128 B][P tile][2 Q tiles][2 x 128 biases][2 x 128 z]; the final
+  // [16][128] row reduction reuses the data region (the host sizes it for both)
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm64);  // P, Q stage 0, Q stage 1
+  double *sP = sm64 + 16, *sQ = sP + TB, *sB = sQ + 2 * TB, *sZ = sB + 2 * K64_T;
+  const int tid = threadIdx.x, tp = tid >> 4, tq = tid & 15;
+  const int64_t pt = blockIdx.x;  // P tile
+  const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
+  const int64_t qhi = min(nq, qlo + q_per_split);
+  const int ntiles = qhi > qlo ? (int)cdiv<int64_t>(qhi - qlo, K64_T) : 0;
+  const bool gauss = KER == FALKON_GAUSSIAN;
+  auto issue = [&](int t) {
+    const int64_t qt = (qlo + (int64_t)t * K64_T) / K64_T;
+    const int s = t & 1;
+    const uint32_t bt = (uint32_t)TB * 8, bv = K64_T * 8;
+    mbar_expect_tx(&bar[1 + s], bt + bv + (gauss ? bv : 0));
+    bulk_g2s(sQ + s * TB, Q + qt * TB, bt, &bar[1 + s]);
+    bulk_g2s(sZ + s * K64_T, z + qt * K64_T, bv, &bar[1 + s]);
+    if (gauss) bulk_g2s(sB + s * K64_T, qb + qt * K64_T, bv, &bar[1 + s]);
+  };
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_expect_tx(&bar[0], (uint32_t)TB * 8);
+    bulk_g2s(sP, P + pt * TB, (uint32_t)TB * 8, &bar[0]);
+    if (ntiles > 0) issue(0);
+    if (ntiles > 1) issue(1);
+  }
+  double pav[8], part[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = pt * K64_T + 2 * tp + 32 * (i >> 1) + (i & 1);
+    pav[i] = gauss ? pa[r] : 0.0;  // biases are padded to the tile
+    part[i] = 0.0;
+  }
+  mbar_wait(&bar[0], 0);
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t & 1;
+    mbar_wait(&bar[1 + s], (t >> 1) & 1);
+    const double *q = sQ + s * TB;
+    double acc[8][8];
+#pragma unroll
+    for (int j2 = 0; j2 < 4; ++j2) {
+      const double2 b2 = gauss ? lds_d2(sB + s * K64_T + 2 * tq + 32 * j2) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        acc[i][2 * j2] = pav[i] + b2.x;
+        acc[i][2 * j2 + 1] = pav[i] + b2.y;
+      }
+    }
+    for (int k = 0; k < dq; ++k) {
+      double pv[8], qv[8];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 a2 = lds_d2(sP + k * K64_T + 2 * tp + 32 * h);
+        const double2 c2 = lds_d2(q + k * K64_T + 2 * tq + 32 * h);
+        pv[2 * h] = a2.x, pv[2 * h + 1] = a2.y;
+        qv[2 * h] = c2.x, qv[2 * h + 1] = c2.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (gauss) {
+            acc[i][j] = fma(pv[i], qv[j], acc[i][j]);
+          } else {
+            const double df = pv[i] - qv[j];
+            acc[i][j] = fma(df, df, acc[i][j]);
+          }
+        }
+    }
+    const int64_t qc0 = qlo + (int64_t)t * K64_T;  // columns past nq contribute zero
+#pragma unroll
+    for (int j2 = 0; j2 < 4; ++j2) {
+      double2 z2 = lds_d2(sZ + s * K64_T + 2 * tq + 32 * j2);
+      const int64_t c = qc0 + 2 * tq + 32 * j2;
+      if (c >= qhi) z2.x = 0.0;
+      if (c + 1 >= qhi) z2.y = 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double k0 = gauss ? exp2_f64(fmin(acc[i][2 * j2], 0.0)) : exp2_f64(-sqrt(acc[i][2 * j2]));
+        const double k1 = gauss ? exp2_f64(fmin(acc[i][2 * j2 + 1], 0.0))
+                                : exp2_f64(-sqrt(acc[i][2 * j2 + 1]));
+        part[i] = fma(k0, z2.x, part[i]);
+        part[i] = fma(k1, z2.y, part[i]);
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && t + 2 < ntiles) issue(t + 2);
+  }
+  // fixed-order reduction over the 16 tq threads of each row (the Q stage buffers are free)
+  double *red = sP;  // [16][128]
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[tq * K64_T + 2 * tp + 32 * (i >> 1) + (i & 1)] = part[i];
+  __syncthreads();
+  if (tid < K64_T) {
+    double sum = 0.0;
+    for (int c = 0; c < 16; ++c) sum += red[c * K64_T + tid];
+    const int64_t r = pt * K64_T + tid;
+    if (r < np) out64[(int64_t)blockIdx.y * np + r] = sum;
+  }
+}
+
 // ------------------------------------------------------------------ reductions / conversions
 __global__ void reduce_splits_kernel(const double *__restrict__ part, int splits, int64_t np,
                                      double *__restrict__ out64, float *__restrict__ out32) {
@@ -749,17 +911,22 @@ static int kvp64_launch(falkon_ctx *ctx, int kernel, int dq, const double *P, co
                         int64_t np, const double *Q, const double *qb, const double *z,
                         int64_t nq, int cls, double *out64) {
   if (np <= 0) return FALKON_OK;
-  constexpr int TQ = KVP64_TQ;
-  const void *fn = kernel == FALKON_GAUSSIAN ? (const void *)kvp64_kernel<FALKON_GAUSSIAN>
-                                             : (const void *)kvp64_kernel<FALKON_LAPLACIAN>;
-  const size_t smem = (size_t)(2 * TQ * dq + 4 * TQ) * 8 + 16;
+  const bool tt = dq <= K64_DMAX;  // register-blocked kernel on the tile-transposed layout
+  const int TQ = tt ? K64_T : KVP64_TQ;
+  const int threads = tt ? 256 : KVP_THREADS;
+  const void *fn = tt ? (kernel == FALKON_GAUSSIAN ? (const void *)kvp64t_kernel<FALKON_GAUSSIAN>
+                                                   : (const void *)kvp64t_kernel<FALKON_LAPLACIAN>)
+                      : (kernel == FALKON_GAUSSIAN ? (const void *)kvp64_kernel<FALKON_GAUSSIAN>
+                                                   : (const void *)kvp64_kernel<FALKON_LAPLACIAN>);
+  const size_t smem = tt ? (size_t)(16 + std::max(3 * dq * K64_T + 4 * K64_T, 16 * K64_T)) * 8
+                         : (size_t)(2 * TQ * dq + 4 * TQ) * 8 + 16;
   if (smem > 227 * 1024) return fail(FALKON_EUNSUPPORTED, "fp64 path: d too large");
   FK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t gx = cdiv<int64_t>(np, KVP_THREADS);
-  const int64_t capacity = (int64_t)ctx->sm_count * occupancy(fn, KVP_THREADS, smem);
+  const int64_t gx = cdiv<int64_t>(np, tt ? K64_T : KVP_THREADS);
+  const int64_t capacity = (int64_t)ctx->sm_count * occupancy(fn, threads, smem);
   int64_t splits = 1;
-  if (gx < capacity) {
-    splits = std::max<int64_t>(1, capacity / gx);
+  if (gx < 4 * capacity) {  // several waves: fewer tail effects
+    splits = std::max<int64_t>(1, 4 * capacity / gx);
     splits = std::min<int64_t>(splits, std::max<int64_t>(1, nq / (4 * TQ)));
     splits = std::min<int64_t>(splits, 65535);
   }
@@ -776,7 +943,7 @@ static int kvp64_launch(falkon_ctx *ctx, int kernel, int dq, const double *P, co
     LaunchScope ls(ctx, cls);
     typedef void (*f64_fn)(const double *, const double *, int64_t, const double *, const double *,
                            const double *, int64_t, int64_t, int, double *);
-    ((f64_fn)fn)<<<dim3((unsigned)gx, (unsigned)splits), KVP_THREADS, smem, ctx->stream>>>(
+    ((f64_fn)fn)<<<dim3((unsigned)gx, (unsigned)splits), threads, smem, ctx->stream>>>(
         P, pa, np, Q, qb, z, nq, qps, dq, part);
   }
   FK_LAUNCH_CHECK();
@@ -811,7 +978,13 @@ int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, cons
     FK_TRY(ws_get(ctx, WS_CP, sizeof(double) * m_pad * dq, &cp));
     FK_TRY(ws_get(ctx, WS_CB, sizeof(double) * m_pad, &cb));
     const bool gauss = kernel == FALKON_GAUSSIAN;
-    {
+    if (dq <= K64_DMAX) {  // tile-transposed layout of the register-blocked kernel
+      LaunchScope ls(ctx, FALKON_T_PREP);
+      pack_rows64_tt_kernel<<<(unsigned)cdiv<int64_t>(m_pad, 256), 256, 0, ctx->stream>>>(
+          C, m, m_pad, d, mu, g, dq, (double *)cp, gauss ? (double *)cb : nullptr);
+      pack_rows64_tt_kernel<<<(unsigned)cdiv<int64_t>(n_pad, 256), 256, 0, ctx->stream>>>(
+          X, n, n_pad, d, mu, g, dq, (double *)xp, gauss ? (double *)xa : nullptr);
+    } else {
       LaunchScope ls(ctx, FALKON_T_PREP);
       pack_rows64_kernel<<<(unsigned)std::min<int64_t>(cdiv<int64_t>(m_pad, 8), 65535), 256, 0,
                            ctx->stream>>>(C, m, m_pad, d, mu, g, dq, (double *)cp,
