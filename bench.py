@@ -183,7 +183,7 @@ def oracle_rate(cfg, n_global, m, seconds: float, rank_workers: int):
 def kt_path_tensor(args, d):
     """Mirror of libfalkon's path choice (tc_supported): tensor cores for the Gaussian kernel
     when d > 4 (measured crossover, profiles/r2_crossover.jsonl), unless --path forces one."""
-    if args.path == "simt":
+    if args.path in ("simt", "f64"):
         return False
     return args.path == "tensor" or d > 4
 

@@ -1415,7 +1415,9 @@ static int tc_launch(falkon_ctx *ctx, const Prepared &pp, bool passA, const floa
   {
     int64_t l2q = (int64_t)40 << 20;
     if (const char *e = getenv("FALKON_TC_L2Q_MB")) l2q = (int64_t)atoi(e) << 20;
-    if (l2q > 0 && gx > slots) {
+    // resident-P kernels only: the streaming kernel (d > 190) re-reads its P boxes per Q tile,
+    // and more Q splits cost it more than the L2 hits save (TIMIT 329 -> 338-346 ms, A/B x2)
+    if (l2q > 0 && gx > slots && !stream) {
       const int64_t need = cdiv<int64_t>(nq * (int64_t)4 * d16, l2q);
       if (need > best_s && qt / need >= 4) best_s = need;
     }
