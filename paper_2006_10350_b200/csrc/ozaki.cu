@@ -132,6 +132,14 @@ __global__ void __launch_bounds__(256) oz_pack_kernel(View V, int64_t r0, int64_
 }
 
 // ------------------------------------------------------------------ int8 tcgen05 GEMM
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1,
+                                            int c2, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                           uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -246,11 +254,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         if (elect_one()) {
           uint8_t *st = sm + stage * OZ_STAGE;
           mbar_expect_tx(&full[stage], OZ_STAGE);
-          for (int p = 0; p < OZ_S; ++p)
-            tma_load_2d(st + p * OZ_ASL, &ta, kb * OZ_BK, p * a.rpa + ra, &full[stage]);
-          for (int q = 0; q < OZ_S; ++q)
-            tma_load_2d(st + OZ_S * OZ_ASL + q * OZ_BSL, &tb, kb * OZ_BK, q * a.rpb + rb,
-                        &full[stage]);
+          // one 3-D box (k, rows, slice) per operand: all OZ_S slices of the tile's rows
+          tma_load_3d(st, &ta, kb * OZ_BK, ra, 0, &full[stage]);
+          tma_load_3d(st + OZ_S * OZ_ASL, &tb, kb * OZ_BK, rb, 0, &full[stage]);
         }
         __syncwarp();
         if (++stage == OZ_STAGES) {
@@ -362,15 +368,15 @@ static PFN_encodeTiled_oz oz_encode() {
   }();
   return fn;
 }
-static int oz_map(CUtensorMap *map, const int8_t *slab, int64_t rows_total, int64_t kpad,
-                  int box_rows) {
+// 3-D map of a slab [slice][rows][kpad] (int8): boxes of OZ_BK x box_rows x all slices
+static int oz_map(CUtensorMap *map, const int8_t *slab, int64_t rows, int64_t kpad, int box_rows) {
   PFN_encodeTiled_oz enc = oz_encode();
   if (!enc) return OZ_DECLINED;
-  cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)rows_total};
-  cuuint64_t strides[1] = {(cuuint64_t)kpad};
-  cuuint32_t box[2] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void *)slab, dims, strides, box, es,
+  cuuint64_t dims[3] = {(cuuint64_t)kpad, (cuuint64_t)rows, (cuuint64_t)OZ_S};
+  cuuint64_t strides[2] = {(cuuint64_t)kpad, (cuuint64_t)(rows * kpad)};
+  cuuint32_t box[3] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows, (cuuint32_t)OZ_S};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void *)slab, dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FALKON_ECUDA, "cuTensorMapEncodeTiled (ozaki) failed");
@@ -418,8 +424,8 @@ static int oz_gemm_core(falkon_ctx *ctx, const GemmArgs &a) {
   FK_TRY(oz_pack(ctx, a.A, a.ra, a.M, a.k0, K, kpad, rpa, sa, ea, nullptr));
   if (!share) FK_TRY(oz_pack(ctx, a.B, a.rb, a.N, a.k0, K, kpad, rpb, sb, eb, a.kscale));
   CUtensorMap ta, tb;
-  FK_TRY(oz_map(&ta, sa, OZ_S * rpa, kpad, OZ_BM));
-  FK_TRY(oz_map(&tb, sb, OZ_S * rpb, kpad, OZ_BN));
+  FK_TRY(oz_map(&ta, sa, rpa, kpad, OZ_BM));
+  FK_TRY(oz_map(&tb, sb, rpb, kpad, OZ_BN));
   OzArgs oa;
   oa.g = a;
   oa.ea = ea;
