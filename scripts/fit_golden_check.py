@@ -9,9 +9,10 @@ import synth
 from paper_2006_10350_b200 import binding
 
 pat = sys.argv[1] if len(sys.argv) > 1 else "*"
-# (name, fp64 contractions, SIMT path, exp on the FMA pipe (tensor path), Ozaki preconditioner)
-variants = [("fp32", 0, 0, 0, 0), ("f64", 1, 0, 0, 0), ("fp32_simt", 0, 1, 0, 0),
-            ("expoly", 0, 0, 1, 0), ("f64_expoly", 1, 0, 1, 0), ("ozaki", 0, 0, 0, 1)]
+# (name, fp64 contractions, path (0 auto, 1 SIMT, 3 fp64), exp on the FMA pipe, Ozaki, FIT_PRECISE)
+variants = [("default", 0, 0, 0, 1, 1), ("fp32_noprecise", 0, 0, 0, 1, 0),
+            ("f64contr_noprecise", 1, 0, 0, 1, 0), ("simt_fp32", 0, 1, 0, 1, 0),
+            ("f64path", 0, 3, 0, 1, 1), ("dmma_precond", 0, 0, 0, 0, 1)]
 if len(sys.argv) > 2:
     variants = [v for v in variants if v[0] in sys.argv[2].split(",")]
 ctx = binding.Context(0)
@@ -23,13 +24,12 @@ for f in sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "fits", pat + ".
     _, X, y, C = synth.make_problem(meta["config"], n=meta["n"], m=meta["m"])
     Xs = synth.gen_X(cfg.seed, 0, meta["n_test"], cfg.d, stream=synth.STREAM_XTEST)
     Xd, yd, Cd, Xsd = (torch.from_numpy(a).cuda() for a in (X, y, C, Xs))
-    for name, acc, simt, expo, oz in variants:
-        if simt and meta["kernel"] == 1:
-            continue
+    for name, acc, path, expo, oz, precise in variants:
         ctx.set_option(binding.OPT_ACCUM_F64, acc)
         ctx.set_option(binding.OPT_EXP_OFFLOAD, expo)
         ctx.set_option(binding.OPT_OZAKI, oz)
-        ctx.set_option(binding.OPT_PATH, binding.PATH_SIMT if simt else binding.PATH_AUTO)
+        ctx.set_option(binding.OPT_FIT_PRECISE, precise)
+        ctx.set_option(binding.OPT_PATH, path)
         alpha = torch.zeros(meta["m"], dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()
         t0 = time.time()
@@ -40,6 +40,7 @@ for f in sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "fits", pat + ".
         fp = torch.zeros(meta["n_test"], dtype=torch.float64, device="cuda")
         ctx.predict(Xsd, Cd, alpha, meta["kernel"], meta["sigma"], fp)
         print(json.dumps({"golden": os.path.basename(f), "variant": name, "n": meta["n"],
+                          "product_path": info.get("product_path"),
                           "m": meta["m"], "d": cfg.d, "alpha_rel_l2": rel(alpha.cpu().numpy(), z["alpha"]),
                           "pred_rel_l2": rel(fp.cpu().numpy(), z["pred"]), "gpu_fit_s": t,
                           "t_precond_s": info["t_precond_s"], "t_cg_s": info["t_cg_s"],
