@@ -464,120 +464,8 @@ __global__ void __launch_bounds__(KVP_THREADS)
 // ------------------------------------------------------------------ fp64 path (FALKON_PATH_F64)
 // For fits whose alpha must match an fp64 reference where fp32 kernel values cannot (small d,
 // large m: the CG iterate amplifies the ~1e-7 relative error of fp32 k; reading d4):
-// coordinates (x - mu) g computed in fp64 from the fp32 inputs (exact upcast), the exponent
-// and the exp2 (CUDA's exp2(double), ~1 ulp) in fp64, fp64 contractions.  Same primitive and
-// tiling as kvp_generic_kernel (one P point per thread, TQ64 Q points per shared-memory tile,
-// bulk-copy ring); the FP64 pipe (~60 DFMA/clk/SM on B200) binds.
-constexpr int KVP64_TQ = 16;
-__global__ void pack_rows64_kernel(const float *__restrict__ in, int64_t rows, int64_t rows_pad,
-                                   int64_t d, const double *__restrict__ mu, double g, int dq,
-                                   double *__restrict__ out, double *__restrict__ bias) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wpb = blockDim.x >> 5;
-  for (int64_t r = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); r < rows_pad;
-       r += (int64_t)gridDim.x * wpb) {
-    double ss = 0.0;
-    for (int k = lane; k < dq; k += 32) {
-      const double v = (r < rows && k < d) ? ((double)in[r * d + k] - mu[k]) * g : 0.0;
-      out[r * dq + k] = v;
-      ss = fma(v, v, ss);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if (bias && lane == 0) bias[r] = -0.5 * ss;
-  }
-}
-
-template <int KER>
-__global__ void __launch_bounds__(KVP_THREADS)
-    kvp64_kernel(const double *__restrict__ P, const double *__restrict__ pa, int64_t np,
-                 const double *__restrict__ Q, const double *__restrict__ qb,
-                 const double *__restrict__ z, int64_t nq, int64_t q_per_split, int dq,
-                 double *__restrict__ out64) {
-  constexpr int TQ = KVP64_TQ;
-  extern __shared__ __align__(128) double smem_d[];
-  const int QF = TQ * dq;
-  double *const SB = smem_d + 2 * QF;
-  double *const SZ = SB + 2 * TQ;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(SZ + 2 * TQ);
-  const int tid = threadIdx.x;
-  const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
-  const int64_t qhi = min(nq, qlo + q_per_split);
-  const int ntiles = qhi > qlo ? (int)cdiv<int64_t>(qhi - qlo, TQ) : 0;
-  auto issue = [&](int t) {  // Q rows, biases and z are zero-padded to a multiple of 128
-    const int64_t q0 = qlo + (int64_t)t * TQ;
-    const int cnt2 = ((int)lmin(TQ, qhi - q0) + 1) & ~1;  // 16-byte multiples
-    const int s = t & 1;
-    const uint32_t bq = (uint32_t)cnt2 * dq * 8, bs = (uint32_t)cnt2 * 8;
-    mbar_expect_tx(&bar[s], bq + (KER == FALKON_GAUSSIAN ? bs : 0) + bs);
-    bulk_g2s(smem_d + s * QF, Q + q0 * dq, bq, &bar[s]);
-    if (KER == FALKON_GAUSSIAN) bulk_g2s(SB + s * TQ, qb + q0, bs, &bar[s]);
-    bulk_g2s(SZ + s * TQ, z + q0, bs, &bar[s]);
-  };
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    if (ntiles > 0) issue(0);
-    if (ntiles > 1) issue(1);
-  }
-  const int64_t p_raw = (int64_t)blockIdx.x * KVP_THREADS + tid;
-  const int64_t p = min(p_raw, np - 1);
-  const double *prow = P + p * dq;
-  const double pav = (KER == FALKON_GAUSSIAN) ? pa[p] : 0.0;
-  double acc = 0.0;
-  for (int t = 0; t < ntiles; ++t) {
-    const int s = t & 1;
-    mbar_wait(&bar[s], (t >> 1) & 1);
-    const int cnt = (int)lmin(TQ, qhi - (qlo + (int64_t)t * TQ));
-    const double *sqs = smem_d + s * QF;
-    double e[TQ];
-#pragma unroll
-    for (int j = 0; j < TQ; ++j) e[j] = (KER == FALKON_GAUSSIAN) ? pav + SB[s * TQ + j] : 0.0;
-    for (int k0 = 0; k0 < dq; k0 += 16) {
-      double pch[16];
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) {
-        double2 v2 = make_double2(0.0, 0.0);
-        if (k0 + 2 * k2 < dq) v2 = __ldg(reinterpret_cast<const double2 *>(prow + k0) + k2);
-        pch[2 * k2] = v2.x;
-        pch[2 * k2 + 1] = v2.y;
-      }
-#pragma unroll
-      for (int j = 0; j < TQ; ++j) {
-        const double2 *qrow = reinterpret_cast<const double2 *>(sqs + j * dq + k0);
-#pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) {
-          if (k0 + 2 * k2 < dq) {
-            const double2 q2 = qrow[k2];
-            if (KER == FALKON_GAUSSIAN) {
-              e[j] = fma(pch[2 * k2], q2.x, e[j]);
-              e[j] = fma(pch[2 * k2 + 1], q2.y, e[j]);
-            } else {
-              double df = pch[2 * k2] - q2.x;
-              e[j] = fma(df, df, e[j]);
-              df = pch[2 * k2 + 1] - q2.y;
-              e[j] = fma(df, df, e[j]);
-            }
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < TQ; ++j)
-      if (j < cnt) {
-        const double kv = (KER == FALKON_GAUSSIAN) ? exp2(fmin(e[j], 0.0)) : exp2(-sqrt(e[j]));
-        acc = fma(kv, SZ[s * TQ + j], acc);
-      }
-    __syncthreads();
-    if (tid == 0 && t + 2 < ntiles) issue(t + 2);
-  }
-  if (p_raw < np) out64[(int64_t)blockIdx.y * np + p_raw] = acc;
-}
-
+// coordinates (x - mu) g computed in fp64 from the fp32 inputs (exact upcast), the exponent,
+// the exp2 and the contractions in fp64.  The FP64 pipe (~64 DFMA/clk/SM on B200) binds.
 // fp64 path, d <= 64 (the fits that reading d4 routes here): register-blocked.  Both operands
 // in the tile-transposed fp64 layout [tile of 128 points][k][128]; a CTA keeps its P tile in
 // shared memory and streams Q tiles of 128 points (bulk copies, 2-stage ring); thread (tp, tq)
@@ -729,6 +617,129 @@ __global__ void __launch_bounds__(256, 1)
   }
   // fixed-order reduction over the 16 tq threads of each row (the Q stage buffers are free)
   double *red = sP;  // [16][128]
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[tq * K64_T + 2 * tp + 32 * (i >> 1) + (i & 1)] = part[i];
+  __syncthreads();
+  if (tid < K64_T) {
+    double sum = 0.0;
+    for (int c = 0; c < 16; ++c) sum += red[c * K64_T + tid];
+    const int64_t r = pt * K64_T + tid;
+    if (r < np) out64[(int64_t)blockIdx.y * np + r] = sum;
+  }
+}
+
+// fp64 path, d > 64: the same 8 x 8 register blocking with the coordinates streamed in chunks
+// of K64_KC (P and Q chunk of a Q tile per stage, 2-stage bulk-copy ring over the flattened
+// (Q tile, chunk) sequence); the operands use the tile-transposed layout with dq a multiple
+// of K64_KC.
+constexpr int K64_KC = 32;
+template <int KER>
+__global__ void __launch_bounds__(256, 1)
+    kvp64c_kernel(const double *__restrict__ P, const double *__restrict__ pa, int64_t np,
+                  const double *__restrict__ Q, const double *__restrict__ qb,
+                  const double *__restrict__ z, int64_t nq, int64_t q_per_split, int dq,
+                  double *__restrict__ out64) {
+  extern __shared__ __align__(128) double sm64c[];
+  constexpr int CB = K64_KC * K64_T;  // doubles per chunk of one tile
+  const int TB = dq * K64_T, nkc = dq / K64_KC;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm64c);  // stage 0, stage 1
+  double *sS = sm64c + 16;                              // 2 stages x (P chunk, Q chunk)
+  double *sB = sS + 4 * CB, *sZ = sB + 2 * K64_T;       // per Q-tile parity
+  const int tid = threadIdx.x, tp = tid >> 4, tq = tid & 15;
+  const int64_t pt = blockIdx.x;
+  const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
+  const int64_t qhi = min(nq, qlo + q_per_split);
+  const int ntiles = qhi > qlo ? (int)cdiv<int64_t>(qhi - qlo, K64_T) : 0;
+  const int nitems = ntiles * nkc;
+  const bool gauss = KER == FALKON_GAUSSIAN;
+  auto issue = [&](int it) {
+    const int t = it / nkc, c = it % nkc, s = it & 1;
+    const int64_t qt = (qlo + (int64_t)t * K64_T) / K64_T;
+    const uint32_t bc = (uint32_t)CB * 8, bv = K64_T * 8;
+    mbar_expect_tx(&bar[s], 2 * bc + (c == 0 ? bv + (gauss ? bv : 0) : 0));
+    bulk_g2s(sS + (2 * s) * CB, P + pt * TB + (int64_t)c * CB, bc, &bar[s]);
+    bulk_g2s(sS + (2 * s + 1) * CB, Q + qt * TB + (int64_t)c * CB, bc, &bar[s]);
+    if (c == 0) {
+      bulk_g2s(sZ + (t & 1) * K64_T, z + qt * K64_T, bv, &bar[s]);
+      if (gauss) bulk_g2s(sB + (t & 1) * K64_T, qb + qt * K64_T, bv, &bar[s]);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (nitems > 0) issue(0);
+    if (nitems > 1) issue(1);
+  }
+  double pav[8], part[8], acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = pt * K64_T + 2 * tp + 32 * (i >> 1) + (i & 1);
+    pav[i] = gauss ? pa[r] : 0.0;
+    part[i] = 0.0;
+  }
+  for (int it = 0; it < nitems; ++it) {
+    const int t = it / nkc, c = it % nkc, s = it & 1;
+    mbar_wait(&bar[s], (it >> 1) & 1);
+    if (c == 0) {
+#pragma unroll
+      for (int j2 = 0; j2 < 4; ++j2) {
+        const double2 b2 =
+            gauss ? lds_d2(sB + (t & 1) * K64_T + 2 * tq + 32 * j2) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc[i][2 * j2] = pav[i] + b2.x;
+          acc[i][2 * j2 + 1] = pav[i] + b2.y;
+        }
+      }
+    }
+    const double *ps = sS + (2 * s) * CB, *qs = sS + (2 * s + 1) * CB;
+    for (int k = 0; k < K64_KC; ++k) {
+      double pv[8], qv[8];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 a2 = lds_d2(ps + k * K64_T + 2 * tp + 32 * h);
+        const double2 c2 = lds_d2(qs + k * K64_T + 2 * tq + 32 * h);
+        pv[2 * h] = a2.x, pv[2 * h + 1] = a2.y;
+        qv[2 * h] = c2.x, qv[2 * h + 1] = c2.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (gauss) {
+            acc[i][j] = fma(pv[i], qv[j], acc[i][j]);
+          } else {
+            const double df = pv[i] - qv[j];
+            acc[i][j] = fma(df, df, acc[i][j]);
+          }
+        }
+    }
+    if (c == nkc - 1) {  // tile done: exp2 and contraction (columns past the range: z = 0)
+      const int64_t qc0 = qlo + (int64_t)t * K64_T;
+#pragma unroll
+      for (int j2 = 0; j2 < 4; ++j2) {
+        double2 z2 = lds_d2(sZ + (t & 1) * K64_T + 2 * tq + 32 * j2);
+        const int64_t col = qc0 + 2 * tq + 32 * j2;
+        if (col >= qhi) z2.x = 0.0;
+        if (col + 1 >= qhi) z2.y = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double k0 = gauss ? exp2_f64(fmin(acc[i][2 * j2], 0.0)) : exp2_f64(-sqrt(acc[i][2 * j2]));
+          const double k1 = gauss ? exp2_f64(fmin(acc[i][2 * j2 + 1], 0.0))
+                                  : exp2_f64(-sqrt(acc[i][2 * j2 + 1]));
+          part[i] = fma(k0, z2.x, part[i]);
+          part[i] = fma(k1, z2.y, part[i]);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && it + 2 < nitems) issue(it + 2);
+  }
+  double *red = sS;  // [16][128] fixed-order row reduction
 #pragma unroll
   for (int i = 0; i < 8; ++i) red[tq * K64_T + 2 * tp + 32 * (i >> 1) + (i & 1)] = part[i];
   __syncthreads();
@@ -911,18 +922,22 @@ static int kvp64_launch(falkon_ctx *ctx, int kernel, int dq, const double *P, co
                         int64_t np, const double *Q, const double *qb, const double *z,
                         int64_t nq, int cls, double *out64) {
   if (np <= 0) return FALKON_OK;
-  const bool tt = dq <= K64_DMAX;  // register-blocked kernel on the tile-transposed layout
-  const int TQ = tt ? K64_T : KVP64_TQ;
-  const int threads = tt ? 256 : KVP_THREADS;
-  const void *fn = tt ? (kernel == FALKON_GAUSSIAN ? (const void *)kvp64t_kernel<FALKON_GAUSSIAN>
-                                                   : (const void *)kvp64t_kernel<FALKON_LAPLACIAN>)
-                      : (kernel == FALKON_GAUSSIAN ? (const void *)kvp64_kernel<FALKON_GAUSSIAN>
-                                                   : (const void *)kvp64_kernel<FALKON_LAPLACIAN>);
-  const size_t smem = tt ? (size_t)(16 + std::max(3 * dq * K64_T + 4 * K64_T, 16 * K64_T)) * 8
-                         : (size_t)(2 * TQ * dq + 4 * TQ) * 8 + 16;
+  // register-blocked kernels on the tile-transposed layout: P resident (dq <= 64) or streamed
+  // in chunks of K64_KC coordinates (dq a multiple of K64_KC, see prepare_operands)
+  const bool resident = dq <= K64_DMAX;
+  const int TQ = K64_T;
+  const int threads = 256;
+  const void *fn = resident
+      ? (kernel == FALKON_GAUSSIAN ? (const void *)kvp64t_kernel<FALKON_GAUSSIAN>
+                                   : (const void *)kvp64t_kernel<FALKON_LAPLACIAN>)
+      : (kernel == FALKON_GAUSSIAN ? (const void *)kvp64c_kernel<FALKON_GAUSSIAN>
+                                   : (const void *)kvp64c_kernel<FALKON_LAPLACIAN>);
+  const size_t smem = resident
+      ? (size_t)(16 + std::max(3 * dq * K64_T + 4 * K64_T, 16 * K64_T)) * 8
+      : (size_t)(16 + 4 * K64_KC * K64_T + 4 * K64_T) * 8;
   if (smem > 227 * 1024) return fail(FALKON_EUNSUPPORTED, "fp64 path: d too large");
   FK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t gx = cdiv<int64_t>(np, tt ? K64_T : KVP_THREADS);
+  const int64_t gx = cdiv<int64_t>(np, K64_T);
   const int64_t capacity = (int64_t)ctx->sm_count * occupancy(fn, threads, smem);
   int64_t splits = 1;
   if (gx < 4 * capacity) {  // several waves: fewer tail effects
@@ -965,9 +980,9 @@ int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, cons
   pp->kernel = kernel;
   double *mu;
   FK_TRY(center_mean(ctx, C, m, d, &mu));
-  if (ctx->opt.path == FALKON_PATH_F64) {  // fp64 coordinates and biases, row-major [rows][dq]
+  if (ctx->opt.path == FALKON_PATH_F64) {  // fp64 coordinates and biases (tile-transposed)
     pp->path = FALKON_PATH_F64;
-    const int dq = (int)round_up<int64_t>(d, 2);
+    const int dq = (int)round_up<int64_t>(d, d <= K64_DMAX ? 2 : K64_KC);
     pp->dq = dq;
     const double g = kernel == FALKON_GAUSSIAN ? std::sqrt(LOG2E) / sigma : LOG2E / sigma;
     const int64_t n_pad = round_up<int64_t>(std::max<int64_t>(n, 1), 128);
@@ -978,20 +993,12 @@ int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, cons
     FK_TRY(ws_get(ctx, WS_CP, sizeof(double) * m_pad * dq, &cp));
     FK_TRY(ws_get(ctx, WS_CB, sizeof(double) * m_pad, &cb));
     const bool gauss = kernel == FALKON_GAUSSIAN;
-    if (dq <= K64_DMAX) {  // tile-transposed layout of the register-blocked kernel
+    {  // tile-transposed layout [tile of 128][dq][128] of the register-blocked kernels
       LaunchScope ls(ctx, FALKON_T_PREP);
       pack_rows64_tt_kernel<<<(unsigned)cdiv<int64_t>(m_pad, 256), 256, 0, ctx->stream>>>(
           C, m, m_pad, d, mu, g, dq, (double *)cp, gauss ? (double *)cb : nullptr);
       pack_rows64_tt_kernel<<<(unsigned)cdiv<int64_t>(n_pad, 256), 256, 0, ctx->stream>>>(
           X, n, n_pad, d, mu, g, dq, (double *)xp, gauss ? (double *)xa : nullptr);
-    } else {
-      LaunchScope ls(ctx, FALKON_T_PREP);
-      pack_rows64_kernel<<<(unsigned)std::min<int64_t>(cdiv<int64_t>(m_pad, 8), 65535), 256, 0,
-                           ctx->stream>>>(C, m, m_pad, d, mu, g, dq, (double *)cp,
-                                          gauss ? (double *)cb : nullptr);
-      pack_rows64_kernel<<<(unsigned)std::min<int64_t>(cdiv<int64_t>(n_pad, 8), (int64_t)ctx->sm_count * 64),
-                           256, 0, ctx->stream>>>(X, n, n_pad, d, mu, g, dq, (double *)xp,
-                                                  gauss ? (double *)xa : nullptr);
     }
     FK_LAUNCH_CHECK();
     pp->Xp = xp;
