@@ -272,13 +272,15 @@ def roofline(args, cfg, kt, ms_total, n_local, m, sms):
                                " per clk (tensor cross term not binding at this d)",
                 **extra, **common}
     if args.path == "f64":  # FALKON_PATH_F64: the FP64 pipe (64 DFMA lanes/clk/SM on B200)
-        peak = sms * 64 * f_hz / (d + 2)
+        # per entry d cross-term FMAs (DMMA or DFMA: the same fp64 rate on B200) + the fp64 exp2
+        # (range reduction + degree-11 polynomial + scaling: 17 operations) + bias + contraction
+        peak = sms * 64 * f_hz / (d + 19)
         ach = evals / (dom_ms * 1e-3)
         return {"bound": "alu", "pipe": "fp64", "achieved": ach / 1e9, "peak": peak / 1e9,
                 "unit": "G kernel-evals/s", "frac": ach / peak,
-                "peak_source": f"sm_max_mhz {f_hz/1e6:.0f} MHz x {sms} SM x 64 DFMA lanes / "
-                               "(d + 2) per clk (d cross-term DFMA + bias + contraction; the "
-                               "fp64 exp2 counted as extra work)", **common}
+                "peak_source": f"sm_max_mhz {f_hz/1e6:.0f} MHz x {sms} SM x 64 fp64 lanes / "
+                               "(d + 19) per clk (d cross-term FMAs, 17-op fp64 exp2, bias, "
+                               "contraction)", **common}
     fp32 = sms * 128 * f_hz / (d + 2)
     mufu = sms * 16 * f_hz
     peak, pipe = min((fp32, "fp32"), (mufu, "mufu"))
@@ -305,8 +307,8 @@ def product_roofline(args, cfg, sms):
         return pk, (f"min(tensor {peaks['bf16_tflops']} TF/s / 3 / 2d = {tc:.3g}, MUFU "
                     f"{sms} SM x 16 x {f_hz/1e6:.0f} MHz = {mufu:.3g}) evals/s ({src} peaks)")
     if args.path == "f64":
-        pk = sms * 64 * f_hz / (d + 2)
-        return pk, f"FP64 {sms} SM x 64 DFMA lanes x {f_hz/1e6:.0f} MHz / (d + 2) evals/s"
+        pk = sms * 64 * f_hz / (d + 19)
+        return pk, f"FP64 {sms} SM x 64 lanes x {f_hz/1e6:.0f} MHz / (d + 19) evals/s"
     fp32 = sms * 128 * f_hz / (d + 3)
     pk = min(fp32, mufu)
     return pk, (f"min(FP32 {sms} SM x 128 x {f_hz/1e6:.0f} MHz / (d+3) = {fp32:.3g}, MUFU "

@@ -470,12 +470,15 @@ __global__ void __launch_bounds__(KVP_THREADS)
 // in the tile-transposed fp64 layout [tile of 128 points][k][128]; a CTA keeps its P tile in
 // shared memory and streams Q tiles of 128 points (bulk copies, 2-stage ring); thread (tp, tq)
 // owns 8 P rows x 8 Q columns (pairs 2tp + 32i, 2tq + 32j: conflict-free LDS.128), so per
-// coordinate 8 LDS.128 feed 64 DFMA.  exp2 by range reduction and a degree-11 polynomial
-// (relative error < 1e-14).  Q columns past the split's range get z = 0 (the padding of z
+// coordinate 8 LDS.128 feed 64 DFMA.  Q columns past the split's range get z = 0 (the padding of z
 // is not guaranteed: pass B's z is pass A's output).
 // The per-row sums of the 16 tq threads are reduced in a fixed order (deterministic).
 constexpr int K64_T = 128;
-constexpr int K64_DMAX = 64;
+constexpr int K64_DMAX = 64;  // multiple of 4
+// exp2 in fp64 for t <= 0: range reduction t = n + f (|f| <= 1/2) and a degree-11 polynomial
+// for e^(f ln2) (remainder < 1e-14 relative), scaled by 2^n in the exponent field.  A 64-entry
+// shared-memory table with a degree-5 polynomial (10 instead of 17 fp64 operations) measured
+// slower (HIGGS / TAXI fp64 products -16 % / -21 %: the per-lane table lookups).
 __device__ __forceinline__ double exp2_f64(double t) {  // t <= 0
   t = fmax(t, -1070.0);
   const double n = (t + 6755399441055744.0) - 6755399441055744.0;  // rint (|t| < 2^51)
@@ -496,6 +499,7 @@ __device__ __forceinline__ double exp2_f64(double t) {  // t <= 0
   if (ni >= -1022) return p * __longlong_as_double((long long)(ni + 1023) << 52);
   return p * __longlong_as_double((long long)(ni + 1023 + 64) << 52) * 5.421010862427522e-20;  // 2^-64
 }
+
 __global__ void pack_rows64_tt_kernel(const float *__restrict__ in, int64_t rows, int64_t rows_pad,
                                       int64_t d, const double *__restrict__ mu, double g, int dq,
                                       double *__restrict__ out, double *__restrict__ bias) {
@@ -625,6 +629,120 @@ __global__ void __launch_bounds__(256, 1)
     for (int c = 0; c < 16; ++c) sum += red[c * K64_T + tid];
     const int64_t r = pt * K64_T + tid;
     if (r < np) out64[(int64_t)blockIdx.y * np + r] = sum;
+  }
+}
+
+// fp64 path, Gaussian, d <= 64: the cross term on the FP64 tensor pipe (DMMA m8n8k4), the exp2
+// and the contraction on the FP64 CUDA cores, so the two pipes work side by side.  Same
+// operands, shared-memory tiles and bulk-copy ring as kvp64t_kernel; warp w computes the
+// 32 x 64 block (P rows 32 (w & 3).., Q columns 64 (w >> 2)..) of a 128 x 128 tile as 4 x 8
+// m8n8 accumulators (fragment: row lane/4, columns 2 (lane % 4) + {0, 1}).  The per-row sums
+// are reduced over the 4 lanes of a row (shuffles) and the 2 warps of a row block (shared
+// memory), in a fixed order.
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(256, 1)
+    kvp64m_kernel(const double *__restrict__ P, const double *__restrict__ pa, int64_t np,
+                  const double *__restrict__ Q, const double *__restrict__ qb,
+                  const double *__restrict__ z, int64_t nq, int64_t q_per_split, int dq,
+                  double *__restrict__ out64) {
+  extern __shared__ __align__(128) double sm64m[];
+  const int TB = dq * K64_T;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm64m);  // P, Q stage 0, Q stage 1
+  double *sP = sm64m + 16, *sQ = sP + TB, *sB = sQ + 2 * TB, *sZ = sB + 2 * K64_T;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wp = warp & 3, wq = warp >> 2, g = lane >> 2, c = lane & 3;
+  const int64_t pt = blockIdx.x;
+  const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
+  const int64_t qhi = min(nq, qlo + q_per_split);
+  const int ntiles = qhi > qlo ? (int)cdiv<int64_t>(qhi - qlo, K64_T) : 0;
+  auto issue = [&](int t) {
+    const int64_t qt = (qlo + (int64_t)t * K64_T) / K64_T;
+    const int s = t & 1;
+    const uint32_t bt = (uint32_t)TB * 8, bv = K64_T * 8;
+    mbar_expect_tx(&bar[1 + s], bt + 2 * bv);
+    bulk_g2s(sQ + s * TB, Q + qt * TB, bt, &bar[1 + s]);
+    bulk_g2s(sZ + s * K64_T, z + qt * K64_T, bv, &bar[1 + s]);
+    bulk_g2s(sB + s * K64_T, qb + qt * K64_T, bv, &bar[1 + s]);
+  };
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_expect_tx(&bar[0], (uint32_t)TB * 8);
+    bulk_g2s(sP, P + pt * TB, (uint32_t)TB * 8, &bar[0]);
+    if (ntiles > 0) issue(0);
+    if (ntiles > 1) issue(1);
+  }
+  const int prow = 32 * wp + g;  // + 8 ti
+  double pav[4], part[4];
+#pragma unroll
+  for (int ti = 0; ti < 4; ++ti) {
+    pav[ti] = pa[pt * K64_T + prow + 8 * ti];  // biases are padded to the tile
+    part[ti] = 0.0;
+  }
+  mbar_wait(&bar[0], 0);
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t & 1;
+    mbar_wait(&bar[1 + s], (t >> 1) & 1);
+    const double *q = sQ + s * TB;
+    double acc[4][8][2];
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+      for (int tj = 0; tj < 8; ++tj) acc[ti][tj][0] = acc[ti][tj][1] = 0.0;
+    for (int k0 = 0; k0 < dq; k0 += 4) {
+      const double *pk = sP + (k0 + c) * K64_T + prow;
+      const double *qk = q + (k0 + c) * K64_T + 64 * wq + g;
+      double a[4], b[8];
+#pragma unroll
+      for (int ti = 0; ti < 4; ++ti) a[ti] = pk[8 * ti];
+#pragma unroll
+      for (int tj = 0; tj < 8; ++tj) b[tj] = qk[8 * tj];
+#pragma unroll
+      for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+        for (int tj = 0; tj < 8; ++tj) dmma884(acc[ti][tj], a[ti], b[tj]);
+    }
+    const int64_t qc0 = qlo + (int64_t)t * K64_T;
+#pragma unroll
+    for (int tj = 0; tj < 8; ++tj) {
+      const int col = 64 * wq + 8 * tj + 2 * c;
+      const double2 b2 = lds_d2(sB + s * K64_T + col);
+      double2 z2 = lds_d2(sZ + s * K64_T + col);
+      if (qc0 + col >= qhi) z2.x = 0.0;  // columns past the split's range contribute zero
+      if (qc0 + col + 1 >= qhi) z2.y = 0.0;
+#pragma unroll
+      for (int ti = 0; ti < 4; ++ti) {
+        const double k0 = exp2_f64(fmin(acc[ti][tj][0] + pav[ti] + b2.x, 0.0));
+        const double k1 = exp2_f64(fmin(acc[ti][tj][1] + pav[ti] + b2.y, 0.0));
+        part[ti] = fma(k0, z2.x, part[ti]);
+        part[ti] = fma(k1, z2.y, part[ti]);
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && t + 2 < ntiles) issue(t + 2);
+  }
+  // fixed-order reductions: the 4 lanes of a row (xor 1, 2), then the 2 column-half warps
+#pragma unroll
+  for (int ti = 0; ti < 4; ++ti) {
+    part[ti] += __shfl_xor_sync(0xffffffffu, part[ti], 1);
+    part[ti] += __shfl_xor_sync(0xffffffffu, part[ti], 2);
+  }
+  double *red = sP;  // [2][128]
+  if (c == 0) {
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti) red[wq * K64_T + prow + 8 * ti] = part[ti];
+  }
+  __syncthreads();
+  if (tid < K64_T) {
+    const int64_t r = pt * K64_T + tid;
+    if (r < np) out64[(int64_t)blockIdx.y * np + r] = red[tid] + red[K64_T + tid];
   }
 }
 
@@ -927,7 +1045,11 @@ static int kvp64_launch(falkon_ctx *ctx, int kernel, int dq, const double *P, co
   const bool resident = dq <= K64_DMAX;
   const int TQ = K64_T;
   const int threads = 256;
-  const void *fn = resident
+  // Gaussian, d <= 64: cross term on DMMA (FALKON_F64_DMMA=0 selects the all-DFMA kernel, A/B)
+  const char *dm = getenv("FALKON_F64_DMMA");
+  const bool dmma = kernel == FALKON_GAUSSIAN && resident && !(dm && atoi(dm) == 0);
+  const void *fn = dmma ? (const void *)kvp64m_kernel
+      : resident
       ? (kernel == FALKON_GAUSSIAN ? (const void *)kvp64t_kernel<FALKON_GAUSSIAN>
                                    : (const void *)kvp64t_kernel<FALKON_LAPLACIAN>)
       : (kernel == FALKON_GAUSSIAN ? (const void *)kvp64c_kernel<FALKON_GAUSSIAN>
@@ -982,7 +1104,7 @@ int prepare_operands(falkon_ctx *ctx, const float *X, int64_t n, int64_t d, cons
   FK_TRY(center_mean(ctx, C, m, d, &mu));
   if (ctx->opt.path == FALKON_PATH_F64) {  // fp64 coordinates and biases (tile-transposed)
     pp->path = FALKON_PATH_F64;
-    const int dq = (int)round_up<int64_t>(d, d <= K64_DMAX ? 2 : K64_KC);
+    const int dq = (int)round_up<int64_t>(d, d <= K64_DMAX ? 4 : K64_KC);  // DMMA k-steps of 4
     pp->dq = dq;
     const double g = kernel == FALKON_GAUSSIAN ? std::sqrt(LOG2E) / sigma : LOG2E / sigma;
     const int64_t n_pad = round_up<int64_t>(std::max<int64_t>(n, 1), 128);
