@@ -173,6 +173,8 @@ struct OzArgs {
   int rpa, rpb;           // rows per slice of the A / B slabs
   int nkb;                // K boxes
   int64_t ntiles;         // C tiles (tri_tiles: the lower ones, or all when tri_rect)
+  int diag;               // FALKON_OZ_DIAG (timing only, wrong results): 1 no C read-modify-
+                          // write, 2 no MMAs, 3 no TMA loads
   int tri_rect;           // tri_tiles on a tall region (N < M): rectangular order, upper tiles skipped
 };
 
@@ -253,10 +255,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         mbar_wait_safe(&empty[stage], phase ^ 1);
         if (elect_one()) {
           uint8_t *st = sm + stage * OZ_STAGE;
+          if (a.diag == 3) {
+            mbar_arrive(&full[stage]);
+          } else {
           mbar_expect_tx(&full[stage], OZ_STAGE);
           // one 3-D box (k, rows, slice) per operand: all OZ_S slices of the tile's rows
           tma_load_3d(st, &ta, kb * OZ_BK, ra, 0, &full[stage]);
           tma_load_3d(st + OZ_S * OZ_ASL, &tb, kb * OZ_BK, rb, 0, &full[stage]);
+          }
         }
         __syncwarp();
         if (++stage == OZ_STAGES) {
@@ -282,7 +288,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint64_t base = sw32_desc(smem_u32(sm + stage * OZ_STAGE));
-          for (int p = 0; p < OZ_S; ++p) {
+          for (int p = 0; p < (a.diag == 2 ? 0 : OZ_S); ++p) {
             const uint64_t ad = base + (uint64_t)((p * OZ_ASL) >> 4);
             for (int q = 0; q < OZ_S - p; ++q)  // the p = 0 pass opens every level
               tc_mma_i8(tmem + (uint32_t)((p + q) * OZ_BN), ad,
@@ -325,7 +331,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(tempty);  // TMEM free for the next tile's MMAs
-      if (gi < g.M) {
+      if (gi < g.M && a.diag != 1) {
         const int64_t r = g.rc + gi;
         const int er = a.ea[gi];
 #pragma unroll
@@ -434,6 +440,10 @@ static int oz_gemm_core(falkon_ctx *ctx, const GemmArgs &a) {
   oa.rpa = (int)rpa;
   oa.rpb = (int)rpb;
   oa.nkb = (int)(kpad / OZ_BK);
+  {
+    const char *e = getenv("FALKON_OZ_DIAG");
+    oa.diag = e ? atoi(e) : 0;
+  }
   FK_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM));
   const int64_t nti = cdiv<int64_t>(a.M, OZ_BM), ntj = cdiv<int64_t>(a.N, OZ_BN);
   oa.tri_rect = a.tri_tiles && a.N < a.M;
