@@ -13,6 +13,8 @@
 #   sanitize                   compute-sanitizer memcheck / racecheck / synccheck
 #   reference [CFG]            the oracle arm (bench.py --impl reference)
 #   probes                     L2 / HBM bandwidth and pipe-rate microbenchmarks
+#   evidence                   round-end bench lines (TIMIT headline + launch list, MSD, HIGGS, TAXI)
+#   ozaki [M ...]              preconditioner builds, Ozaki vs DMMA GEMMs (scripts/ozaki_probe.py)
 #   configscale                the -m gpu slow config-scale fit parity against tests/golden/fits
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"; mkdir -p gpurun_out
 task=$1; shift
@@ -70,6 +72,15 @@ probes)
   for p in l2_bw pipe_rates; do
     nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/$p scripts/probes/$p.cu && /tmp/$p | tee gpurun_out/probe_$p.txt
   done ;;
+evidence)  # round-end evidence: headline bench, launch list, per-config lines with fits, oracle arm
+  bash "$0" bench timit final > /dev/null; tail -c 400 gpurun_out/bench_timit_final.json; echo
+  bash "$0" launches timit final | tail -8
+  bash "$0" bench msd final > /dev/null
+  bash "$0" bench higgs final --steps 5 > /dev/null
+  bash "$0" bench taxi final --n 100000000 --steps 3 --fit-iters 7 > /dev/null
+  bash "$0" reference timit ;;
+ozaki)  # preconditioner build times and per-kernel device time, Ozaki vs DMMA GEMMs
+  OZ_KERNELS=1 timeout 900 python scripts/ozaki_probe.py ${1:-20000} ${2:-50000} | tee gpurun_out/ozaki_probe.jsonl ;;
 configscale)
   timeout 3000 python -m pytest tests/test_gpu_fit_configscale.py -m gpu -q -rA > gpurun_out/configscale.txt 2>&1
   tail -15 gpurun_out/configscale.txt ;;
