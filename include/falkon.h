@@ -79,7 +79,8 @@ enum {
   FALKON_OPT_EXP_OFFLOAD = 5,   /* tensor path: exp2 on the FMA pipe for 0 = none, 1 = all,
                                    2 = 1/4, 3 = 1/2 of the entries (rest on MUFU) */
   FALKON_OPT_POTRF_OUTER = 6,   /* blocked Cholesky: depth of the trailing fp64 GEMM updates in
-                                   units of 128 columns (1..64, default 8) */
+                                   units of 128 columns (1..64; 0 = auto (default): 16 with the
+                                   Ozaki GEMMs, 8 with the DMMA ones, as measured) */
   FALKON_OPT_GEMM_WARPS = 7,    /* fp64 DMMA GEMM CTA: 8 (128 x 128 tile, 8 warps), 16 (16 warps),
                                    2 (128 x 64 tiles, 2 CTAs of 8 warps per SM) or 5 (default:
                                    TMA-fed producer warp + 8 DMMA warps for the GEMMs whose A and B

@@ -601,7 +601,8 @@ int falkon_ctx_set_option(falkon_ctx *ctx, int option, int64_t value) {
       ctx->opt.gemm_warps = (int)value;
       return FALKON_OK;
     case FALKON_OPT_POTRF_OUTER:
-      if (value < 1 || value > 64) return fail(FALKON_EINVAL, "potrf outer block must be 1..64 x 128");
+      if (value < 0 || value > 64)
+        return fail(FALKON_EINVAL, "potrf outer block must be 1..64 x 128 (0 = auto)");
       ctx->opt.potrf_outer = (int)value;
       return FALKON_OK;
     case FALKON_OPT_SINGLE_EVAL:

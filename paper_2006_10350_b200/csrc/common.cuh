@@ -90,8 +90,9 @@ struct Options {
                         // A and B are the same view (trailing updates, LAUUM; measured m = 5e4
                         // 4.45 s, bitwise-identical factors), else 2; 2 = 128 x 64 tiles,
                         // 2 CTAs/SM (4.76 s); 8 = 128 x 128 tiles, 1 CTA/SM (4.96 s); 16 warps
-  int potrf_outer = 8;  // outer POTRF block in units of NB = 128 (trailing-update depth;
-                        // measured m = 5e4: 2 -> 5.46 s, 4 -> 5.21 s, 8 -> 5.10 s)
+  int potrf_outer = 0;  // outer POTRF block in units of NB = 128 (trailing-update depth);
+                        // 0 = auto: 16 with the Ozaki GEMMs (m = 5e4: 8 -> 3.00 s, 16 -> 2.88 s,
+                        // 32 -> 3.01 s), 8 with DMMA (2 -> 5.46 s, 4 -> 5.21 s, 8 -> 5.10 s)
   int lookahead = 1;    // blocked Cholesky: overlap the next panel with the trailing update
   int single_eval = 2;  // 0 two-pass, 1 single evaluation (k strip through HBM), 2 auto
   int tc_cluster = 2;   // tensor path: clusters of 2 CTAs multicasting the Q boxes (measured
@@ -138,6 +139,11 @@ struct falkon_ctx {
 };
 
 namespace falkon {
+
+// effective outer POTRF block (FALKON_OPT_POTRF_OUTER, 0 = auto)
+inline int potrf_outer(const falkon_ctx *ctx) {
+  return ctx->opt.potrf_outer > 0 ? ctx->opt.potrf_outer : (ctx->opt.ozaki ? 16 : 8);
+}
 
 // Grow-only workspace slot (contents undefined after growth).  Sizes are rounded up to
 // 256 B and a 256 B tail is always available so vector/bulk loads may overrun slightly.

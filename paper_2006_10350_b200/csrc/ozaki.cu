@@ -46,7 +46,11 @@ constexpr int OZ_S = OZ_S_OVR;     // slices per operand (7 bits each: 56-bit si
 constexpr int OZ_BM = 128;         // C tile rows (TMEM lanes)
 constexpr int OZ_BN = OZ_BN_OVR;         // C tile columns; 8 level accumulators x 64 = 512 TMEM columns
 constexpr int OZ_BK = 32;          // int8 per K box = one MMA's K (32 B rows, SWIZZLE_32B)
-constexpr int OZ_KMAX = 1024;      // 8 * 1024 * 127^2 < 2^31: level sums exact in int32
+#ifndef OZ_KMAX_OVR
+#define OZ_KMAX_OVR 4096
+#endif
+constexpr int OZ_KMAX = OZ_KMAX_OVR;  // 8 * K * 127^2 < 2^31 (K < 16,640): level sums exact in int32
+static_assert((int64_t)8 * OZ_KMAX * 127 * 127 < ((int64_t)1 << 31), "int32 level sums");
 constexpr int OZ_STAGES = 4;
 constexpr int64_t OZ_MIN_LD = 512;  // preconditioners of m < 512 stay on DMMA (launch-bound)
 constexpr int OZ_ASL = OZ_BM * OZ_BK;                   // 4 KB per A slice box

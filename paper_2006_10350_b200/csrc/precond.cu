@@ -854,7 +854,7 @@ static int potrf_lookahead(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, dou
     FK_CUDA(cudaStreamCreateWithPriority(&ctx->hi_stream, cudaStreamNonBlocking, greatest));
     FK_CUDA(cudaStreamCreateWithPriority(&ctx->lo_stream, cudaStreamNonBlocking, least));
   }
-  const int NBO = NB * ctx->opt.potrf_outer;
+  const int NBO = NB * potrf_outer(ctx);
   const int64_t nob = cdiv<int64_t>(m, NBO);
   std::vector<cudaEvent_t> ev((size_t)(2 * nob + 2));
   for (auto &e : ev) FK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -909,7 +909,7 @@ static int potrf(falkon_ctx *ctx, View S, int64_t m, double *Wbuf, double *Dinv,
   // then one trailing update of the remaining matrix with K = NBO (FALKON_OPT_POTRF_OUTER x 128;
   // fewer passes
   // over the trailing matrix and doubles the GEMM depth per tile).
-  const int NBO = NB * ctx->opt.potrf_outer;
+  const int NBO = NB * potrf_outer(ctx);
   if (ctx->opt.lookahead && m > 2 * (int64_t)NBO) return potrf_lookahead(ctx, S, m, Wbuf, Dinv, fail);
   for (int64_t K0 = 0; K0 < m; K0 += NBO) {
     const int64_t K1 = std::min<int64_t>(K0 + NBO, m);
@@ -1067,7 +1067,7 @@ static int potrf_dist(falkon_ctx *ctx, const DistBuild &D, int which, int64_t m,
   const size_t dsm = sizeof(double) * NB * (NB + 1);
   FK_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)dsm));
-  const int64_t NBO = (int64_t)NB * ctx->opt.potrf_outer;
+  const int64_t NBO = (int64_t)NB * potrf_outer(ctx);
   const int64_t nob = cdiv<int64_t>(m, NBO);
   auto view = [&](int i) {
     return which == 0 ? View{D.P[i], m, 1, 1, D.diagT[i]} : View{D.P[i], m, 0, 1, D.diagA[i]};
@@ -1093,7 +1093,7 @@ static int potrf_dist(falkon_ctx *ctx, const DistBuild &D, int which, int64_t m,
 // single-GPU call (panel starts are multiples of the 128-row GEMM tile).
 static int lauum_dist(falkon_ctx *ctx, const DistBuild &D, int64_t m, double lambda,
                       const double *dscale) {
-  const int64_t NBO = (int64_t)NB * ctx->opt.potrf_outer;
+  const int64_t NBO = (int64_t)NB * potrf_outer(ctx);
   const int64_t nob = cdiv<int64_t>(m, NBO);
   for (int i = 0; i < D.nranks_local(); ++i) {
     View L2{D.P[i], m, 0, 1, D.diagA[i]};
@@ -1246,7 +1246,7 @@ static int dist_for_ctx(falkon_ctx *ctx, int64_t m, double **P, double **dT, dou
   if (ctx->world > 1) {
     void *st;
     FK_TRY(ws_get(ctx, WS_DIST_STAGE,
-                  sizeof(double) * (size_t)m * NB * (size_t)ctx->opt.potrf_outer, &st));
+                  sizeof(double) * (size_t)m * NB * (size_t)potrf_outer(ctx), &st));
     D->stage = (double *)st;
   }
   return FALKON_OK;

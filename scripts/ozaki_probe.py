@@ -8,6 +8,8 @@ import synth
 from paper_2006_10350_b200 import binding
 
 ctx = binding.Context(0)
+if os.environ.get("POTRF_OUTER"):
+    ctx.set_option(binding.OPT_POTRF_OUTER, int(os.environ["POTRF_OUTER"]))
 for m in [int(x) for x in (sys.argv[1:] or ["20000", "50000"])]:
     cfg = synth.CONFIGS["higgs"]
     C = torch.from_numpy(synth.gen_X(cfg.seed, 0, m, cfg.d)).cuda()
