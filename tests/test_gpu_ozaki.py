@@ -131,3 +131,24 @@ def test_ozaki_weighted_lauum_gsc(oz, ctx):
     ao = gsc.gsc_falkon(X, y, C, yC, gsc.LOGISTIC, G, sigma, mus, its)
     assert rel_l2(host(a1), ao) <= 1e-3
     assert rel_l2(host(a1), host(a0)) <= 1e-9
+
+
+def test_ozaki_and_outer_block_options(ctx):
+    """FALKON_OPT_OZAKI takes 0 / 1; FALKON_OPT_POTRF_OUTER takes 0 (auto: 16 with Ozaki, 8 with
+    DMMA) .. 64; the auto and the explicit 16 build give bitwise-identical factors."""
+    from paper_2006_10350_b200 import FalkonError, binding
+    for bad in (-1, 2):
+        with pytest.raises(FalkonError):
+            ctx.set_option(binding.OPT_OZAKI, bad)
+    for bad in (-1, 65):
+        with pytest.raises(FalkonError):
+            ctx.set_option(binding.OPT_POTRF_OUTER, bad)
+    C = synth.gen_X(23, 0, 2600, 28)
+    try:
+        ctx.set_option(binding.OPT_POTRF_OUTER, 0)
+        T0, A0, _ = _build(ctx, C, 3.8)
+        ctx.set_option(binding.OPT_POTRF_OUTER, 16)
+        T1, A1, _ = _build(ctx, C, 3.8)
+    finally:
+        ctx.set_option(binding.OPT_POTRF_OUTER, 0)
+    assert np.array_equal(T0, T1) and np.array_equal(A0, A1)
