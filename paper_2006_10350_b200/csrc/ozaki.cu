@@ -192,11 +192,12 @@ __device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
   d |= (uint64_t)6 << 61;  // SWIZZLE_32B
   return d;
 }
-// tile t -> (ti, tj); false: a tile above the diagonal of a tall tri_tiles region (skipped by
-// every role alike, so the roles' tile sequences stay in step)
+// tile t -> (ti, tj) for row tiles of BM rows; false: a tile above the diagonal of a tall
+// tri_tiles region (skipped by every role alike, so the roles' tile sequences stay in step)
+template <int BM>
 __device__ __forceinline__ bool oz_tile(const OzArgs &a, int64_t t, int64_t &ti, int64_t &tj) {
-  constexpr int R = OZ_BM / OZ_BN;
-  if (a.g.tri_tiles && !a.tri_rect) {  // row tile ti holds 2 (ti + 1) column tiles of the lower region
+  constexpr int R = BM / OZ_BN;
+  if (a.g.tri_tiles && !a.tri_rect) {  // row tile ti holds R (ti + 1) column tiles of the lower region
     ti = (int64_t)((sqrt(8.0 * (double)t / R + 1.0) - 1.0) * 0.5);
     while (R * (ti + 1) * (ti + 2) / 2 <= t) ++ti;
     while (R * ti * (ti + 1) / 2 > t) --ti;
@@ -208,6 +209,22 @@ __device__ __forceinline__ bool oz_tile(const OzArgs &a, int64_t t, int64_t &ti,
   tj = t % ntj;
   return !(a.g.tri_tiles && tj >= R * (ti + 1));
 }
+__device__ __forceinline__ void tma_load_3d_pair(void *dst, const CUtensorMap *map, int c0, int c1,
+                                                 int c2, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(smem_u32(bar) & TC_PEER_MASK)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ double pow2(int e) {  // exact 2^e for normal e
   return __longlong_as_double((long long)(e + 1023) << 52);
 }
@@ -215,99 +232,132 @@ __device__ __forceinline__ double pow2(int e) {  // exact 2^e for normal e
 // Persistent: CTA c takes tiles c, c + grid, ...; the TMA ring runs on across tiles (the next
 // tile's boxes land while the epilogue drains), the epilogue releases TMEM right after its
 // tcgen05.ld's and then does the fp64 read-modify-write of C beside the next tile's MMAs.
+// PAIR: clusters of two CTAs run one tcgen05.mma.cta_group::2 of M = 256 (each CTA's 128 A rows)
+// x N = 64 (each CTA stages ITS 32-row half of the B slices): per CTA 40 KB per stage instead of
+// 48 KB and 5 KB of shared-memory operand reads per 128 x 64 x 32 product instead of 6 KB (the
+// two bounds of the single-CTA kernel).  The leader waits on its full barrier for both CTAs'
+// boxes, issues the MMAs and commits to both CTAs' empty / tfull barriers; both epilogues
+// release the accumulators on the leader's tempty.
+template <bool PAIR>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                    OzArgs a) {
+  constexpr int BMP = PAIR ? 2 * OZ_BM : OZ_BM;       // C rows per tile (pair)
+  constexpr int BROWS = PAIR ? OZ_BN / 2 : OZ_BN;     // B rows staged by this CTA
+  constexpr int BSL = BROWS * OZ_BK;
+  constexpr int STAGE = OZ_S * (OZ_ASL + BSL);
+  constexpr int NST = PAIR ? 5 : OZ_STAGES;
   extern __shared__ uint8_t oz_raw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) &
                                             ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(sm + OZ_STAGES * OZ_STAGE);
-  uint64_t *empty = full + OZ_STAGES, *tfull = empty + OZ_STAGES, *tempty = tfull + 1;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + NST * STAGE);
+  uint64_t *empty = full + NST, *tfull = empty + NST, *tempty = tfull + 1;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 1);
   const GemmArgs &g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t cid = PAIR ? blockIdx.x >> 1 : blockIdx.x;  // cluster (pair) id
+  const int64_t ncl = PAIR ? gridDim.x >> 1 : gridDim.x;
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < OZ_STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 32 * OZ_EPIW);
+    mbar_init(tempty, PAIR ? 2 * OZ_EPIW : OZ_EPIW);  // one arrival per epilogue warp
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tslot)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tslot)),
+                   "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tslot)),
+                   "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // the partner's barriers initialised before any remote arrival
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  const uint32_t crank = PAIR ? cluster_rank() : 0;
 
   if (warp == 0) {  // TMA producer
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    for (int64_t t = cid; t < a.ntiles; t += ncl) {
       int64_t ti, tj;
-      if (!oz_tile(a, t, ti, tj)) continue;
-      const int ra = (int)(ti * OZ_BM), rb = (int)(a.brow0 + tj * OZ_BN);
+      if (!oz_tile<BMP>(a, t, ti, tj)) continue;
+      const int ra = (int)(ti * BMP + OZ_BM * crank);
+      const int rb = (int)(a.brow0 + tj * OZ_BN + BROWS * crank);
       for (int kb = 0; kb < a.nkb; ++kb) {
         mbar_wait_safe(&empty[stage], phase ^ 1);
         if (elect_one()) {
-          uint8_t *st = sm + stage * OZ_STAGE;
-          if (a.diag == 3) {
+          uint8_t *st = sm + stage * STAGE;
+          if (!PAIR && a.diag == 3) {
             mbar_arrive(&full[stage]);
+          } else if (PAIR) {  // both CTAs' boxes complete on the leader's full barrier
+            if (crank == 0) mbar_expect_tx(&full[stage], 2 * STAGE);
+            tma_load_3d_pair(st, &ta, kb * OZ_BK, ra, 0, &full[stage]);
+            tma_load_3d_pair(st + OZ_S * OZ_ASL, &tb, kb * OZ_BK, rb, 0, &full[stage]);
           } else {
-          mbar_expect_tx(&full[stage], OZ_STAGE);
-          // one 3-D box (k, rows, slice) per operand: all OZ_S slices of the tile's rows
-          tma_load_3d(st, &ta, kb * OZ_BK, ra, 0, &full[stage]);
-          tma_load_3d(st + OZ_S * OZ_ASL, &tb, kb * OZ_BK, rb, 0, &full[stage]);
+            mbar_expect_tx(&full[stage], STAGE);
+            // one 3-D box (k, rows, slice) per operand: all OZ_S slices of the tile's rows
+            tma_load_3d(st, &ta, kb * OZ_BK, ra, 0, &full[stage]);
+            tma_load_3d(st + OZ_S * OZ_ASL, &tb, kb * OZ_BK, rb, 0, &full[stage]);
           }
         }
         __syncwarp();
-        if (++stage == OZ_STAGES) {
+        if (++stage == NST) {
           stage = 0;
           phase ^= 1;
         }
       }
     }
-  } else if (warp == 1) {  // MMA issuer: level L = p + q accumulates in TMEM columns [64 L, 64 L + 64)
-    // kind::i8 instruction descriptor: D s32 (bits 4-5 = 2), A and B signed (bits 7-9, 10-12 = 1),
-    // K-major, N >> 3 at bit 17, M >> 4 at bit 24
+  } else if (warp == 1 && crank == 0) {  // MMA issuer (the pair's leader): level L = p + q
+    // accumulates in TMEM columns [64 L, 64 L + 64).  kind::i8 instruction descriptor: D s32
+    // (bits 4-5 = 2), A and B signed (bits 7-9, 10-12 = 1), K-major, N >> 3 at 17, M >> 4 at 24
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
-                           ((uint32_t)(OZ_BM >> 4) << 24);
+                           ((uint32_t)(BMP >> 4) << 24);
     int stage = 0;
     uint32_t phase = 0, it = 0;
-    for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    for (int64_t t = cid; t < a.ntiles; t += ncl) {
       int64_t ti, tj;
-      if (!oz_tile(a, t, ti, tj)) continue;
+      if (!oz_tile<BMP>(a, t, ti, tj)) continue;
       mbar_wait_safe(tempty, (it & 1) ^ 1);  // the epilogue has read the previous tile
       tc_fence_after();
       for (int kb = 0; kb < a.nkb; ++kb) {
         mbar_wait_safe(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t base = sw32_desc(smem_u32(sm + stage * OZ_STAGE));
-          for (int p = 0; p < (a.diag == 2 ? 0 : OZ_S); ++p) {
+          const uint64_t base = sw32_desc(smem_u32(sm + stage * STAGE));
+          for (int p = 0; p < ((!PAIR && a.diag == 2) ? 0 : OZ_S); ++p) {
             const uint64_t ad = base + (uint64_t)((p * OZ_ASL) >> 4);
-            for (int q = 0; q < OZ_S - p; ++q)  // the p = 0 pass opens every level
-              tc_mma_i8(tmem + (uint32_t)((p + q) * OZ_BN), ad,
-                        base + (uint64_t)((OZ_S * OZ_ASL + q * OZ_BSL) >> 4), idesc,
-                        (kb | p) ? 1u : 0u);
+            for (int q = 0; q < OZ_S - p; ++q) {  // the p = 0 pass opens every level
+              const uint64_t bd = base + (uint64_t)((OZ_S * OZ_ASL + q * BSL) >> 4);
+              if (PAIR) tc_mma_i8_pair(tmem + (uint32_t)((p + q) * OZ_BN), ad, bd, idesc, (kb | p) ? 1u : 0u);
+              else tc_mma_i8(tmem + (uint32_t)((p + q) * OZ_BN), ad, bd, idesc, (kb | p) ? 1u : 0u);
+            }
           }
-          tc_commit(&empty[stage]);
+          if (PAIR) tc_commit_pair(&empty[stage]);
+          else tc_commit(&empty[stage]);
         }
         __syncwarp();
-        if (++stage == OZ_STAGES) {
+        if (++stage == NST) {
           stage = 0;
           phase ^= 1;
         }
       }
-      if (elect_one()) tc_commit(tfull);
+      if (elect_one()) {
+        if (PAIR) tc_commit_pair(tfull);
+        else tc_commit(tfull);
+      }
       __syncwarp();
       ++it;
     }
@@ -315,10 +365,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     const int lg = warp & 3, ch = (warp - 4) >> 2;
     const uint32_t tl = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(32 * ch);
     uint32_t it = 0;
-    for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    for (int64_t t = cid; t < a.ntiles; t += ncl) {
       int64_t ti, tj;
-      if (!oz_tile(a, t, ti, tj)) continue;
-      const int64_t gi = ti * OZ_BM + lg * 32 + lane, j0 = tj * OZ_BN + 32 * ch;
+      if (!oz_tile<BMP>(a, t, ti, tj)) continue;
+      const int64_t gi = ti * BMP + OZ_BM * crank + lg * 32 + lane, j0 = tj * OZ_BN + 32 * ch;
       mbar_wait_safe(tfull, it & 1);
       tc_fence_after();
       double sum[32];
@@ -334,7 +384,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         for (int c = 0; c < 32; ++c) sum[c] = fma((double)(int)r[c], sc, sum[c]);
       }
       tc_fence_before();
-      mbar_arrive(tempty);  // TMEM free for the next tile's MMAs
+      __syncwarp();
+      if (lane == 0) {  // TMEM free for the next tile's MMAs (PAIR: on the leader's barrier)
+        if (PAIR && crank != 0) mbar_arrive_cluster(tempty, 0);
+        else mbar_arrive(tempty);
+      }
       if (gi < g.M && a.diag != 1) {
         const int64_t r = g.rc + gi;
         const int er = a.ea[gi];
@@ -356,8 +410,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  if (PAIR) cluster_sync_all();  // the partner's last commits / arrivals into this CTA are done
+  if (warp == 2) {
+    tc_fence_after();
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
 }
 
 // ------------------------------------------------------------------ host
@@ -448,14 +508,38 @@ static int oz_gemm_core(falkon_ctx *ctx, const GemmArgs &a) {
     const char *e = getenv("FALKON_OZ_DIAG");
     oa.diag = e ? atoi(e) : 0;
   }
-  FK_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM));
-  const int64_t nti = cdiv<int64_t>(a.M, OZ_BM), ntj = cdiv<int64_t>(a.N, OZ_BN);
+  // CTA pairs (default; FALKON_OZ_PAIR=0 selects the single-CTA kernel, A/B): the B map then
+  // delivers 32-row halves
+  const char *pe = getenv("FALKON_OZ_PAIR");
+  const bool pair = !(pe && atoi(pe) == 0) && oa.diag == 0;
+  if (pair) FK_TRY(oz_map(&tb, sb, rpb, kpad, OZ_BN / 2));
+  const int bmp = pair ? 2 * OZ_BM : OZ_BM;
+  const int64_t nti = cdiv<int64_t>(a.M, bmp), ntj = cdiv<int64_t>(a.N, OZ_BN);
   oa.tri_rect = a.tri_tiles && a.N < a.M;
-  oa.ntiles = (a.tri_tiles && !oa.tri_rect) ? (OZ_BM / OZ_BN) * nti * (nti + 1) / 2 : nti * ntj;
-  const unsigned grid = (unsigned)std::min<int64_t>(oa.ntiles, ctx->sm_count);
-  {
+  oa.ntiles = (a.tri_tiles && !oa.tri_rect) ? (bmp / OZ_BN) * nti * (nti + 1) / 2 : nti * ntj;
+  if (pair) {
+    const int smem = 1024 + 5 * OZ_S * (OZ_ASL + OZ_BN / 2 * OZ_BK) + 256;
+    FK_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t clusters = std::min<int64_t>(oa.ntiles, ctx->sm_count / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * clusters));
+    cfg.blockDim = dim3(OZ_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
     LaunchScope ls(ctx, FALKON_T_PRECOND);
-    oz_gemm_kernel<<<grid, OZ_THREADS, OZ_SMEM, ctx->stream>>>(ta, tb, oa);
+    FK_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<true>, ta, tb, oa));
+  } else {
+    FK_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM));
+    const unsigned grid = (unsigned)std::min<int64_t>(oa.ntiles, ctx->sm_count);
+    LaunchScope ls(ctx, FALKON_T_PRECOND);
+    oz_gemm_kernel<false><<<grid, OZ_THREADS, OZ_SMEM, ctx->stream>>>(ta, tb, oa);
   }
   FK_LAUNCH_CHECK();
   return FALKON_OK;
