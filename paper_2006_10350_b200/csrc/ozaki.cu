@@ -12,18 +12,22 @@
 //   then  (A B^T)_ij = 2^(e_i + f_j) sum_{p,q} 2^(-7(p+q+2)) (Q^(p) Q'^(q)T)_ij,
 //
 // where each slice product is an int8 x int8 -> int32 MMA (tcgen05.mma kind::i8), exact while
-// K * 127^2 * (products per level) < 2^31 (K <= OZ_KMAX = 1024).  Products with p + q >= OZ_S
-// are dropped (each below 2^-70 K 127^2 of the scaled rows' product: the same order as the
-// fp64 GEMM's own rounding), leaving 36 slice products in 8 levels L = p + q; the levels are
-// summed in int32 inside TMEM (8 accumulators of 128 x 64) and combined once per tile in fp64,
-// smallest level first.  The result is deterministic (integer sums; fixed combination order),
-// but not bitwise equal to the DMMA GEMM (different rounding): factors agree to ~1e-15
-// relative (tests/test_gpu_ozaki.py).
+// K * 127^2 * (products per level) < 2^31 (K <= OZ_KMAX = 4096 per call; LAUUM in k chunks of
+// 4096 at absolute boundaries).  Products with p + q >= OZ_S are dropped (each below
+// 2^-70 K 127^2 of the scaled rows' product: the order of the fp64 GEMM's own rounding),
+// leaving 36 slice products in 8 levels L = p + q; the levels are summed in int32 inside TMEM
+// (8 accumulators of 128 x 64 per CTA) and combined once per tile in fp64, smallest level first.
+// The result is deterministic (integer sums; fixed combination order) and independent of the
+// call's row range (the distributed schedule reproduces the single-GPU factors bitwise), but
+// not bitwise equal to the DMMA GEMM: factors agree to ~1e-13 relative (tests/test_gpu_ozaki.py).
 //
-// Kernel: one 128 x 64 C tile per CTA, K streamed in boxes of 64 int8 (SWIZZLE_64B) through a
-// 2-stage TMA ring of 96 KB stages (8 A slices of 128 x 64 + 8 B slices of 64 x 64): warp 0 TMA
-// producer, warp 1 MMA issuer (72 MMAs of 128 x 64 x 32 per stage), warp 2 TMEM allocator,
-// warps 4-7 the epilogue (thread = TMEM lane = C row).
+// Kernel (default): persistent 2-CTA clusters, one 256 x 64 C tile per pair as
+// tcgen05.mma.cta_group::2 (M = 256, N = 64, K = 32); each CTA stages its 128 A rows and a
+// 32-row half of the B slices (one 3-D TMA box per operand: k, rows, 8 slices; 32-byte rows,
+// SWIZZLE_32B) through a 5-stage ring of 40 KB; warp 0 TMA producer, warp 1 of the leader the
+// MMA issuer (36 MMAs per stage), warp 2 TMEM allocator, warps 4-11 the epilogue (thread = TMEM
+// lane = C row, 32 of the tile's columns), which releases TMEM before its fp64 read-modify-write
+// of C.  FALKON_OZ_PAIR=0 selects the single-CTA kernel (128 x 64 tiles, 4 x 48 KB stages).
 #include <math.h>
 
 #include <algorithm>
