@@ -396,8 +396,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       if (gi < g.M && a.diag != 1) {
         const int64_t r = g.rc + gi;
         const int er = a.ea[gi];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {  // unrolled: sum[] stays in registers
+        auto put = [&](int c) {  // one element through the view (masks, diagonal vector)
           const int64_t gj = j0 + c;
           const int64_t cc = g.cc + gj;
           const bool ok = gj < g.N && !(g.C.tri == 1 && r < cc) && !(g.C.tri == 2 && cc < r);
@@ -407,6 +406,39 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             const double cv = g.beta != 0.0 ? g.beta * vget(g.C, r, cc) : 0.0;
             vset(g.C, r, cc, g.alpha * ab + cv);
           }
+        };
+        // row-major C (trans = 0: the A factor, the LAUUM): a thread's 32 columns are
+        // contiguous, so pairs strictly inside the stored part go as one 16-byte access
+        // (half the L2 transactions of the lane-strided pattern); the rest element-wise
+        const bool vec = !g.C.trans && g.C.tri != 2 && ((r * g.C.ld + g.cc + j0) & 1) == 0;
+        if (vec) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const int64_t gj = j0 + c, cc = g.cc + gj;
+            if (gj + 1 < g.N && (g.C.tri != 1 || r > cc + 1)) {
+              const int e0 = er + a.eb[a.brow0 + gj], e1 = er + a.eb[a.brow0 + gj + 1];
+              const double ab0 = (e0 > -1000 && e0 < 1000) ? sum[c] * pow2(e0) : ldexp(sum[c], e0);
+              const double ab1 =
+                  (e1 > -1000 && e1 < 1000) ? sum[c + 1] * pow2(e1) : ldexp(sum[c + 1], e1);
+              double2 *p = reinterpret_cast<double2 *>(g.C.base + r * g.C.ld + cc);
+              double2 o;
+              if (g.beta != 0.0) {
+                const double2 cv = *p;
+                o.x = g.alpha * ab0 + g.beta * cv.x;
+                o.y = g.alpha * ab1 + g.beta * cv.y;
+              } else {
+                o.x = g.alpha * ab0;
+                o.y = g.alpha * ab1;
+              }
+              *p = o;
+            } else {
+              put(c);
+              put(c + 1);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) put(c);  // unrolled: sum[] stays in registers
         }
       }
       ++it;
@@ -515,7 +547,7 @@ static int oz_gemm_core(falkon_ctx *ctx, const GemmArgs &a) {
   // CTA pairs (default; FALKON_OZ_PAIR=0 selects the single-CTA kernel, A/B): the B map then
   // delivers 32-row halves
   const char *pe = getenv("FALKON_OZ_PAIR");
-  const bool pair = !(pe && atoi(pe) == 0) && oa.diag == 0;
+  const bool pair = !(pe && atoi(pe) == 0) && oa.diag <= 1;
   if (pair) FK_TRY(oz_map(&tb, sb, rpb, kpad, OZ_BN / 2));
   const int bmp = pair ? 2 * OZ_BM : OZ_BM;
   const int64_t nti = cdiv<int64_t>(a.M, bmp), ntj = cdiv<int64_t>(a.N, OZ_BN);
