@@ -55,6 +55,7 @@ constexpr int OZ_BK = 32;          // int8 per K box = one MMA's K (32 B rows, S
 #endif
 constexpr int OZ_KMAX = OZ_KMAX_OVR;  // 8 * K * 127^2 < 2^31 (K < 16,640): level sums exact in int32
 static_assert((int64_t)8 * OZ_KMAX * 127 * 127 < ((int64_t)1 << 31), "int32 level sums");
+static_assert(OZ_S == 8, "the pack's one-conversion split assumes 8 slices of 7 bits (56 bits)");
 constexpr int OZ_STAGES = 4;
 constexpr int64_t OZ_MIN_LD = 512;  // preconditioners of m < 512 stay on DMMA (launch-bound)
 constexpr int OZ_ASL = OZ_BM * OZ_BK;                   // 4 KB per A slice box
@@ -123,13 +124,16 @@ __global__ void __launch_bounds__(256) oz_pack_kernel(View V, int64_t r0, int64_
     for (int p = 0; p < OZ_S; ++p) w[p] = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      double y = t[pr][pk + u] * sc;  // |y| < 1, exact
+      // the 56-bit truncation toward zero of y in one conversion; slice p = base-128 digit p of
+      // |Y| with the sign of y (the same digits as repeated y *= 128, q = trunc(y), y -= q)
+      const double y = t[pr][pk + u] * sc;                             // |y| < 1, exact
+      const long long Y = __double2ll_rz(y * 72057594037927936.0);     // 2^56 y, exact scale
+      const unsigned long long A = Y < 0 ? (unsigned long long)(-Y) : (unsigned long long)Y;
 #pragma unroll
       for (int p = 0; p < OZ_S; ++p) {
-        y *= 128.0;                 // exact
-        const double q = trunc(y);  // |q| <= 127
-        y -= q;                     // exact
-        w[p] |= (uint32_t)(uint8_t)(int8_t)(int)q << (8 * u);
+        int q = (int)((A >> (7 * (OZ_S - 1 - p))) & 127u);
+        if (Y < 0) q = -q;
+        w[p] |= (uint32_t)(uint8_t)(int8_t)q << (8 * u);
       }
     }
     const int64_t row = rb + pr;
