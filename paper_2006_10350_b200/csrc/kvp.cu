@@ -475,29 +475,30 @@ __global__ void __launch_bounds__(KVP_THREADS)
 // The per-row sums of the 16 tq threads are reduced in a fixed order (deterministic).
 constexpr int K64_T = 128;
 constexpr int K64_DMAX = 64;  // multiple of 4
-// exp2 in fp64 for t <= 0: range reduction t = n + f (|f| <= 1/2) and a degree-11 polynomial
-// for e^(f ln2) (remainder < 1e-14 relative), scaled by 2^n in the exponent field.  A 64-entry
-// shared-memory table with a degree-5 polynomial (10 instead of 17 fp64 operations) measured
-// slower (HIGGS / TAXI fp64 products -16 % / -21 %: the per-lane table lookups).
+// exp2 in fp64 for t <= 0: range reduction t = n + f (|f| <= 1/2, n by the 1.5 * 2^52 rounding
+// trick, which also leaves n in the low word), a degree-11 polynomial for 2^f in f itself
+// (coefficients (ln 2)^k / k!: remainder < 1e-14 relative), and 2^n added to the exponent field
+// with an integer add (no conversions, no final multiply: 14 fp64 operations).  t is clamped at
+// -1000 (2^-1000 ~ 1e-301: below any contribution).  A 64-entry shared-memory table with a
+// degree-5 polynomial measured slower (HIGGS / TAXI fp64 products -16 % / -21 %).
 __device__ __forceinline__ double exp2_f64(double t) {  // t <= 0
-  t = fmax(t, -1070.0);
-  const double n = (t + 6755399441055744.0) - 6755399441055744.0;  // rint (|t| < 2^51)
-  const double y = (t - n) * 0.6931471805599453;                    // |y| <= 0.347
-  double p = 2.505210838544172e-08;                                 // 1/11!
-  p = fma(p, y, 2.755731922398589e-07);
-  p = fma(p, y, 2.7557319223985893e-06);
-  p = fma(p, y, 2.48015873015873e-05);
-  p = fma(p, y, 1.984126984126984e-04);
-  p = fma(p, y, 1.388888888888889e-03);
-  p = fma(p, y, 8.333333333333333e-03);
-  p = fma(p, y, 4.1666666666666664e-02);
-  p = fma(p, y, 0.16666666666666666);
-  p = fma(p, y, 0.5);
-  p = fma(p, y, 1.0);
-  p = fma(p, y, 1.0);
-  const int ni = (int)n;  // in [-1070, 0]
-  if (ni >= -1022) return p * __longlong_as_double((long long)(ni + 1023) << 52);
-  return p * __longlong_as_double((long long)(ni + 1023 + 64) << 52) * 5.421010862427522e-20;  // 2^-64
+  t = fmax(t, -1000.0);
+  const double u = t + 6755399441055744.0;  // 1.5 * 2^52 + rint(t)
+  const int ni = __double2loint(u);         // rint(t), two's complement
+  const double f = t - (u - 6755399441055744.0);
+  double p = 4.44553827187081e-10;  // (ln 2)^11 / 11!
+  p = fma(p, f, 7.054911620801121e-09);
+  p = fma(p, f, 1.0178086009239696e-07);
+  p = fma(p, f, 1.3215486790144305e-06);
+  p = fma(p, f, 1.5252733804059838e-05);
+  p = fma(p, f, 0.00015403530393381606);
+  p = fma(p, f, 0.0013333558146428441);
+  p = fma(p, f, 0.009618129107628477);
+  p = fma(p, f, 0.055504108664821576);
+  p = fma(p, f, 0.2402265069591007);
+  p = fma(p, f, 0.6931471805599453);
+  p = fma(p, f, 1.0);  // in [0.70, 1.42]
+  return __hiloint2double(__double2hiint(p) + (ni << 20), __double2loint(p));
 }
 
 __global__ void pack_rows64_tt_kernel(const float *__restrict__ in, int64_t rows, int64_t rows_pad,
@@ -691,11 +692,16 @@ __global__ void __launch_bounds__(256, 1)
     const int s = t & 1;
     mbar_wait(&bar[1 + s], (t >> 1) & 1);
     const double *q = sQ + s * TB;
-    double acc[4][8][2];
+    double acc[4][8][2];  // the DMMAs accumulate onto the biases a_p + b_q
 #pragma unroll
-    for (int ti = 0; ti < 4; ++ti)
+    for (int tj = 0; tj < 8; ++tj) {
+      const double2 b2 = lds_d2(sB + s * K64_T + 64 * wq + 8 * tj + 2 * c);
 #pragma unroll
-      for (int tj = 0; tj < 8; ++tj) acc[ti][tj][0] = acc[ti][tj][1] = 0.0;
+      for (int ti = 0; ti < 4; ++ti) {
+        acc[ti][tj][0] = pav[ti] + b2.x;
+        acc[ti][tj][1] = pav[ti] + b2.y;
+      }
+    }
     for (int k0 = 0; k0 < dq; k0 += 4) {
       const double *pk = sP + (k0 + c) * K64_T + prow;
       const double *qk = q + (k0 + c) * K64_T + 64 * wq + g;
@@ -713,14 +719,13 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
     for (int tj = 0; tj < 8; ++tj) {
       const int col = 64 * wq + 8 * tj + 2 * c;
-      const double2 b2 = lds_d2(sB + s * K64_T + col);
       double2 z2 = lds_d2(sZ + s * K64_T + col);
       if (qc0 + col >= qhi) z2.x = 0.0;  // columns past the split's range contribute zero
       if (qc0 + col + 1 >= qhi) z2.y = 0.0;
 #pragma unroll
       for (int ti = 0; ti < 4; ++ti) {
-        const double k0 = exp2_f64(fmin(acc[ti][tj][0] + pav[ti] + b2.x, 0.0));
-        const double k1 = exp2_f64(fmin(acc[ti][tj][1] + pav[ti] + b2.y, 0.0));
+        const double k0 = exp2_f64(fmin(acc[ti][tj][0], 0.0));
+        const double k1 = exp2_f64(fmin(acc[ti][tj][1], 0.0));
         part[ti] = fma(k0, z2.x, part[ti]);
         part[ti] = fma(k1, z2.y, part[ti]);
       }
