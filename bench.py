@@ -543,6 +543,9 @@ def main():
             fit = {"seconds": wall, "iters": iters, "t_precond_s": info["t_precond_s"],
                    "t_rhs_s": info["t_rhs_s"], "t_cg_s": info["t_cg_s"],
                    "iters_run": info["iters_run"],
+                   # product kernels the fit ran on (readings d3 / d4)
+                   "product_path": {1: "simt", 2: "tensor", 3: "f64"}.get(info.get("product_path"),
+                                                                           info.get("product_path")),
                    "paper_context": PAPER_FIT.get(cfg.name)}
         except Exception as ex:  # report, do not hide
             fit = {"error": str(ex)}
