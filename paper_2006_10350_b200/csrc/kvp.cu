@@ -645,7 +645,9 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
-__global__ void __launch_bounds__(256, 1)
+// NWQ warps split a row block's 128 columns (2: 8 warps of 32 x 64; 4: 16 warps of 32 x 32)
+template <int NWQ>
+__global__ void __launch_bounds__(128 * NWQ, 1)
     kvp64m_kernel(const double *__restrict__ P, const double *__restrict__ pa, int64_t np,
                   const double *__restrict__ Q, const double *__restrict__ qb,
                   const double *__restrict__ z, int64_t nq, int64_t q_per_split, int dq,
@@ -655,6 +657,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t *bar = reinterpret_cast<uint64_t *>(sm64m);  // P, Q stage 0, Q stage 1
   double *sP = sm64m + 16, *sQ = sP + TB, *sB = sQ + 2 * TB, *sZ = sB + 2 * K64_T;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int TJ = 16 / NWQ, WC = 128 / NWQ;  // 8-column tiles and columns per warp
   const int wp = warp & 3, wq = warp >> 2, g = lane >> 2, c = lane & 3;
   const int64_t pt = blockIdx.x;
   const int64_t qlo = (int64_t)blockIdx.y * q_per_split;
@@ -692,10 +695,10 @@ __global__ void __launch_bounds__(256, 1)
     const int s = t & 1;
     mbar_wait(&bar[1 + s], (t >> 1) & 1);
     const double *q = sQ + s * TB;
-    double acc[4][8][2];  // the DMMAs accumulate onto the biases a_p + b_q
+    double acc[4][TJ][2];  // the DMMAs accumulate onto the biases a_p + b_q
 #pragma unroll
-    for (int tj = 0; tj < 8; ++tj) {
-      const double2 b2 = lds_d2(sB + s * K64_T + 64 * wq + 8 * tj + 2 * c);
+    for (int tj = 0; tj < TJ; ++tj) {
+      const double2 b2 = lds_d2(sB + s * K64_T + WC * wq + 8 * tj + 2 * c);
 #pragma unroll
       for (int ti = 0; ti < 4; ++ti) {
         acc[ti][tj][0] = pav[ti] + b2.x;
@@ -704,21 +707,21 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int k0 = 0; k0 < dq; k0 += 4) {
       const double *pk = sP + (k0 + c) * K64_T + prow;
-      const double *qk = q + (k0 + c) * K64_T + 64 * wq + g;
-      double a[4], b[8];
+      const double *qk = q + (k0 + c) * K64_T + WC * wq + g;
+      double a[4], b[TJ];
 #pragma unroll
       for (int ti = 0; ti < 4; ++ti) a[ti] = pk[8 * ti];
 #pragma unroll
-      for (int tj = 0; tj < 8; ++tj) b[tj] = qk[8 * tj];
+      for (int tj = 0; tj < TJ; ++tj) b[tj] = qk[8 * tj];
 #pragma unroll
       for (int ti = 0; ti < 4; ++ti)
 #pragma unroll
-        for (int tj = 0; tj < 8; ++tj) dmma884(acc[ti][tj], a[ti], b[tj]);
+        for (int tj = 0; tj < TJ; ++tj) dmma884(acc[ti][tj], a[ti], b[tj]);
     }
     const int64_t qc0 = qlo + (int64_t)t * K64_T;
 #pragma unroll
-    for (int tj = 0; tj < 8; ++tj) {
-      const int col = 64 * wq + 8 * tj + 2 * c;
+    for (int tj = 0; tj < TJ; ++tj) {
+      const int col = WC * wq + 8 * tj + 2 * c;
       double2 z2 = lds_d2(sZ + s * K64_T + col);
       if (qc0 + col >= qhi) z2.x = 0.0;  // columns past the split's range contribute zero
       if (qc0 + col + 1 >= qhi) z2.y = 0.0;
@@ -733,13 +736,13 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     if (tid == 0 && t + 2 < ntiles) issue(t + 2);
   }
-  // fixed-order reductions: the 4 lanes of a row (xor 1, 2), then the 2 column-half warps
+  // fixed-order reductions: the 4 lanes of a row (xor 1, 2), then the NWQ column-block warps
 #pragma unroll
   for (int ti = 0; ti < 4; ++ti) {
     part[ti] += __shfl_xor_sync(0xffffffffu, part[ti], 1);
     part[ti] += __shfl_xor_sync(0xffffffffu, part[ti], 2);
   }
-  double *red = sP;  // [2][128]
+  double *red = sP;  // [NWQ][128]
   if (c == 0) {
 #pragma unroll
     for (int ti = 0; ti < 4; ++ti) red[wq * K64_T + prow + 8 * ti] = part[ti];
@@ -747,7 +750,10 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (tid < K64_T) {
     const int64_t r = pt * K64_T + tid;
-    if (r < np) out64[(int64_t)blockIdx.y * np + r] = red[tid] + red[K64_T + tid];
+    double sum = red[tid];
+#pragma unroll
+    for (int w = 1; w < NWQ; ++w) sum += red[w * K64_T + tid];
+    if (r < np) out64[(int64_t)blockIdx.y * np + r] = sum;
   }
 }
 
@@ -1049,11 +1055,14 @@ static int kvp64_launch(falkon_ctx *ctx, int kernel, int dq, const double *P, co
   // in chunks of K64_KC coordinates (dq a multiple of K64_KC, see prepare_operands)
   const bool resident = dq <= K64_DMAX;
   const int TQ = K64_T;
-  const int threads = 256;
   // Gaussian, d <= 64: cross term on DMMA (FALKON_F64_DMMA=0 selects the all-DFMA kernel, A/B)
   const char *dm = getenv("FALKON_F64_DMMA");
   const bool dmma = kernel == FALKON_GAUSSIAN && resident && !(dm && atoi(dm) == 0);
-  const void *fn = dmma ? (const void *)kvp64m_kernel
+  // FALKON_F64_NWQ=2 (A/B): 8 warps of 32 x 64 instead of 16 of 32 x 32
+  const char *nw = getenv("FALKON_F64_NWQ");
+  const bool w16 = !(nw && atoi(nw) == 2);
+  const int threads = (dmma && w16) ? 512 : 256;
+  const void *fn = dmma ? (w16 ? (const void *)kvp64m_kernel<4> : (const void *)kvp64m_kernel<2>)
       : resident
       ? (kernel == FALKON_GAUSSIAN ? (const void *)kvp64t_kernel<FALKON_GAUSSIAN>
                                    : (const void *)kvp64t_kernel<FALKON_LAPLACIAN>)
